@@ -1,0 +1,112 @@
+"""CPU oracle for arXiv 1812.02056 Algorithms 1-3 — TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg and
+``--impl reference``) may import this package.  It shares no code with the CUDA product
+path in ``paper_1812_02056_b200/`` and never imports it.
+
+The arithmetic lives in ``stepfact_oracle.c`` (plain C, fp64, ``-ffp-contract=off``); this
+module only compiles it, loads it with ctypes and marshals numpy arrays.  Matrices are
+numpy arrays indexed ``A[i, j]`` as in the paper; they are handed to C in column-major
+(Fortran) order.
+
+Pins (tests/test_oracle.py): s=1 and s=n degeneracy bitwise against
+independent textbook routines, hand-worked examples (tests/golden/), planted integer
+factors (exact), LAPACK cross-checks, invariants, restricted-column bitwise equality.
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_DIR = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_DIR, "stepfact_oracle.c")
+_LIB = os.path.join(_DIR, "liboracle.so")
+_lib = None
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-std=c11"]
+
+
+def build(force=False):
+    """Compile liboracle.so in-tree (gcc).  Building the checker is not using it."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        i64, dbl, p = ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+        lib.orc_chol.restype = i64
+        lib.orc_chol.argtypes = [i64, i64, i64, p, i64, p, i64]
+        lib.orc_lu.restype = i64
+        lib.orc_lu.argtypes = [i64, i64, i64, p, i64, p, i64, p, i64, dbl]
+        lib.orc_qr.restype = i64
+        lib.orc_qr.argtypes = [i64, i64, i64, p, i64, p, i64, p, i64, dbl, ctypes.POINTER(dbl)]
+        lib.orc_flush_count.restype = i64
+        lib.orc_flush_count.argtypes = [i64, i64]
+        lib.orc_frobenius.restype = dbl
+        lib.orc_frobenius.argtypes = [i64, p, i64]
+        lib.orc_set_threads.argtypes = [ctypes.c_int]
+        lib.orc_max_threads.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _colmajor(A):
+    A = np.asarray(A, dtype=np.float64)
+    assert A.ndim == 2 and A.shape[0] == A.shape[1], "square matrix expected"
+    return np.asfortranarray(A)
+
+
+def _check_s(n, s):
+    if not (1 <= s <= n):
+        raise ValueError(f"step s={s} outside [1, n={n}]")
+
+
+def set_threads(n):
+    _load().orc_set_threads(int(n))
+
+
+def max_threads():
+    return int(_load().orc_max_threads())
+
+
+def flush_count(n, s):
+    """Flushes performed by the c = z+s schedule."""
+    return int(_load().orc_flush_count(n, s))
+
+
+def chol(A, s, kcols=None):
+    """Algorithm 1. Returns (L, info); info 0 or 1-based failing column."""
+    A = _colmajor(A); n = A.shape[0]; _check_s(n, s)
+    L = np.zeros((n, n), order="F")
+    info = _load().orc_chol(n, s, n if kcols is None else kcols, A.ctypes.data, n, L.ctypes.data, n)
+    return L, int(info)
+
+
+def lu(A, s, kcols=None, tol=0.0):
+    """Algorithm 2, Crout form (U unit upper). Returns (L, U, info)."""
+    A = _colmajor(A); n = A.shape[0]; _check_s(n, s)
+    L = np.zeros((n, n), order="F"); U = np.zeros((n, n), order="F")
+    info = _load().orc_lu(n, s, n if kcols is None else kcols, A.ctypes.data, n,
+                          L.ctypes.data, n, U.ctypes.data, n, float(tol))
+    return L, U, int(info)
+
+
+def qr(A, s, kcols=None, tol=0.0):
+    """Algorithm 3. Returns (Q, R, info, lower_mass)."""
+    A = _colmajor(A); n = A.shape[0]; _check_s(n, s)
+    Q = np.zeros((n, n), order="F"); R = np.zeros((n, n), order="F")
+    mass = ctypes.c_double(0.0)
+    info = _load().orc_qr(n, s, n if kcols is None else kcols, A.ctypes.data, n,
+                          Q.ctypes.data, n, R.ctypes.data, n, float(tol), ctypes.byref(mass))
+    return Q, R, int(info), float(mass.value)
+
+
+def frobenius(A):
+    A = _colmajor(A)
+    return float(_load().orc_frobenius(A.shape[0], A.ctypes.data, A.shape[0]))
