@@ -1,0 +1,128 @@
+/*
+ * stepfact.h — C ABI of libstepfact, a B200 (sm_100a) implementation of the step-s
+ * Cholesky / LU / QR algorithms of C. Camarero, arXiv 1812.02056 ("the paper";
+ * PAPER.md:<line> cites /root/reference/PAPER.md).
+ *
+ * Problem statement: given A, find triangular L (and U) with A = L L^T /
+ * A = L U, or orthogonal Q and upper triangular R with A = Q R.  The step size s
+ * is the number of columns factored between two trailing updates
+ * ("flushes"): a flush fires when c = z + s and subtracts ONE
+ * rectangular product from the trailing matrix.
+ *
+ * Conventions for every entry point
+ *   - Matrices are column-major: element (i,j) of an n x n matrix X with leading
+ *     dimension ldx >= n lives at X[i + j*ldx] (0-based i, j).  Pointers to device memory
+ *     are prefixed d, host memory h.  The caller owns every matrix and the info word; the
+ *     library owns only temporary workspace, taken from the CUDA stream-ordered allocator
+ *     on `stream` and released before the call's work completes.
+ *   - Device entry points are asynchronous and stream-ordered on `stream` (a
+ *     cudaStream_t; NULL = the legacy default stream).  They never synchronize.
+ *   - Numerical failure is NOT a return code: it is written, stream-ordered, to the device
+ *     int64 *d_info: 0 = success, k >= 1 = the first (1-based) column
+ *     at which the algorithm could not continue (see each function).  Columns >= k of the
+ *     outputs are then unspecified (LAPACK/cuSOLVER devInfo semantics).
+ *   - Return codes (sf_status) report argument / resource / launch errors, synchronously;
+ *     on SF_EINVAL nothing has been enqueued.  sf_last_error() gives a one-line detail.
+ *   - dtype: SF_F64 (double storage and arithmetic; the update runs on the FP64 tensor
+ *     cores, DMMA) or SF_F32 (float storage; see each function).
+ *   - Alignment: any; 16-byte aligned pointers with even ld take the vectorised path.
+ */
+#ifndef STEPFACT_H
+#define STEPFACT_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum sf_dtype { SF_F64 = 0, SF_F32 = 1 };
+enum sf_status { SF_OK = 0, SF_EINVAL = 1, SF_ENOTSUP = 2, SF_ENOMEM = 3, SF_ECUDA = 4, SF_ENCCL = 5 };
+
+/* Algorithm 1, "A fast Cholesky decomposition algorithm".
+ *   n      order of A, n >= 1
+ *   s      step size, 1 <= s <= n
+ *   dA     n x n symmetric positive definite input, leading dimension lda >= n; ONLY its
+ *          lower triangle (incl. diagonal) is read.  Read-only unless dA == dL.
+ *   dL     n x n output, leading dimension ldl >= n: the lower triangle (incl. diagonal)
+ *          receives L with A = L L^T and L_cc > 0; the strict upper triangle of dL is
+ *          never written (so dA == dL factors in place, "could be done in
+ *          place of A").  dL may alias dA only exactly (dA == dL, lda == ldl).
+ *   d_info device int64: 0, or k if the value under the square root at column k
+ *           was <= 0 or NaN.
+ * Per panel p (columns [p*s, min((p+1)*s, n))): panel recurrences PAPER.md:53-67, then, if a
+ * later panel exists, the flush A[c:n,c:n] -= R R^T with R = L[c:n, z:c),
+ * lower triangle only (Alg. 1 never reads the upper part of A). */
+int chol_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dL, int64_t ldl,
+                int64_t* d_info, void* stream);
+
+/* Algorithm 2, "A fast LU decomposition algorithm", no pivoting, Crout
+ * normalisation: L lower triangular with its own diagonal, U unit upper triangular
+ * (U_cc = L_cc / L_cc = 1 exactly).
+ *   dA     n x n input with nonzero leading principal minors, read-only
+ *          unless dA == dLU.
+ *   dLU    n x n output: lower triangle incl. diagonal = L, strict upper triangle = U
+ *          (the unit diagonal of U is implicit, not stored).  dLU == dA factors in place.
+ *   d_info 0, or k if |L_kk| < 1e-12 * ||A||_F / n (||A||_F of the input; R3).
+ * Flush: A[c:n,c:n] -= R_L R_U, R_L = L[c:n, z:c), R_U = U[z:c, c:n). */
+int lu_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dLU, int64_t ldlu,
+              int64_t* d_info, void* stream);
+
+/* Algorithm 3, "A fast QR decomposition algorithm", modified
+ * Gram-Schmidt inside the panel, block projection at each flush.
+ *   dA     n x n input of full rank, read-only (it is needed again for R := Q^T A, :170)
+ *   dQ     n x n output, orthonormal columns; also used as the working matrix M
+ *          (columns < c hold Q, columns >= c hold M).  Must not alias dA.
+ *   dR     n x n output: R = Q^T A on and above the diagonal, exact zeros below
+ *          (R5).  Must not alias dA or dQ.
+ *   d_info 0, or k if ||v_k|| < 1e-12 * ||A||_F / n (R3).
+ * Flush: C = B_Q^T B_M, S = B_Q C, M[:, c:n] -= S over all rows. */
+int qr_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dQ, int64_t ldq,
+              void* dR, int64_t ldr, int64_t* d_info, void* stream);
+
+/* Host-buffer variants (the end-to-end path): same arguments with HOST matrices (pinned
+ * memory recommended) and a host info word.  The library copies A to the device, runs
+ * the device entry point on an internal stream, copies the outputs back and
+ * synchronizes before returning.  Outputs may alias the input exactly (in place). */
+int chol_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hL, int64_t ldl,
+                     int64_t* info);
+int lu_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hLU, int64_t ldlu,
+                   int64_t* info);
+int qr_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hQ, int64_t ldq,
+                   void* hR, int64_t ldr, int64_t* info);
+
+/* Building blocks — one call per hot-path step, exposed so
+ * each step can be parity-tested and timed on its own.  All device, column-major,
+ * stream-ordered; `fail`-style numerical errors go to *d_info as above (column indices
+ * relative to the block's first column + col0).
+ *
+ * sf_chol_panel: PAPER.md:53-67 on the m x w block dP (top-left = the panel's diagonal
+ *   entry), in place; the block's earlier-panel contributions must already be subtracted.
+ * sf_syrk_sub:   PAPER.md:43-50: C(m x m, lower incl. diagonal) -= R R^T, R m x k.
+ * sf_gemm_sub:   C(m x n) -= op(A) op(B), op(A)(i,k) = ta ? A[k + i*lda] : A[i + k*lda],
+ *                op(B)(k,j) = tb ? B[j + k*ldb] : B[k + j*ldb]  (the LU/QR flush products).
+ * sf_lu_panel:   PAPER.md:105-121 on the panel with top-left (z,z): m = n - z rows, w
+ *   columns for L, and ncols_right = n - z - w further columns for U, in place.
+ * sf_qr_panel:   PAPER.md:158-168, MGS of the n x w columns dV in place (-> Q columns). */
+int sf_chol_panel(int64_t m, int64_t w, int dtype, void* dP, int64_t ld, int64_t col0, int64_t* d_info, void* stream);
+int sf_syrk_sub(int64_t m, int64_t k, int dtype, const void* dR, int64_t ldr, void* dC, int64_t ldc, void* stream);
+int sf_gemm_sub(int64_t m, int64_t n, int64_t k, int dtype, const void* dA, int64_t lda, int ta,
+                const void* dB, int64_t ldb, int tb, void* dC, int64_t ldc, void* stream);
+int sf_lu_panel(int64_t m, int64_t w, int64_t ncols_right, int dtype, void* dP, int64_t ld, int64_t col0,
+                double tol, int64_t* d_info, void* stream);
+int sf_qr_panel(int64_t n, int64_t w, int dtype, void* dV, int64_t ld, int64_t col0, double tol,
+                int64_t* d_info, void* stream);
+
+/* Number of flushes the c = z+s schedule performs: floor((n-1)/s). */
+int64_t sf_flush_count(int64_t n, int64_t s);
+/* Cumulative number of kernel launches this library has enqueued in this process
+ * (launch accounting for benchmarks: read it before and after a timed region). */
+int64_t sf_launch_counter(void);
+
+const char* sf_strerror(int status);
+const char* sf_last_error(void);
+int sf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STEPFACT_H */

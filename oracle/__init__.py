@@ -81,10 +81,16 @@ def flush_count(n, s):
 
 
 def chol(A, s, kcols=None):
-    """Algorithm 1. Returns (L, info); info 0 or 1-based failing column."""
-    A = _colmajor(A); n = A.shape[0]; _check_s(n, s)
-    L = np.zeros((n, n), order="F")
-    info = _load().orc_chol(n, s, n if kcols is None else kcols, A.ctypes.data, n, L.ctypes.data, n)
+    """Algorithm 1. Returns (L, info); info 0 or 1-based failing column.
+
+    With kcols=K < n, A may be the n x K block of its first K columns; L is then n x K."""
+    A = np.asfortranarray(np.asarray(A, dtype=np.float64)); n = A.shape[0]; _check_s(n, s)
+    K = n if kcols is None else min(int(kcols), n)
+    assert A.shape[1] >= K and (kcols is not None or A.shape[1] == n), "square matrix expected"
+    L = np.zeros((n, K), order="F")
+    info = _load().orc_chol(n, s, K, A.ctypes.data, n, L.ctypes.data, n)
+    if K < n and A.shape[1] == n:
+        L = np.concatenate([L, np.zeros((n, n - K))], axis=1)
     return L, int(info)
 
 

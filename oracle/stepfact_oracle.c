@@ -86,14 +86,17 @@ int64_t orc_flush_count(int64_t n, int64_t s) {
  * Algorithm 1, "A fast Cholesky decomposition algorithm".
  *   A: n x n SPD input (read only; the algorithm's mutations of A go to a private copy W)
  *   L: n x n output, lower triangular; entries never written stay 0
+ *   With K < n only the first K columns of A are read and of L written (n x K blocks).
  * Returns info (0 or 1-based failing column).
  */
 int64_t orc_chol(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t lda,
                  double* L, int64_t ldl) {
   const int64_t K = min64(kcols, n);
-  double* W = (double*)malloc(sizeof(double) * (size_t)n * (size_t)n);  /* the paper's A */
+  /* the paper's A (mutated by the flushes); a restricted run only ever touches columns < K,
+     so only those are copied (A and L may then be n x K blocks) */
+  double* W = (double*)malloc(sizeof(double) * (size_t)n * (size_t)K);
   if (!W) return -1;
-  for (int64_t j = 0; j < n; ++j)
+  for (int64_t j = 0; j < K; ++j)
     for (int64_t i = 0; i < n; ++i) { AT(W, n, i, j) = AT(A, lda, i, j); AT(L, ldl, i, j) = 0.0; }
 
   int64_t info = 0;

@@ -1,0 +1,209 @@
+"""stepfact on B200 — thin Python binding over libstepfact.so (include/stepfact.h).
+
+Argument marshalling only: every step of the factorizations runs in the library's CUDA
+kernels (sm_100a).  PyTorch supplies device memory and streams.  There is no CPU
+fallback: if the shared library is missing or fails to load, importing the binding's
+compute functions raises.
+
+Layout: the C ABI is column-major.  A torch tensor T (row-major, contiguous) read as a
+column-major buffer is T^T, so:
+  * `*_colmajor` functions take buffers that already hold column-major matrices
+    (what bench.py uses; no torch kernel runs);
+  * `chol(A)`, `lu(A)`, `qr(A)` take ordinary (row-major) torch matrices and return
+    ordinary torch matrices, doing the layout transposes with torch (marshalling).
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libstepfact.so")
+
+SF_F64, SF_F32 = 0, 1
+_STATUS = {0: "SF_OK", 1: "SF_EINVAL", 2: "SF_ENOTSUP", 3: "SF_ENOMEM", 4: "SF_ECUDA", 5: "SF_ENCCL"}
+_lib = None
+
+
+class StepfactError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{_STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+def lib():
+    """Load libstepfact.so (built by paper_1812_02056_b200/build.py or __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `python -m paper_1812_02056_b200.build` "
+                          "(no CPU fallback exists)")
+    L = ctypes.CDLL(LIB_PATH)
+    i64, i32, p, dbl = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_double
+    sig = {
+        "chol_factor": [i64, i64, i32, p, i64, p, i64, p, p],
+        "lu_factor": [i64, i64, i32, p, i64, p, i64, p, p],
+        "qr_factor": [i64, i64, i32, p, i64, p, i64, p, i64, p, p],
+        "chol_factor_host": [i64, i64, i32, p, i64, p, i64, p],
+        "lu_factor_host": [i64, i64, i32, p, i64, p, i64, p],
+        "qr_factor_host": [i64, i64, i32, p, i64, p, i64, p, i64, p],
+        "sf_chol_panel": [i64, i64, i32, p, i64, i64, p, p],
+        "sf_syrk_sub": [i64, i64, i32, p, i64, p, i64, p],
+        "sf_gemm_sub": [i64, i64, i64, i32, p, i64, i32, p, i64, i32, p, i64, p],
+        "sf_lu_panel": [i64, i64, i64, i32, p, i64, i64, dbl, p, p],
+        "sf_qr_panel": [i64, i64, i32, p, i64, i64, dbl, p, p],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = i32
+    L.sf_flush_count.argtypes = [i64, i64]
+    L.sf_flush_count.restype = i64
+    L.sf_launch_counter.argtypes = []
+    L.sf_launch_counter.restype = i64
+    L.sf_strerror.argtypes = [i32]
+    L.sf_strerror.restype = ctypes.c_char_p
+    L.sf_last_error.argtypes = []
+    L.sf_last_error.restype = ctypes.c_char_p
+    L.sf_version.restype = i32
+    _lib = L
+    return L
+
+
+EXPORTS = ("chol_factor", "lu_factor", "qr_factor", "chol_factor_host", "lu_factor_host", "qr_factor_host",
+           "sf_chol_panel", "sf_syrk_sub", "sf_gemm_sub", "sf_lu_panel", "sf_qr_panel", "sf_flush_count",
+           "sf_launch_counter", "sf_strerror", "sf_last_error", "sf_version")
+
+
+def _check(rc):
+    if rc != 0:
+        raise StepfactError(rc, lib().sf_last_error().decode())
+
+
+def _dtype_code(t):
+    import torch
+    if t.dtype == torch.float64:
+        return SF_F64
+    if t.dtype == torch.float32:
+        return SF_F32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if not t.is_cuda:
+            raise ValueError("device entry points need CUDA tensors")
+
+
+def flush_count(n, s):
+    return int(lib().sf_flush_count(n, s))
+
+
+def launch_counter():
+    return int(lib().sf_launch_counter())
+
+
+# ----------------------------------------------------------------------- raw column-major API
+
+def chol_colmajor(n, s, dA, lda, dL, ldl, d_info, dtype=SF_F64, stream=None):
+    """chol_factor on raw column-major device buffers (torch tensors or int pointers)."""
+    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
+    _check(lib().chol_factor(n, s, dtype, ptr(dA), lda, ptr(dL), ldl, ptr(d_info), _stream(stream)))
+
+
+def lu_colmajor(n, s, dA, lda, dLU, ldlu, d_info, dtype=SF_F64, stream=None):
+    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
+    _check(lib().lu_factor(n, s, dtype, ptr(dA), lda, ptr(dLU), ldlu, ptr(d_info), _stream(stream)))
+
+
+def qr_colmajor(n, s, dA, lda, dQ, ldq, dR, ldr, d_info, dtype=SF_F64, stream=None):
+    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
+    _check(lib().qr_factor(n, s, dtype, ptr(dA), lda, ptr(dQ), ldq, ptr(dR), ldr, ptr(d_info), _stream(stream)))
+
+
+# ----------------------------------------------------------------------- torch convenience API
+
+def _colmajor_copy(A):
+    """Column-major copy of the logical matrix A: buffer B with B.T == A (a torch transpose)."""
+    return A.mT.contiguous()
+
+
+def chol(A, s, stream=None):
+    """Cholesky of a symmetric positive definite CUDA matrix A (Alg. 1). Returns (L, info)."""
+    import torch
+    _need_cuda(A)
+    n = A.shape[0]
+    B = _colmajor_copy(A)
+    L = torch.zeros_like(B)
+    info = torch.zeros(1, dtype=torch.int64, device=A.device)
+    chol_colmajor(n, s, B, n, L, n, info, _dtype_code(A), stream)
+    return L.mT, int(info.item())
+
+
+def lu(A, s, stream=None):
+    """Crout LU without pivoting (Alg. 2). Returns (L, U, info) with U unit upper."""
+    import torch
+    _need_cuda(A)
+    n = A.shape[0]
+    B = _colmajor_copy(A)
+    info = torch.zeros(1, dtype=torch.int64, device=A.device)
+    lu_colmajor(n, s, B, n, B, n, info, _dtype_code(A), stream)
+    F = B.mT
+    L = torch.tril(F)
+    U = torch.triu(F, 1) + torch.eye(n, dtype=A.dtype, device=A.device)
+    return L, U, int(info.item())
+
+
+def qr(A, s, stream=None):
+    """QR by Alg. 3 (MGS panels, block projection flushes). Returns (Q, R, info)."""
+    import torch
+    _need_cuda(A)
+    n = A.shape[0]
+    B = _colmajor_copy(A)
+    Q = torch.empty_like(B)
+    R = torch.empty_like(B)
+    info = torch.zeros(1, dtype=torch.int64, device=A.device)
+    qr_colmajor(n, s, B, n, Q, n, R, n, info, _dtype_code(A), stream)
+    return Q.mT, R.mT, int(info.item())
+
+
+# ----------------------------------------------------------------------- host (end-to-end) API
+
+def _host_ptr(x):
+    if hasattr(x, "data_ptr"):
+        assert not x.is_cuda
+        return x.data_ptr()
+    assert isinstance(x, np.ndarray) and x.flags["F_CONTIGUOUS"] or x.flags["C_CONTIGUOUS"]
+    return x.ctypes.data
+
+
+def chol_host(hA, s, hL=None, dtype=SF_F64):
+    """chol_factor_host on column-major host buffers (pinned torch tensors or numpy)."""
+    n = hA.shape[0]
+    out = hA if hL is None else hL
+    info = ctypes.c_int64(0)
+    _check(lib().chol_factor_host(n, s, dtype, _host_ptr(hA), n, _host_ptr(out), n, ctypes.addressof(info)))
+    return out, info.value
+
+
+def lu_host(hA, s, hLU=None, dtype=SF_F64):
+    n = hA.shape[0]
+    out = hA if hLU is None else hLU
+    info = ctypes.c_int64(0)
+    _check(lib().lu_factor_host(n, s, dtype, _host_ptr(hA), n, _host_ptr(out), n, ctypes.addressof(info)))
+    return out, info.value
+
+
+def qr_host(hA, s, hQ, hR, dtype=SF_F64):
+    n = hA.shape[0]
+    info = ctypes.c_int64(0)
+    _check(lib().qr_factor_host(n, s, dtype, _host_ptr(hA), n, _host_ptr(hQ), n, _host_ptr(hR), n,
+                                ctypes.addressof(info)))
+    return hQ, hR, info.value

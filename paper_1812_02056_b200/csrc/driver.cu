@@ -1,0 +1,514 @@
+// driver.cu — the step-s schedule and the C ABI (include/stepfact.h).
+//
+// Schedule: z := 0; for c in 0..n-1: if c == z+s then
+// flush and z := c.  In panel terms: panels p = [p*s, min((p+1)s, n)) are factored in
+// order; after every panel except the last, ONE rectangular product updates the trailing
+// matrix.  Flush count = floor((n-1)/s).
+//
+// Out-of-place support: every kernel reads from `src` and writes to `dst`.  The first
+// panel and the first flush read the caller's A; from then on everything lives in the
+// output buffer (the first flush rewrites the whole trailing lower triangle / square), so
+// A is never modified unless the caller passes dA == dOut.
+//
+// Panels wider than the leaf width are factored recursively: factor the left half,
+// subtract its contribution from the right half with one GEMM (the same terms the paper's
+// k-loops subtract, grouped), factor the right half.  DESIGN.md §5 discusses why.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "../../include/stepfact.h"
+#include "kernels.h"
+
+namespace sf {
+
+static std::atomic<long long> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+static thread_local char g_last_error[512] = "";
+
+static int fail_with(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+#define SF_CUDA(expr)                                                                               \
+  do {                                                                                              \
+    cudaError_t _e = (expr);                                                                        \
+    if (_e != cudaSuccess) return fail_with(SF_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                                           __FILE__, __LINE__);                                     \
+  } while (0)
+
+static int leaf_width() {
+  static int w = [] {
+    const char* e = getenv("SF_LEAF");
+    int v = e ? atoi(e) : 64;
+    if (v != 16 && v != 32 && v != 64) v = 64;
+    return v;
+  }();
+  return w;
+}
+
+static int64_t half_of(int64_t w, int leaf) {
+  int64_t h = (w / 2 + leaf - 1) / leaf * leaf;
+  if (h >= w) h = w - leaf;
+  if (h <= 0) h = w / 2;
+  return h;
+}
+
+// ------------------------------------------------------------------ workspace
+struct Workspace {
+  char* base = nullptr;
+  size_t off = 0, cap = 0;
+  cudaStream_t st = nullptr;
+  cudaError_t init(size_t bytes, cudaStream_t s) {
+    st = s;
+    cap = bytes;
+    return cudaMallocAsync((void**)&base, bytes, s);
+  }
+  template <typename U>
+  U* take(size_t n) {
+    off = (off + 255) & ~(size_t)255;
+    U* p = (U*)(base + off);
+    off += n * sizeof(U);
+    return p;
+  }
+  ~Workspace() {
+    if (base) cudaFreeAsync(base, st);
+  }
+};
+
+// ------------------------------------------------------------------ GEMM dispatch per dtype
+template <typename T>
+struct Gemm {
+  int64_t M, N, K;
+  const T* A; int64_t lda; int ak;
+  const T* B; int64_t ldb; int bk;
+  const T* Cin; int64_t ldcin;
+  T* C; int64_t ldc;
+  double alpha; int beta; int mask;
+  int splits; T* work;
+  const long long* fail;
+};
+
+static cudaError_t run_gemm(const Gemm<double>& g, cudaStream_t st) {
+  GemmF64 p{g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, g.Cin, g.ldcin, g.C, g.ldc,
+            g.alpha, g.beta, g.splits, g.work, g.fail};
+  return gemm_f64(p, g.ak, g.bk, g.mask, st);
+}
+static cudaError_t run_gemm(const Gemm<float>&, cudaStream_t) { return cudaErrorNotSupported; }
+
+// C -= op(A) op(B) with C read from Cin (may differ) : common "subtract" form
+template <typename T>
+static cudaError_t gemm_sub(int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, int ak, const T* B,
+                            int64_t ldb, int bk, const T* Cin, int64_t ldcin, T* C, int64_t ldc, int mask,
+                            const long long* fail, cudaStream_t st) {
+  Gemm<T> g{M, N, K, A, lda, ak, B, ldb, bk, Cin, ldcin, C, ldc, -1.0, 1, mask, 1, nullptr, fail};
+  return run_gemm(g, st);
+}
+
+// ------------------------------------------------------------------ Cholesky
+template <typename T>
+static cudaError_t chol_panel_rec(int64_t m, int64_t w, const T* src, int64_t lds, T* dst, int64_t ldd,
+                                  int64_t col0, long long* fail, cudaStream_t st) {
+  const int leaf = leaf_width();
+  if (w <= leaf) return chol_leaf<T>(m, (int)w, src, lds, dst, ldd, col0, fail, st);
+  const int64_t h = half_of(w, leaf);
+  cudaError_t e = chol_panel_rec<T>(m, h, src, lds, dst, ldd, col0, fail, st);
+  if (e != cudaSuccess) return e;
+  // columns [h, w), rows [h, m):  X -= L[h:m, 0:h] * L[h:w, 0:h]^T  (lower part only)
+  e = gemm_sub<T>(m - h, w - h, h, dst + h, ldd, 0, dst + h, ldd, 0, src + h + h * lds, lds, dst + h + h * ldd, ldd,
+                  kMaskLower, fail, st);
+  if (e != cudaSuccess) return e;
+  return chol_panel_rec<T>(m - h, w - h, dst + h + h * ldd, ldd, dst + h + h * ldd, ldd, col0 + h, fail, st);
+}
+
+template <typename T>
+static int chol_run(int64_t n, int64_t s, const T* A, int64_t lda, T* L, int64_t ldl, int64_t* d_info,
+                    cudaStream_t st) {
+  Workspace ws;
+  SF_CUDA(ws.init(4096, st));
+  long long* fail = ws.take<long long>(1);
+  SF_CUDA(init_fail(fail, st));
+  for (int64_t z = 0; z < n; z += s) {
+    const int64_t w = (s < n - z) ? s : n - z, m = n - z;
+    const T* src = (z == 0) ? A : L;
+    const int64_t lds = (z == 0) ? lda : ldl;
+    SF_CUDA(chol_panel_rec<T>(m, w, src + z + z * lds, lds, L + z + z * ldl, ldl, z, fail, st));
+    const int64_t c = z + w;
+    if (c < n) {  // flush: A[c:n,c:n] -= R R^T, R = L[c:n, z:c)
+      SF_CUDA(gemm_sub<T>(n - c, n - c, w, L + c + z * ldl, ldl, 0, L + c + z * ldl, ldl, 0, src + c + c * lds, lds,
+                          L + c + c * ldl, ldl, kMaskLower, fail, st));
+    }
+  }
+  SF_CUDA(finish_info(fail, d_info, st));
+  return SF_OK;
+}
+
+// ------------------------------------------------------------------ LU
+template <typename T>
+static cudaError_t lu_panel_rec(int64_t m, int64_t w, int64_t ncr, const T* src, int64_t lds, T* dst, int64_t ldd,
+                                int64_t col0, const T* tol, long long* fail, cudaStream_t st) {
+  const int leaf = leaf_width();
+  if (w <= leaf) return lu_leaf<T>(m, ncr, (int)w, src, lds, dst, ldd, col0, tol, fail, st);
+  const int64_t h = half_of(w, leaf);
+  cudaError_t e = lu_panel_rec<T>(m, h, ncr + (w - h), src, lds, dst, ldd, col0, tol, fail, st);
+  if (e != cudaSuccess) return e;
+  // L part and U11 part of the right half: rows [h, m), cols [h, w) -= L[h:m, 0:h] U[0:h, h:w]
+  e = gemm_sub<T>(m - h, w - h, h, dst + h, ldd, 0, dst + h * ldd, ldd, 1, src + h + h * lds, lds, dst + h + h * ldd,
+                  ldd, kMaskNone, fail, st);
+  if (e != cudaSuccess) return e;
+  // U rows [h, w) of the columns right of the panel: -= L[h:w, 0:h] U[0:h, w:w+ncr]
+  if (ncr > 0) {
+    e = gemm_sub<T>(w - h, ncr, h, dst + h, ldd, 0, dst + w * ldd, ldd, 1, src + h + w * lds, lds, dst + h + w * ldd,
+                    ldd, kMaskNone, fail, st);
+    if (e != cudaSuccess) return e;
+  }
+  return lu_panel_rec<T>(m - h, w - h, ncr, dst + h + h * ldd, ldd, dst + h + h * ldd, ldd, col0 + h, tol, fail, st);
+}
+
+template <typename T>
+static int lu_run(int64_t n, int64_t s, const T* A, int64_t lda, T* LU, int64_t ldd, int64_t* d_info,
+                  cudaStream_t st) {
+  Workspace ws;
+  SF_CUDA(ws.init(16384, st));
+  long long* fail = ws.take<long long>(1);
+  T* tol = ws.take<T>(1);
+  double* part = ws.take<double>(512);
+  SF_CUDA(init_fail(fail, st));
+  SF_CUDA(frob_norm_tol<T>(n, A, lda, tol, part, st));
+  for (int64_t z = 0; z < n; z += s) {
+    const int64_t w = (s < n - z) ? s : n - z, m = n - z, ncr = n - z - w;
+    const T* src = (z == 0) ? A : LU;
+    const int64_t lds = (z == 0) ? lda : ldd;
+    SF_CUDA(lu_panel_rec<T>(m, w, ncr, src + z + z * lds, lds, LU + z + z * ldd, ldd, z, tol, fail, st));
+    const int64_t c = z + w;
+    if (c < n) {  // flush: A[c:n,c:n] -= R_L R_U
+      SF_CUDA(gemm_sub<T>(n - c, n - c, w, LU + c + z * ldd, ldd, 0, LU + z + c * ldd, ldd, 1, src + c + c * lds, lds,
+                          LU + c + c * ldd, ldd, kMaskNone, fail, st));
+    }
+  }
+  SF_CUDA(finish_info(fail, d_info, st));
+  return SF_OK;
+}
+
+// ------------------------------------------------------------------ QR
+static int splitk_for(int64_t M, int64_t N, int64_t K) {
+  const int64_t tiles = ((M + 127) / 128) * ((N + 127) / 128);
+  int64_t sp = (2 * 148 + tiles - 1) / tiles;
+  const int64_t maxsp = K / 256 > 1 ? K / 256 : 1;
+  if (sp > maxsp) sp = maxsp;
+  if (sp > 16) sp = 16;
+  return (int)(sp < 1 ? 1 : sp);
+}
+
+struct QrWork {
+  void* cw; void* split; void* mgs;
+  int64_t split_elems;
+};
+
+// Project the columns [0, wc) of V (n rows) against the orthonormal columns Qb (n x k):
+//   C = Qb^T V ; V = Vin - Qb C   (PAPER.md:147-155 restricted to the given columns)
+template <typename T>
+static cudaError_t qr_project(int64_t n, int64_t k, int64_t wc, const T* Qb, int64_t ldq, const T* Vin, int64_t ldvin,
+                              T* V, int64_t ldv, T* Cw, T* split, int64_t split_elems, long long* fail,
+                              cudaStream_t st) {
+  int sp = splitk_for(k, wc, n);
+  while (sp > 1 && (int64_t)sp * k * wc > split_elems) --sp;
+  Gemm<T> g1{k, wc, n, Qb, ldq, 1, Vin, ldvin, 1, nullptr, 0, Cw, k, 1.0, 0, kMaskNone, sp, split, fail};
+  cudaError_t e = run_gemm(g1, st);
+  if (e != cudaSuccess) return e;
+  return gemm_sub<T>(n, wc, k, Qb, ldq, 0, Cw, k, 1, Vin, ldvin, V, ldv, kMaskNone, fail, st);
+}
+
+template <typename T>
+static cudaError_t qr_panel(int64_t n, int64_t w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
+                           const T* tol, T* mgswork, T* Cw, T* split, int64_t split_elems, long long* fail,
+                           cudaStream_t st) {
+  const int64_t wmax = qr_mgs_max_width(n, (int)sizeof(T));
+  if (w <= wmax) return qr_mgs_panel<T>(n, (int)w, src, lds, dst, ldd, col0, tol, mgswork, fail, st);
+  // panel wider than one cooperative MGS launch holds: chunks, projected against the
+  // finished chunks of the same panel ("wide QR panels")
+  for (int64_t z0 = 0; z0 < w; z0 += wmax) {
+    const int64_t wc = (wmax < w - z0) ? wmax : w - z0;
+    const T* vin = src + z0 * lds;
+    int64_t ldvin = lds;
+    if (z0 > 0) {
+      cudaError_t e = qr_project<T>(n, z0, wc, dst, ldd, vin, ldvin, dst + z0 * ldd, ldd, Cw, split, split_elems, fail, st);
+      if (e != cudaSuccess) return e;
+      vin = dst + z0 * ldd;
+      ldvin = ldd;
+    }
+    cudaError_t e = qr_mgs_panel<T>(n, (int)wc, vin, ldvin, dst + z0 * ldd, ldd, col0 + z0, tol, mgswork, fail, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+template <typename T>
+static int qr_run(int64_t n, int64_t s, const T* A, int64_t lda, T* Q, int64_t ldq, T* R, int64_t ldr, int64_t* d_info,
+                  cudaStream_t st) {
+  const int64_t wmax = qr_mgs_max_width(n, (int)sizeof(T));
+  const int64_t wcap = s < wmax ? s : wmax;
+  const size_t mgs_elems = qr_mgs_work_elems(n, (int)wcap) + 64;
+  const int64_t cw_elems = s * n;
+  int64_t split_elems = 0;
+  for (int64_t z = 0; z < n; z += s) {
+    const int64_t w = (s < n - z) ? s : n - z;
+    if (z + w < n) {
+      const int sp = splitk_for(w, n - z - w, n);
+      if ((int64_t)sp * w * (n - z - w) > split_elems) split_elems = (int64_t)sp * w * (n - z - w);
+    }
+  }
+  if (s > wmax) {
+    const int sp = splitk_for(s, wmax, n);
+    if ((int64_t)sp * s * wmax > split_elems) split_elems = (int64_t)sp * s * wmax;
+  }
+  Workspace ws;
+  SF_CUDA(ws.init(sizeof(T) * (mgs_elems + cw_elems + split_elems) + 16384 + 4 * 256, st));
+  long long* fail = ws.take<long long>(1);
+  T* tol = ws.take<T>(1);
+  double* part = ws.take<double>(512);
+  T* mgsw = ws.take<T>(mgs_elems);
+  T* Cw = ws.take<T>(cw_elems);
+  T* split = ws.take<T>(split_elems > 0 ? split_elems : 1);
+  SF_CUDA(init_fail(fail, st));
+  SF_CUDA(frob_norm_tol<T>(n, A, lda, tol, part, st));
+  for (int64_t z = 0; z < n; z += s) {
+    const int64_t w = (s < n - z) ? s : n - z;
+    const T* src = (z == 0) ? A : Q;           // M := copy of A lives in Q
+    const int64_t lds = (z == 0) ? lda : ldq;
+    SF_CUDA(qr_panel<T>(n, w, src + z * lds, lds, Q + z * ldq, ldq, z, tol, mgsw, Cw, split, split_elems, fail, st));
+    const int64_t c = z + w;
+    if (c < n) {  // flush: C = B_Q^T B_M, M[:, c:n] -= B_Q C over all rows
+      SF_CUDA(qr_project<T>(n, w, n - c, Q + z * ldq, ldq, src + c * lds, lds, Q + c * ldq, ldq, Cw, split,
+                            split_elems, fail, st));
+    }
+  }
+  // R := Q^T A: upper triangle on the tensor cores, exact zeros below
+  SF_CUDA(zero_strict_lower<T>(n, R, ldr, st));
+  {
+    Gemm<T> g{n, n, n, Q, ldq, 1, A, lda, 1, nullptr, 0, R, ldr, 1.0, 0, kMaskUpper, 1, nullptr, fail};
+    SF_CUDA(run_gemm(g, st));
+  }
+  SF_CUDA(finish_info(fail, d_info, st));
+  return SF_OK;
+}
+
+// ------------------------------------------------------------------ argument checks
+static int check_common(int64_t n, int64_t s, int dtype, const void* a, int64_t lda, const void* o, int64_t ldo) {
+  if (n < 1) return fail_with(SF_EINVAL, "n=%lld < 1", (long long)n);
+  if (s < 1 || s > n) return fail_with(SF_EINVAL, "step s=%lld outside [1, n=%lld]", (long long)s, (long long)n);
+  if (dtype != SF_F64 && dtype != SF_F32) return fail_with(SF_EINVAL, "unknown dtype %d", dtype);
+  if (!a || !o) return fail_with(SF_EINVAL, "null matrix pointer");
+  if (lda < n || ldo < n) return fail_with(SF_EINVAL, "leading dimension < n");
+  const size_t elt = dtype == SF_F64 ? 8 : 4;
+  if (((uintptr_t)a % elt) || ((uintptr_t)o % elt)) return fail_with(SF_EINVAL, "misaligned matrix pointer");
+  if (a != o) {
+    // out of place: the two n x n extents must not overlap
+    const char* pa = (const char*)a; const char* po = (const char*)o;
+    const char* ea = pa + elt * (size_t)(lda * (n - 1) + n);
+    const char* eo = po + elt * (size_t)(ldo * (n - 1) + n);
+    if (pa < eo && po < ea) return fail_with(SF_EINVAL, "input and output overlap without being identical");
+  } else if (lda != ldo) {
+    return fail_with(SF_EINVAL, "in-place call with lda != ld_out");
+  }
+  return SF_OK;
+}
+
+}  // namespace sf
+
+using namespace sf;
+
+extern "C" {
+
+int chol_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dL, int64_t ldl, int64_t* d_info,
+                void* stream) {
+  int rc = check_common(n, s, dtype, dA, lda, dL, ldl);
+  if (rc) return rc;
+  if (!d_info) return fail_with(SF_EINVAL, "null d_info");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SF_F64) return chol_run<double>(n, s, (const double*)dA, lda, (double*)dL, ldl, d_info, st);
+  return fail_with(SF_ENOTSUP, "fp32 Cholesky not built yet");
+}
+
+int lu_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dLU, int64_t ldlu, int64_t* d_info,
+              void* stream) {
+  int rc = check_common(n, s, dtype, dA, lda, dLU, ldlu);
+  if (rc) return rc;
+  if (!d_info) return fail_with(SF_EINVAL, "null d_info");
+  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp32 LU not implemented (SURVEY.md §8 f4)");
+  return lu_run<double>(n, s, (const double*)dA, lda, (double*)dLU, ldlu, d_info, (cudaStream_t)stream);
+}
+
+int qr_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dQ, int64_t ldq, void* dR,
+              int64_t ldr, int64_t* d_info, void* stream) {
+  int rc = check_common(n, s, dtype, dA, lda, dQ, ldq);
+  if (rc) return rc;
+  rc = check_common(n, s, dtype, dA, lda, dR, ldr);
+  if (rc) return rc;
+  if (dA == dQ || dA == dR || dQ == dR) return fail_with(SF_EINVAL, "qr_factor outputs must not alias");
+  if (!d_info) return fail_with(SF_EINVAL, "null d_info");
+  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp32 QR not implemented (SURVEY.md §8 f4)");
+  return qr_run<double>(n, s, (const double*)dA, lda, (double*)dQ, ldq, (double*)dR, ldr, d_info,
+                        (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------ host-buffer variants
+static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hO1, int64_t ld1,
+                     void* hO2, int64_t ld2, int64_t* info) {
+  if (n < 1 || !hA || !hO1 || !info || (kind == 2 && !hO2)) return fail_with(SF_EINVAL, "bad host arguments");
+  if (lda < n || ld1 < n || (kind == 2 && ld2 < n)) return fail_with(SF_EINVAL, "leading dimension < n");
+  const size_t elt = dtype == SF_F64 ? 8 : 4;
+  const size_t bytes = elt * (size_t)n * (size_t)n;
+  cudaStream_t st;
+  SF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  char* d = nullptr;
+  const int nbuf = kind == 2 ? 3 : 1;
+  cudaError_t e = cudaMallocAsync((void**)&d, nbuf * bytes + 256, st);
+  if (e != cudaSuccess) { cudaStreamDestroy(st); return fail_with(SF_ENOMEM, "device allocation failed"); }
+  int64_t* dinfo = (int64_t*)(d + nbuf * bytes);
+  int rc = SF_OK;
+  e = cudaMemcpy2DAsync(d, n * elt, hA, lda * elt, n * elt, n, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    if (kind == 0) {
+      // upper triangle of the device copy is A's own (in-place factorization)
+      rc = chol_factor(n, s, dtype, d, n, d, n, dinfo, st);
+      if (!rc) e = cudaMemcpy2DAsync(hO1, ld1 * elt, d, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);
+    } else if (kind == 1) {
+      rc = lu_factor(n, s, dtype, d, n, d, n, dinfo, st);
+      if (!rc) e = cudaMemcpy2DAsync(hO1, ld1 * elt, d, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);
+    } else {
+      rc = qr_factor(n, s, dtype, d, n, d + bytes, n, d + 2 * bytes, n, dinfo, st);
+      if (!rc) e = cudaMemcpy2DAsync(hO1, ld1 * elt, d + bytes, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);
+      if (!rc && e == cudaSuccess)
+        e = cudaMemcpy2DAsync(hO2, ld2 * elt, d + 2 * bytes, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);
+    }
+    if (!rc && e == cudaSuccess) e = cudaMemcpyAsync(info, dinfo, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  }
+  cudaFreeAsync(d, st);
+  cudaError_t e2 = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail_with(SF_ECUDA, "host copy: %s", cudaGetErrorString(e));
+  if (e2 != cudaSuccess) return fail_with(SF_ECUDA, "stream sync: %s", cudaGetErrorString(e2));
+  return SF_OK;
+}
+
+int chol_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hL, int64_t ldl,
+                     int64_t* info) {
+  return host_call(0, n, s, dtype, hA, lda, hL, ldl, nullptr, 0, info);
+}
+int lu_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hLU, int64_t ldlu,
+                   int64_t* info) {
+  return host_call(1, n, s, dtype, hA, lda, hLU, ldlu, nullptr, 0, info);
+}
+int qr_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hQ, int64_t ldq, void* hR,
+                   int64_t ldr, int64_t* info) {
+  return host_call(2, n, s, dtype, hA, lda, hQ, ldq, hR, ldr, info);
+}
+
+// ------------------------------------------------------------------ building blocks
+int sf_chol_panel(int64_t m, int64_t w, int dtype, void* dP, int64_t ld, int64_t col0, int64_t* d_info, void* stream) {
+  if (m < 1 || w < 1 || w > m || ld < m || !dP || !d_info) return fail_with(SF_EINVAL, "bad panel arguments");
+  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp64 only");
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace ws;
+  SF_CUDA(ws.init(256, st));
+  long long* fail = ws.take<long long>(1);
+  SF_CUDA(init_fail(fail, st));
+  SF_CUDA(chol_panel_rec<double>(m, w, (double*)dP, ld, (double*)dP, ld, col0, fail, st));
+  SF_CUDA(finish_info(fail, d_info, st));
+  return SF_OK;
+}
+
+int sf_syrk_sub(int64_t m, int64_t k, int dtype, const void* dR, int64_t ldr, void* dC, int64_t ldc, void* stream) {
+  if (m < 0 || k < 0 || !dR || !dC || ldr < m || ldc < m) return fail_with(SF_EINVAL, "bad syrk arguments");
+  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp64 only");
+  const double* R = (const double*)dR;
+  SF_CUDA(gemm_sub<double>(m, m, k, R, ldr, 0, R, ldr, 0, (double*)dC, ldc, (double*)dC, ldc, kMaskLower, nullptr,
+                           (cudaStream_t)stream));
+  return SF_OK;
+}
+
+int sf_gemm_sub(int64_t m, int64_t n, int64_t k, int dtype, const void* dA, int64_t lda, int ta, const void* dB,
+                int64_t ldb, int tb, void* dC, int64_t ldc, void* stream) {
+  if (m < 0 || n < 0 || k < 0 || !dA || !dB || !dC || ldc < m) return fail_with(SF_EINVAL, "bad gemm arguments");
+  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp64 only");
+  SF_CUDA(gemm_sub<double>(m, n, k, (const double*)dA, lda, ta ? 1 : 0, (const double*)dB, ldb, tb ? 0 : 1,
+                           (double*)dC, ldc, (double*)dC, ldc, kMaskNone, nullptr, (cudaStream_t)stream));
+  return SF_OK;
+}
+
+int sf_lu_panel(int64_t m, int64_t w, int64_t ncr, int dtype, void* dP, int64_t ld, int64_t col0, double tol,
+                int64_t* d_info, void* stream) {
+  if (m < 1 || w < 1 || w > m || ncr < 0 || ld < m || !dP || !d_info) return fail_with(SF_EINVAL, "bad panel arguments");
+  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp64 only");
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace ws;
+  SF_CUDA(ws.init(512, st));
+  long long* fail = ws.take<long long>(1);
+  double* dtol = ws.take<double>(1);
+  SF_CUDA(init_fail(fail, st));
+  SF_CUDA(cudaMemcpyAsync(dtol, &tol, sizeof(double), cudaMemcpyHostToDevice, st));
+  SF_CUDA(lu_panel_rec<double>(m, w, ncr, (double*)dP, ld, (double*)dP, ld, col0, dtol, fail, st));
+  SF_CUDA(finish_info(fail, d_info, st));
+  SF_CUDA(cudaStreamSynchronize(st));  // tol lives in pageable host memory
+  return SF_OK;
+}
+
+int sf_qr_panel(int64_t n, int64_t w, int dtype, void* dV, int64_t ld, int64_t col0, double tol, int64_t* d_info,
+                void* stream) {
+  if (n < 1 || w < 1 || w > n || ld < n || !dV || !d_info) return fail_with(SF_EINVAL, "bad panel arguments");
+  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp64 only");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t wmax = qr_mgs_max_width(n, 8);
+  const int64_t wcap = w < wmax ? w : wmax;
+  const int sp = splitk_for(w, wcap, n);
+  const int64_t split_elems = (int64_t)sp * w * wcap;
+  const size_t mgs = qr_mgs_work_elems(n, (int)wcap) + 64;
+  Workspace ws;
+  SF_CUDA(ws.init(8 * (mgs + w * wcap + split_elems) + 4096, st));
+  long long* fail = ws.take<long long>(1);
+  double* dtol = ws.take<double>(1);
+  double* mgsw = ws.take<double>(mgs);
+  double* Cw = ws.take<double>(w * wcap);
+  double* split = ws.take<double>(split_elems);
+  SF_CUDA(init_fail(fail, st));
+  SF_CUDA(cudaMemcpyAsync(dtol, &tol, sizeof(double), cudaMemcpyHostToDevice, st));
+  SF_CUDA(qr_panel<double>(n, w, (double*)dV, ld, (double*)dV, ld, col0, dtol, mgsw, Cw, split, split_elems, fail, st));
+  SF_CUDA(finish_info(fail, d_info, st));
+  SF_CUDA(cudaStreamSynchronize(st));
+  return SF_OK;
+}
+
+int64_t sf_flush_count(int64_t n, int64_t s) {
+  if (n < 1 || s < 1) return 0;
+  int64_t f = 0;
+  for (int64_t z = 0; z < n; z += s)
+    if (z + s < n) ++f;
+  return f;
+}
+
+int64_t sf_launch_counter(void) { return g_launches.load(); }
+
+const char* sf_strerror(int status) {
+  switch (status) {
+    case SF_OK: return "success";
+    case SF_EINVAL: return "invalid argument";
+    case SF_ENOTSUP: return "not supported";
+    case SF_ENOMEM: return "out of device memory";
+    case SF_ECUDA: return "CUDA error";
+    case SF_ENCCL: return "NCCL error";
+    default: return "unknown status";
+  }
+}
+const char* sf_last_error(void) { return g_last_error; }
+int sf_version(void) { return 1; }
+
+}  // extern "C"

@@ -1,0 +1,277 @@
+// gemm_f64.cu — FP64 tensor-core (DMMA.8x8x4) GEMM / SYRK with the trailing-matrix
+// subtraction fused into the epilogue.
+//
+// Serves every dense contraction of the three algorithms:
+//   Cholesky flush   A[c:n,c:n] -= R R^T,      R = L[c:n, z:c)
+//   LU flush         A[c:n,c:n] -= R_L R_U
+//   QR flush         C = B_Q^T B_M ; M[:,c:n] -= B_Q C
+//   QR R             R = Q^T A  (upper tiles only)
+//   in-panel corrections of the nested sub-panels (same formulas, narrower N).
+// The product S is never materialised: each 128x128 tile of C is read, decremented by
+// the register accumulator and written once (Cin may differ from C: out-of-place first
+// step).  MASK restricts work to the lower (Cholesky) or upper (R) triangle of C.
+//
+// Design (DESIGN.md §5 K1/K2): 256 threads = 8 warps as 2 (i) x 4 (j); warp tile 64x32 =
+// 8x4 DMMA atoms; 4-stage cp.async pipeline of 128x16 operand slices; smem layouts padded
+// so every fragment load is bank-conflict free; C tile prefetched into L2 during the
+// mainloop.  The D fragment is used transposed (D = C^T) so each lane owns two
+// consecutive rows of a column-major C.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sf {
+
+namespace g64 {
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 256;
+constexpr int PAD_IK = BM + 4;    // smem row stride (doubles) for idx-contiguous slices
+constexpr int PAD_KI = BK + 4;    // smem row stride for k-contiguous slices
+constexpr int OPER = (BK * PAD_IK > BM * PAD_KI) ? BK * PAD_IK : BM * PAD_KI;  // 2560
+constexpr size_t SMEM = sizeof(double) * (size_t)OPER * 2 * STAGES;           // 160 KiB
+}  // namespace g64
+
+// Load a 128 (idx) x 16 (k) slice of op(X) into shared memory.
+//  KC=false: op(X)(idx,k) = X[idx + k*ld]  (idx contiguous)  -> Xs[k*PAD_IK + idx]
+//  KC=true : op(X)(idx,k) = X[k + idx*ld]  (k contiguous)    -> Xs[idx*PAD_KI + k]
+template <bool KC, bool V16>
+__device__ __forceinline__ void load_slice(double* Xs, const double* __restrict__ X, int64_t ld,
+                                           int64_t idx0, int64_t nidx, int64_t k0, int64_t K,
+                                           int tid) {
+  using namespace g64;
+  if (!KC) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int id = tid + r * THREADS;
+      const int kk = id >> 6, ch = id & 63;
+      const int64_t idx = idx0 + 2 * ch, kg = k0 + kk;
+      double* dst = Xs + kk * PAD_IK + 2 * ch;
+      const bool kin = kg < K;
+      if (V16) {
+        int bytes = (!kin || idx >= nidx) ? 0 : (idx + 1 >= nidx ? 8 : 16);
+        const double* src = bytes ? X + idx + kg * ld : X;
+        cp_async16(dst, src, bytes);
+      } else {
+        int b0 = (kin && idx < nidx) ? 8 : 0, b1 = (kin && idx + 1 < nidx) ? 8 : 0;
+        cp_async8(dst, b0 ? X + idx + kg * ld : X, b0);
+        cp_async8(dst + 1, b1 ? X + idx + 1 + kg * ld : X, b1);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int id = tid + r * THREADS;
+      const int ii = id >> 3, ch = id & 7;
+      const int64_t idx = idx0 + ii, kg = k0 + 2 * ch;
+      double* dst = Xs + ii * PAD_KI + 2 * ch;
+      const bool iin = idx < nidx;
+      if (V16) {
+        int bytes = (!iin || kg >= K) ? 0 : (kg + 1 >= K ? 8 : 16);
+        const double* src = bytes ? X + kg + idx * ld : X;
+        cp_async16(dst, src, bytes);
+      } else {
+        int b0 = (iin && kg < K) ? 8 : 0, b1 = (iin && kg + 1 < K) ? 8 : 0;
+        cp_async8(dst, b0 ? X + kg + idx * ld : X, b0);
+        cp_async8(dst + 1, b1 ? X + kg + 1 + idx * ld : X, b1);
+      }
+    }
+  }
+}
+
+template <bool KC>
+__device__ __forceinline__ double frag(const double* Xs, int base, int kk, int lane) {
+  using namespace g64;
+  if (!KC) return Xs[(kk * 4 + (lane & 3)) * PAD_IK + base + (lane >> 2)];
+  return Xs[(base + (lane >> 2)) * PAD_KI + kk * 4 + (lane & 3)];
+}
+
+// Map the linear CTA index to a (tile-row, tile-col) pair, visiting only the tiles that
+// intersect the masked triangle.  Tiles are enumerated column by column.
+template <int MASK>
+__device__ __forceinline__ void tile_of(int bid, int TM, int TN, int& ti, int& tj) {
+  if (MASK == kMaskNone) { ti = bid % TM; tj = bid / TM; return; }
+  int j = 0;
+  for (; j < TN; ++j) {
+    const int cnt = (MASK == kMaskLower) ? (TM - j) : (j + 1 < TM ? j + 1 : TM);
+    if (bid < cnt) break;
+    bid -= cnt;
+  }
+  tj = j;
+  ti = (MASK == kMaskLower) ? j + bid : bid;
+}
+
+template <bool AK, bool BKC, bool V16, int MASK>
+__global__ void __launch_bounds__(g64::THREADS, 1) gemm_f64_kernel(GemmF64 p) {
+  using namespace g64;
+  if (p.fail && failed(p.fail)) return;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                       // [STAGES][OPER]
+  double* Bs = smem + STAGES * OPER;       // [STAGES][OPER]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int TM = (int)((p.M + BM - 1) / BM), TN = (int)((p.N + BN - 1) / BN);
+  int ti, tj;
+  tile_of<MASK>(blockIdx.x, TM, TN, ti, tj);
+  const int64_t i0 = (int64_t)ti * BM, j0 = (int64_t)tj * BN;
+
+  // K range of this split
+  const int sp = blockIdx.y;
+  int64_t kchunk = (p.K + p.splits - 1) / p.splits;
+  kchunk = (kchunk + BK - 1) / BK * BK;
+  const int64_t kbeg = (int64_t)sp * kchunk;
+  const int64_t kend = (kbeg + kchunk < p.K) ? kbeg + kchunk : p.K;
+  const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+
+  // Warm L2 with the C tile we will read-modify-write in the epilogue.
+  if (p.beta && p.splits == 1) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int id = tid + r * THREADS;      // 1024 lines: 128 columns x 8 lines of 128 B
+      const int64_t jj = j0 + (id >> 3), ii = i0 + (id & 7) * 16;
+      if (jj < p.N && ii < p.M) prefetch_l2(p.Cin + ii + jj * p.ldcin);
+    }
+  }
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  auto issue = [&](int kb) {
+    if (kb < nk) {
+      const int slot = kb % STAGES;
+      const int64_t k0 = kbeg + (int64_t)kb * BK;
+      load_slice<AK, V16>(As + slot * OPER, p.A, p.lda, i0, p.M, k0, kend, tid);
+      load_slice<BKC, V16>(Bs + slot * OPER, p.B, p.ldb, j0, p.N, k0, kend, tid);
+    }
+    cp_async_commit();
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) issue(s);
+
+  for (int kb = 0; kb < nk; ++kb) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    issue(kb + STAGES - 1);
+    const double* as = As + (kb % STAGES) * OPER;
+    const double* bs = Bs + (kb % STAGES) * OPER;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double fa[8], fb[4];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) fa[a] = frag<AK>(as, wm * 64 + a * 8, kk, lane);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) fb[b] = frag<BKC>(bs, wn * 32 + b * 8, kk, lane);
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          // D = C^T: the MMA's A operand is op(B) (rows j), its B operand is op(A) (cols i)
+          dmma_8x8x4(acc[a][b][0], acc[a][b][1], fb[b], fa[a]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // Epilogue: lane owns C(i, j) for i = ibase + {0,1}, j = jbase.
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int64_t i = i0 + wm * 64 + a * 8 + 2 * (lane & 3);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int64_t j = j0 + wn * 32 + b * 8 + (lane >> 2);
+      if (j >= p.N) continue;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t ie = i + e;
+        if (ie >= p.M) continue;
+        if (MASK == kMaskLower && ie < j) continue;
+        if (MASK == kMaskUpper && ie > j) continue;
+        if (p.splits > 1) {
+          p.work[(int64_t)sp * p.M * p.N + j * p.M + ie] = acc[a][b][e];
+        } else {
+          const double v = p.alpha * acc[a][b][e];
+          p.C[ie + j * p.ldc] = p.beta ? p.Cin[ie + j * p.ldcin] + v : v;
+        }
+      }
+    }
+  }
+}
+
+// Fixed-order split-K reduction: C = (beta ? Cin : 0) + alpha * sum_sp work[sp].
+__global__ void splitk_reduce_f64(GemmF64 p) {
+  if (p.fail && failed(p.fail)) return;
+  const int64_t total = p.M * p.N;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % p.M, j = t / p.M;
+    double s = 0.0;
+    for (int sp = 0; sp < p.splits; ++sp) s += p.work[(int64_t)sp * total + t];
+    const double v = p.alpha * s;
+    p.C[i + j * p.ldc] = p.beta ? p.Cin[i + j * p.ldcin] + v : v;
+  }
+}
+
+template <bool AK, bool BKC, bool V16, int MASK>
+static cudaError_t launch_t(const GemmF64& p, int ntiles, cudaStream_t st) {
+  auto k = gemm_f64_kernel<AK, BKC, V16, MASK>;
+  static bool attr_set = false;  // per template instance
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g64::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid(ntiles, p.splits);
+  k<<<grid, g64::THREADS, g64::SMEM, st>>>(p); count_launch();
+  return cudaGetLastError();
+}
+
+template <bool AK, bool BKC, bool V16>
+static cudaError_t launch_mask(const GemmF64& p, int mask, int ntiles, cudaStream_t st) {
+  switch (mask) {
+    case kMaskLower: return launch_t<AK, BKC, V16, kMaskLower>(p, ntiles, st);
+    case kMaskUpper: return launch_t<AK, BKC, V16, kMaskUpper>(p, ntiles, st);
+    default: return launch_t<AK, BKC, V16, kMaskNone>(p, ntiles, st);
+  }
+}
+
+static bool aligned16(const void* ptr, int64_t ld) {
+  return (((uintptr_t)ptr) & 15) == 0 && (ld % 2) == 0;
+}
+
+cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStream_t st) {
+  if (p.M <= 0 || p.N <= 0) return cudaSuccess;
+  if (p.K <= 0) {
+    // nothing to subtract: C = beta ? Cin : 0 (only needed out of place)
+    if (p.beta && p.Cin == p.C && p.ldcin == p.ldc) return cudaSuccess;
+    p.K = 0;
+  }
+  if (p.splits < 1) p.splits = 1;
+  const int TM = (int)((p.M + g64::BM - 1) / g64::BM), TN = (int)((p.N + g64::BN - 1) / g64::BN);
+  int ntiles = 0;
+  if (mask == kMaskLower) { for (int j = 0; j < TN; ++j) ntiles += (TM - j > 0 ? TM - j : 0); }
+  else if (mask == kMaskUpper) { for (int j = 0; j < TN; ++j) ntiles += (j + 1 < TM ? j + 1 : TM); }
+  else ntiles = TM * TN;
+  if (ntiles == 0) return cudaSuccess;
+  const bool v16 = aligned16(p.A, p.lda) && aligned16(p.B, p.ldb);
+  cudaError_t e;
+  const int key = (a_kcontig ? 1 : 0) | (b_kcontig ? 2 : 0) | (v16 ? 4 : 0);
+  switch (key) {
+    case 0: e = launch_mask<false, false, false>(p, mask, ntiles, st); break;
+    case 1: e = launch_mask<true, false, false>(p, mask, ntiles, st); break;
+    case 2: e = launch_mask<false, true, false>(p, mask, ntiles, st); break;
+    case 3: e = launch_mask<true, true, false>(p, mask, ntiles, st); break;
+    case 4: e = launch_mask<false, false, true>(p, mask, ntiles, st); break;
+    case 5: e = launch_mask<true, false, true>(p, mask, ntiles, st); break;
+    case 6: e = launch_mask<false, true, true>(p, mask, ntiles, st); break;
+    default: e = launch_mask<true, true, true>(p, mask, ntiles, st); break;
+  }
+  if (e != cudaSuccess || p.splits == 1) return e;
+  const int64_t total = p.M * p.N;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  splitk_reduce_f64<<<blocks, 256, 0, st>>>(p); count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace sf

@@ -1,0 +1,63 @@
+// kernels.h — internal launch interface between the drivers (driver.cu) and the kernels.
+// Not part of the public C ABI (include/stepfact.h).  All matrices column-major.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sf {
+
+// process-wide count of kernel launches enqueued by the library (sf_launch_counter)
+void count_launch(int n = 1);
+
+enum { kMaskNone = 0, kMaskLower = 1, kMaskUpper = 2 };
+
+// C(MxN) = (beta ? Cin : 0) + alpha * op(A)(MxK) * op(B)(KxN)
+//   op(A)(i,k) = a_kcontig ? A[k + i*lda] : A[i + k*lda]
+//   op(B)(k,j) = b_kcontig ? B[k + j*ldb] : B[j + k*ldb]
+//   mask: write only i >= j (lower) / i <= j (upper) of C
+//   splits > 1: split-K with a fixed-order reduction through `work` (splits*M*N doubles)
+struct GemmF64 {
+  int64_t M, N, K;
+  const double* A; int64_t lda;
+  const double* B; int64_t ldb;
+  const double* Cin; int64_t ldcin;
+  double* C; int64_t ldc;
+  double alpha;
+  int beta;
+  int splits;
+  double* work;
+  const long long* fail;   // device "first failed column" word; kernels exit early if set
+};
+cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStream_t st);
+
+// ---------------------------------------------------------------- panels (templated T)
+// Cholesky leaf (Alg. 1 inner loops) on columns [0,w) of the m x w block
+// whose top-left corner is the diagonal entry (z',z').  src may equal dst.
+template <typename T>
+cudaError_t chol_leaf(int64_t m, int w, const T* src, int64_t lds, T* dst, int64_t ldd,
+                      int64_t col0, long long* fail, cudaStream_t st);
+
+// LU leaf (Alg. 2 inner loops): diagonal w x w block, the L rows below
+// it (m-w rows) and the U columns right of it (ncols_right columns), all in place/out.
+template <typename T>
+cudaError_t lu_leaf(int64_t m, int64_t ncols_right, int w, const T* src, int64_t lds, T* dst,
+                    int64_t ldd, int64_t col0, const T* tol, long long* fail, cudaStream_t st);
+
+// QR panel, modified Gram-Schmidt (Alg. 3) on n x w columns.
+template <typename T>
+cudaError_t qr_mgs_panel(int64_t n, int w, const T* src, int64_t lds, T* dst, int64_t ldd,
+                         int64_t col0, const T* tol, T* work, long long* fail, cudaStream_t st);
+size_t qr_mgs_work_elems(int64_t n, int w);
+int qr_mgs_max_width(int64_t n, int elt);   // widest panel the smem-resident MGS kernel takes
+
+// utilities
+template <typename T>
+cudaError_t frob_norm_tol(int64_t n, const T* A, int64_t lda, T* tol_out, double* work, cudaStream_t st);  // work: 512 doubles
+cudaError_t init_fail(long long* fail, cudaStream_t st);
+cudaError_t finish_info(const long long* fail, int64_t* d_info, cudaStream_t st);
+template <typename T>
+cudaError_t zero_strict_lower(int64_t n, T* R, int64_t ldr, cudaStream_t st);
+template <typename T>
+cudaError_t copy_matrix(int64_t m, int64_t n, const T* src, int64_t lds, T* dst, int64_t ldd, cudaStream_t st);
+
+}  // namespace sf

@@ -1,0 +1,285 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bar (BASELINE.json north_star; DESIGN.md §3 readings P6/P7):
+  fp64: floored relative elementwise error (synth.r2_error) <= 1e-10, residual <= 1e-13*n
+  QR:   R2 <= 1e-10 on Q columns / R rows [0, n-2s); tail columns within 100*u*kappa
+  planted integer factors: bit-exact.
+Inputs are the same bytes on both sides (synth generators).  Sizes span several 128-wide
+tiles and ragged tails; full BASELINE sizes are checked on sampled (restricted-column)
+outputs the oracle computes exactly as in the full run.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1812_02056_b200 as sf  # noqa: E402
+
+EPS = np.finfo(np.float64).eps
+TOL64 = 1e-10
+
+
+def dev(A):
+    """numpy logical matrix -> device buffer holding it column-major."""
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(A, np.float64).T)).cuda()
+
+
+def host(B):
+    """device column-major buffer -> numpy logical matrix."""
+    return B.cpu().numpy().T.copy()
+
+
+def run_chol(A, s, inplace=True):
+    n = A.shape[0]
+    dA = dev(A)
+    info = torch.zeros(1, dtype=torch.int64, device="cuda")
+    if inplace:
+        sf.chol_colmajor(n, s, dA, n, dA, n, info)
+        out = dA
+    else:
+        out = torch.full_like(dA, 7.0)
+        sf.chol_colmajor(n, s, dA, n, out, n, info)
+        assert np.array_equal(host(dA), A), "out-of-place call modified A"
+    torch.cuda.synchronize()
+    return host(out), int(info.item())
+
+
+def run_lu(A, s, inplace=True):
+    n = A.shape[0]
+    dA = dev(A)
+    info = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out = dA if inplace else torch.empty_like(dA)
+    sf.lu_colmajor(n, s, dA, n, out, n, info)
+    torch.cuda.synchronize()
+    F = host(out)
+    return np.tril(F), np.triu(F, 1) + np.eye(n), int(info.item())
+
+
+def run_qr(A, s):
+    n = A.shape[0]
+    dA = dev(A)
+    Q = torch.empty_like(dA); R = torch.full_like(dA, 3.0)
+    info = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sf.qr_colmajor(n, s, dA, n, Q, n, R, n, info)
+    torch.cuda.synchronize()
+    return host(Q), host(R), int(info.item())
+
+
+def svals(n):
+    return sorted({1, 2, 3, 7, 16, 32, 64, 100, 128, 130, 200, n // 2, n} & set(range(1, n + 1)))
+
+
+# ============================================================ Cholesky
+
+@pytest.mark.parametrize("n", [1, 2, 5, 33, 127, 130, 300])
+def test_chol_small_grid(n):
+    A = synth.gen_numpy("paper_spd", n, seed=n)
+    for s in svals(n):
+        Lo, io = oracle.chol(A, s)
+        for inplace in (True, False):
+            Lg, ig = run_chol(A, s, inplace)
+            assert ig == io == 0
+            low = np.tril(Lg)
+            assert synth.r2_error(low, Lo) <= TOL64, (n, s, inplace)
+            if inplace:
+                assert np.array_equal(np.triu(Lg, 1), np.triu(A, 1)), "strict upper must be untouched"
+            else:
+                assert np.all(Lg[np.triu_indices(n, 1)] == 7.0), "out of place: strict upper of L never written"
+            assert np.all(np.diag(low) > 0)
+            assert synth.rel_residual(A, low, low.T) <= 1e-13 * n
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_chol_cfg1(seed):
+    """BASELINE.json configs[0]: n=256, s=16, A = G G^T + n I."""
+    n, s = 256, 16
+    A = synth.gen_numpy("spd_shift", n, seed)
+    Lo, _ = oracle.chol(A, s)
+    Lg, info = run_chol(A, s)
+    Lg = np.tril(Lg)
+    assert info == 0
+    assert synth.r2_error(Lg, Lo) <= TOL64
+    assert synth.rel_residual(A, Lg, Lg.T) <= 1e-13 * n
+
+
+@pytest.mark.parametrize("n,s", [(512, 1), (1000, 16), (1000, 168), (4096, 64), (4096, 512), (2048, 2048)])
+def test_chol_planted_exact(n, s):
+    Lx = synth.planted_chol(n, seed=n + s)
+    Lg, info = run_chol(Lx @ Lx.T, s)
+    assert info == 0
+    assert np.array_equal(np.tril(Lg), Lx)
+
+
+def test_chol_not_pd_info():
+    A = np.array([[1.0, 2.0], [2.0, 1.0]])
+    for s in (1, 2):
+        assert run_chol(A, s)[1] == 2
+    B = synth.gen_numpy("paper_spd", 300, seed=3)
+    B[200, 200] = -5.0
+    io = oracle.chol(B, 64)[1]
+    assert run_chol(B, 64)[1] == io == 201
+
+
+def test_chol_deterministic():
+    A = synth.gen_numpy("spd_scaled", 700, seed=5)
+    a, _ = run_chol(A, 96)
+    b, _ = run_chol(A, 96)
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("s", [64, 168, 512, 1024])
+def test_chol_cfg3_sampled(s):
+    """BASELINE.json configs[2] at full size n=16384: the first K columns of L against the
+    restricted oracle (bitwise the full oracle's first K columns), plus a Freivalds residual
+    of the whole factor computed with torch (an independent checker)."""
+    n, K = 16384, 384
+    A = synth.gen_torch("spd_scaled", n, seed=0)
+    B = A.clone()                                   # symmetric: column-major buffer == A
+    info = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sf.chol_colmajor(n, s, B, n, B, n, info)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    L = torch.tril(B.mT)                            # logical L
+    Ak = A[:, :K].cpu().numpy()                     # column j of A = A[:, j] (symmetric)
+    Lo, io = oracle.chol(Ak, s, kcols=K)
+    assert io == 0
+    assert synth.r2_error(L[:, :K].cpu().numpy(), Lo[:, :K]) <= TOL64
+    g = torch.Generator(device="cuda"); g.manual_seed(1)
+    x = torch.randn(n, 4, device="cuda", dtype=torch.float64, generator=g)
+    r = (A @ x - L @ (L.mT @ x)).norm() / (A @ x).norm()
+    assert float(r) <= 1e-13 * n
+
+
+# ============================================================ LU
+
+@pytest.mark.parametrize("n", [1, 3, 33, 130, 257])
+def test_lu_small_grid(n):
+    A = synth.gen_numpy("diag_dominant", n, seed=n)
+    for s in svals(n):
+        Lo, Uo, io = oracle.lu(A, s)
+        for inplace in (True, False):
+            Lg, Ug, ig = run_lu(A, s, inplace)
+            assert ig == io == 0
+            assert synth.r2_error(Lg, Lo) <= TOL64 and synth.r2_error(Ug, Uo) <= TOL64, (n, s)
+            assert synth.rel_residual(A, Lg, Ug) <= 1e-13 * n
+
+
+def test_lu_cfg2():
+    """BASELINE.json configs[1]: n=4096, s=64, strictly diagonally dominant U(-1,1)."""
+    n, s = 4096, 64
+    A = synth.gen_numpy("diag_dominant", n, seed=0)
+    Lo, Uo, io = oracle.lu(A, s)
+    Lg, Ug, ig = run_lu(A, s)
+    assert io == ig == 0
+    assert synth.r2_error(Lg, Lo) <= TOL64 and synth.r2_error(Ug, Uo) <= TOL64
+    assert synth.rel_residual(A, Lg, Ug) <= 1e-13 * n
+
+
+@pytest.mark.parametrize("n,s", [(512, 1), (1000, 64), (2048, 200)])
+def test_lu_planted_exact(n, s):
+    Lx, Ux = synth.planted_lu(n, seed=n + s)
+    Lg, Ug, info = run_lu(Lx @ Ux, s)
+    assert info == 0 and np.array_equal(Lg, Lx) and np.array_equal(Ug, Ux)
+
+
+def test_lu_zero_pivot_info():
+    A = np.array([[0.0, 1.0], [1.0, 1.0]])
+    for s in (1, 2):
+        assert run_lu(A, s)[2] == 1
+
+
+# ============================================================ QR
+
+def check_qr(A, s, Qg, Rg, Qo, Ro):
+    n = A.shape[0]
+    head = max(0, n - 2 * s)
+    kappa = np.linalg.cond(A)
+    if head > 0:
+        assert synth.r2_error(Qg[:, :head], Qo[:, :head]) <= TOL64
+        assert synth.r2_error(Rg[:head, :], Ro[:head, :]) <= TOL64
+    # tail columns: forward error of MGS is ~u*kappa (reading P7)
+    assert np.max(np.linalg.norm(Qg - Qo, axis=0)) <= max(100 * EPS * kappa, 1e-13)
+    assert np.max(np.linalg.norm(Rg - Ro, axis=1)) <= max(100 * EPS * kappa, 1e-13) * np.linalg.norm(A, 2)
+    assert np.all(np.tril(Rg, -1) == 0)
+    assert synth.orthogonality(Qg) <= 1e-12 * n
+    assert synth.rel_residual(A, Qg, Rg) <= 1e-13 * n
+
+
+@pytest.mark.parametrize("n", [1, 4, 33, 130, 257])
+def test_qr_small_grid(n):
+    A = synth.gen_numpy("gaussian", n, seed=n)
+    for s in svals(n):
+        Qo, Ro, io, _ = oracle.qr(A, s)
+        Qg, Rg, ig = run_qr(A, s)
+        assert io == ig == 0
+        check_qr(A, s, Qg, Rg, Qo, Ro)
+
+
+@pytest.mark.parametrize("n,s", [(256, 1), (256, 64), (1024, 128), (4096, 128)])
+def test_qr_planted_exact(n, s):
+    Qx, Rx = synth.planted_qr(n, seed=n + s)
+    Qg, Rg, info = run_qr(Qx @ Rx, s)
+    assert info == 0 and np.array_equal(Qg, Qx) and np.array_equal(Rg, Rx)
+
+
+def test_qr_cfg4_sampled():
+    """BASELINE.json configs[3] at full size: n=8192, s=128, N(0,1); first K columns of Q
+    and rows of R against the restricted oracle, plus orthogonality/residual probes."""
+    n, s, K = 8192, 128, 256
+    A = synth.gen_numpy("gaussian", n, seed=0)
+    Qg, Rg, ig = run_qr(A, s)
+    Qo, Ro, io, _ = oracle.qr(A, s, kcols=K)
+    assert io == ig == 0
+    assert synth.r2_error(Qg[:, :K], Qo[:, :K]) <= TOL64
+    assert synth.r2_error(Rg[:K, :], Ro[:K, :]) <= TOL64
+    Qt = torch.from_numpy(Qg).cuda(); At = torch.from_numpy(A).cuda(); Rt = torch.from_numpy(Rg).cuda()
+    assert float((Qt.mT @ Qt - torch.eye(n, device="cuda", dtype=torch.float64)).norm()) <= 1e-12 * n
+    assert float((At - Qt @ Rt).norm() / At.norm()) <= 1e-13 * n
+    assert np.all(np.tril(Rg, -1) == 0)
+
+
+# ============================================================ building blocks
+
+def test_syrk_and_gemm_blocks():
+    rng = np.random.default_rng(0)
+    m, k = 300, 40
+    R = rng.standard_normal((m, k)); C = rng.standard_normal((m, m))
+    dR, dC = dev(R), dev(C)
+    assert sf.lib().sf_syrk_sub(m, k, 0, dR.data_ptr(), m, dC.data_ptr(), m, None) == 0
+    torch.cuda.synchronize()
+    ref = C - R @ R.T
+    got = host(dC)
+    assert np.abs(np.tril(got) - np.tril(ref)).max() <= 1e-13 * k * 10
+    assert np.array_equal(np.triu(got, 1), np.triu(C, 1))
+    A = rng.standard_normal((k, m)); B = rng.standard_normal((m, k)); C = rng.standard_normal((m, m))
+    dA, dB, dC = dev(A), dev(B), dev(C)
+    # C -= A^T B^T  (ta=1: A stored k x m; tb=1: B stored m x k)
+    assert sf.lib().sf_gemm_sub(m, m, k, 0, dA.data_ptr(), k, 1, dB.data_ptr(), m, 1, dC.data_ptr(), m, None) == 0
+    torch.cuda.synchronize()
+    assert np.abs(host(dC) - (C - A.T @ B.T)).max() <= 1e-12
+
+
+def test_torch_api_roundtrip():
+    A = synth.gen_numpy("spd_shift", 200, seed=1)
+    L, info = sf.chol(torch.from_numpy(A).cuda(), 32)
+    assert info == 0 and synth.r2_error(np.tril(L.cpu().numpy()), oracle.chol(A, 32)[0]) <= TOL64
+    B = synth.gen_numpy("gaussian", 150, seed=2)
+    Q, R, info = sf.qr(torch.from_numpy(B).cuda(), 32)
+    assert info == 0 and synth.rel_residual(B, Q.cpu().numpy(), R.cpu().numpy()) <= 1e-13 * 150
+
+
+def test_host_entry_points():
+    n, s = 300, 64
+    A = synth.gen_numpy("spd_shift", n, seed=4)
+    hA = np.asfortranarray(A.copy())
+    out, info = sf.chol_host(hA, s)
+    assert info == 0 and synth.r2_error(np.tril(out), oracle.chol(A, s)[0]) <= TOL64
+    B = synth.gen_numpy("diag_dominant", n, seed=5)
+    hB = np.asfortranarray(B.copy())
+    out, info = sf.lu_host(hB, s)
+    Lo, Uo, _ = oracle.lu(B, s)
+    assert info == 0 and synth.r2_error(np.tril(out), Lo) <= TOL64
