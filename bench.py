@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py — step-s factorization throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--s S] [--impl reference]
+
+A "step" is one complete factorization (every panel + every flush of Alg. 1/2/3 —
+SURVEY.md §8 rows a1..a8) of the workload's synthetic matrix, out of place (A stays
+pristine, so no restore is needed between steps; A is 2.1 GB > the 126 MB L2, so nothing
+survives in L2 between steps).  Metric: classical-count GFLOP/s (n^3/3 Cholesky, 2n^3/3 LU,
+4n^3/3 QR), whole job = sum over ranks / max-over-ranks device time.
+
+Default workload: BASELINE.json configs[2] (Cholesky fp64, n=16384) at s=512 — the config
+BASELINE names as the tensor-pipe roofline measurement and on which north_star sets the
+>= 70% FP64-tensor-peak target; DESIGN.md §6 explains the choice.  Other configs are
+selectable with --workload (they are also parity-test cases).
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (the only
+reference that exists: PAPER.md's own code is not available) on a bounded sample.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (kind, n, s, generator, dtype, BASELINE config)
+    "chol_f64_n16384_s512": ("chol", 16384, 512, "spd_scaled", "f64", "configs[2]"),
+    "chol_f64_n256_s16": ("chol", 256, 16, "spd_shift", "f64", "configs[0]"),
+    "lu_f64_n4096_s64": ("lu", 4096, 64, "diag_dominant", "f64", "configs[1]"),
+    "qr_f64_n8192_s128": ("qr", 8192, 128, "gaussian", "f64", "configs[3]"),
+    "chol_f64_n65536_s512": ("chol", 65536, 512, "spd_scaled", "f64", "configs[4]"),
+}
+DEFAULT = "chol_f64_n16384_s512"
+CALIB = os.path.join(ROOT, "calib", "peaks_fp64_tf32.json")
+
+
+def classical_flops(kind, n):
+    return {"chol": n ** 3 / 3.0, "lu": 2.0 * n ** 3 / 3.0, "qr": 4.0 * n ** 3 / 3.0}[kind]
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0])); mx.append(float(parts[1])); pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm_sorted = sorted(sm)
+        return {"sm_mhz": sm_sorted[len(sm) // 2], "sm_max_mhz": max(mx), "power_w_max": max(pw),
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------------------- oracle sample
+
+def oracle_executed_flops(kind, n, s, K):
+    """Flops the restricted oracle run executes for the first K columns (exact loop counts)."""
+    f = 0.0
+    for c in range(K):
+        z = c - (c % s)
+        if c > 0 and c % s == 0:   # flush at c (z_prev = c - s)
+            w = s
+            if kind == "chol":
+                f += (K - c) * (n - c) * (2.0 * w + 1)
+            elif kind == "lu":
+                f += ((n - c) ** 2 - (n - K) ** 2) * (2.0 * w + 1)
+            else:
+                f += 2.0 * n * w * (K - c) + (2.0 * w + 1) * n * (K - c)
+        d = c - z
+        if kind == "chol":
+            f += 2 * d + 1 + (n - c - 1) * (2.0 * d + 1)
+        elif kind == "lu":
+            f += (n - c) * (2.0 * d) + (n - c) * (2.0 * d + 1)
+        else:
+            f += d * 4.0 * n + 3.0 * n
+    if kind == "qr":
+        f += 2.0 * K * n * n
+    return f
+
+
+def oracle_sample(kind, n, s, A_host_cols, K, A_full=None):
+    """Run the oracle restricted to K columns; returns (seconds, flops, threads)."""
+    import oracle
+    t0 = time.perf_counter()
+    if kind == "chol":
+        _, info = oracle.chol(A_host_cols, s, kcols=K)
+    elif kind == "lu":
+        _, _, info = oracle.lu(A_full, s, kcols=K)
+    else:
+        _, _, info, _ = oracle.qr(A_full, s, kcols=K)
+    dt = time.perf_counter() - t0
+    assert info == 0, f"oracle failed at column {info}"
+    return dt, oracle_executed_flops(kind, n, s, K), oracle.max_threads()
+
+
+def host_inputs(kind, gen, n, seed, K, dev_A=None):
+    """Host copies the oracle needs (same bytes as the device run when dev_A is given)."""
+    import numpy as np
+    if dev_A is not None:
+        if kind == "chol":   # symmetric: device buffer column-major == logical A; first K columns
+            return np.asfortranarray(dev_A[:K, :].cpu().numpy().T), None
+        full = dev_A.cpu().numpy().T.copy()   # buffer -> logical matrix
+        return None, full
+    import synth
+    A = synth.gen_numpy(gen, n, seed)
+    return (np.asfortranarray(A[:, :K]) if kind == "chol" else None), A
+
+
+def sample_cols(kind, n):
+    # ~10-30 s of oracle work on a 16-core host for cpu_baseline; smaller per --impl reference step
+    return {"chol": 2048 if n >= 8192 else n, "lu": 512 if n > 2048 else n, "qr": 96 if n > 2048 else n}[kind]
+
+
+# ----------------------------------------------------------------------------- main
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default=DEFAULT, choices=sorted(WORKLOADS))
+    ap.add_argument("--s", type=int, default=None, help="override the step size (s-sweep)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    kind, n, s, gen, dtype, cfgname = WORKLOADS[args.workload]
+    s = args.s or s
+    K = max(1, sample_cols(kind, n) // 2)
+    dev_A = None
+    try:
+        import torch
+        if torch.cuda.is_available():
+            import synth
+            dev_A = synth.gen_torch(gen, n, args.seed) if n > 4096 else None
+            if dev_A is not None and kind != "chol":
+                dev_A = dev_A.mT.contiguous()
+    except Exception:
+        dev_A = None
+    Acols, Afull = host_inputs(kind, gen, n, args.seed, K, dev_A)
+    for _ in range(args.warmup):
+        oracle_sample(kind, n, s, Acols, K, Afull)
+    tot_t, tot_f, thr = 0.0, 0.0, 1
+    for _ in range(args.steps):
+        dt, fl, thr = oracle_sample(kind, n, s, Acols, K, Afull)
+        tot_t += dt; tot_f += fl
+    value = tot_f / tot_t / 1e9
+    sample = (f"oracle (oracle/stepfact_oracle.c, -O2, OpenMP) restricted to the first {K} of {n} columns "
+              f"of the {args.workload} matrix per step; value = executed flops / time")
+    line = {"impl": "reference", "metric": "factorization GFLOP/s (classical count) and % of FP64 tensor peak",
+            "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": args.workload, "kind": kind, "n": n, "s": s, "baseline_config": cfgname,
+                       "generator": gen, "seed": args.seed, "sample_cols": K},
+            "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": thr, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    import paper_1812_02056_b200 as sf
+    import synth
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    kind, n, s, gen, dtype, cfgname = WORKLOADS[args.workload]
+    s = args.s or s
+    assert args.warmup >= 3 or os.environ.get("SF_BENCH_ALLOW_SHORT"), "timing rules need >= 3 warm-up steps"
+
+    # ---- inputs (synthetic, seeded; every rank factors its own replica: seed + rank)
+    seed = args.seed + rank
+    Alog = synth.gen_torch(gen, n, seed) if n > 4096 else torch.from_numpy(synth.gen_numpy(gen, n, seed)).cuda()
+    # column-major buffer of the logical matrix (identical bytes for symmetric A)
+    A = Alog if kind == "chol" else Alog.mT.contiguous()
+    del Alog
+    info = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out1 = torch.zeros_like(A)
+    out2 = torch.zeros_like(A) if kind == "qr" else None
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if kind == "chol":
+            sf.chol_colmajor(n, s, A, n, out1, n, info, stream=stream)
+        elif kind == "lu":
+            sf.lu_colmajor(n, s, A, n, out1, n, info, stream=stream)
+        else:
+            sf.qr_colmajor(n, s, A, n, out1, n, out2, n, info, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if int(info.item()) != 0:
+        raise RuntimeError(f"factorization failed at column {int(info.item())}")
+
+    # ---- timed region
+    clocks = ClockSampler(local)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)                               # let the sampler start
+    sf.profile_enable(True)
+    sf.profile_collect()
+    l0 = sf.launch_counter()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    l1 = sf.launch_counter()
+    prof = sf.profile_collect()
+    sf.profile_enable(False)
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if int(info.item()) != 0:
+        raise RuntimeError(f"factorization failed at column {int(info.item())}")
+    t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    t_max = float(t_max.item())
+    flops = classical_flops(kind, n)
+    value = ws * args.steps * flops / (t_max * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (the trailing-update GEMM/SYRK launches)
+    peaks = json.load(open(CALIB)) if os.path.exists(CALIB) else {}
+    peak = peaks.get("fp64_dmma_tflops")
+    upd_ms, upd_n, upd_fl = prof["update"]
+    pan_ms, pan_n, _ = prof["panel"]
+    qr_ms, qr_n, qr_fl = prof["qr_r"]
+    achieved = upd_fl / (upd_ms * 1e-3) / 1e12 if upd_ms > 0 else None
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr_path):
+        traffic = json.load(open(tr_path)).get(args.workload)
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
+                "kernel": "gemm_f64_kernel (flush update, DMMA.8x8x4)",
+                "peak_source": "measured: calib/peaks_fp64_tf32.json fp64_dmma_tflops (DMMA microbenchmark, "
+                               "this pool's B200); MEASURED_PEAKS.json has no fp64 entry",
+                "launches_per_step": upd_n / args.steps if args.steps else None,
+                "avg_launch_ms": upd_ms / upd_n if upd_n else None,
+                "flops_per_launch": upd_fl / upd_n if upd_n else None,
+                "update_share_of_step": upd_ms / ms if ms else None,
+                "panel_ms_per_step": pan_ms / args.steps, "qr_r_ms_per_step": qr_ms / args.steps}
+
+    # ---- end to end through the C ABI with HOST buffers (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        hA = A.cpu().pin_memory()
+        h1 = torch.empty_like(hA).pin_memory()
+        h2 = torch.empty_like(hA).pin_memory() if kind == "qr" else None
+        hin = hA.clone().pin_memory()
+
+        def hstep():
+            if kind == "chol":
+                _, inf = sf.chol_host(hA, s, h1)
+            elif kind == "lu":
+                _, inf = sf.lu_host(hA, s, h1)
+            else:
+                _, _, inf = sf.qr_host(hA, s, h1, h2)
+            assert inf == 0
+        hstep()
+        ke = max(1, min(args.steps, 3))
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            hstep()
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        if ws > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        nbytes = A.numel() * A.element_size()
+        e2e = {"value": ws * ke * flops / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes * (2 if kind == "qr" else 1), "steps": ke,
+               "api": f"{kind}_factor_host (C ABI, pinned host buffers)"}
+        del hA, h1, h2, hin
+
+    # ---- CPU oracle beside it (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        K = sample_cols(kind, n)
+        Acols, Afull = host_inputs(kind, gen, n, seed, K, dev_A=A if n > 4096 else None)
+        dt, fl, thr = oracle_sample(kind, n, s, Acols, K, Afull)
+        cpu = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": thr, "kind": "oracle",
+               "sample": f"oracle restricted to the first {K} of {n} columns of this workload's matrix "
+                         f"({fl:.3g} executed flops in {dt:.1f} s); full-run time extrapolates to "
+                         f"{flops / (fl / dt) / 3600:.2f} h"}
+
+    if rank == 0:
+        line = {"metric": "factorization GFLOP/s (classical count) and % of FP64 tensor peak",
+                "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+                "config": {"workload": args.workload, "kind": kind, "n": n, "s": s, "baseline_config": cfgname,
+                           "generator": gen, "seed": args.seed, "parallelism": "replicas" if ws > 1 else "single",
+                           "l2": f"inputs larger than L2 ({A.numel() * A.element_size() / 1e9:.2f} GB > 126 MB); "
+                                 "out-of-place factorization, A re-read from HBM every step"},
+                "pct_fp64_peak": (value / ws / 1e3 / peak) if peak else None,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(l1 - l0), "clocks": ck}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

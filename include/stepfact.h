@@ -118,6 +118,16 @@ int64_t sf_flush_count(int64_t n, int64_t s);
  * (launch accounting for benchmarks: read it before and after a timed region). */
 int64_t sf_launch_counter(void);
 
+/* Profiling hook.  sf_profile_enable(1) makes the drivers record a CUDA event pair on the
+ * factorization stream around every flush (kind 0: the trailing-update kernel launches),
+ * every panel (kind 1) and QR's R := Q^T A (kind 2).  sf_profile_collect synchronizes on
+ * the recorded events and returns, per kind, total device milliseconds, number of
+ * bracketed regions and the algorithmic flops they performed (SURVEY.md §8(d) formulas:
+ * Cholesky flush s*m*(m+1), LU flush 2*s*m^2, QR flush 4*n*s*m, R n^2*(n+1));
+ * arrays of length 3; then it clears the record.  Not for use during graph capture. */
+void sf_profile_enable(int on);
+int sf_profile_collect(double* ms, int64_t* count, double* flops);
+
 const char* sf_strerror(int status);
 const char* sf_last_error(void);
 int sf_version(void);

@@ -67,13 +67,18 @@ def lib():
     L.sf_last_error.argtypes = []
     L.sf_last_error.restype = ctypes.c_char_p
     L.sf_version.restype = i32
+    L.sf_profile_enable.argtypes = [i32]
+    L.sf_profile_enable.restype = None
+    L.sf_profile_collect.argtypes = [p, p, p]
+    L.sf_profile_collect.restype = i32
     _lib = L
     return L
 
 
 EXPORTS = ("chol_factor", "lu_factor", "qr_factor", "chol_factor_host", "lu_factor_host", "qr_factor_host",
            "sf_chol_panel", "sf_syrk_sub", "sf_gemm_sub", "sf_lu_panel", "sf_qr_panel", "sf_flush_count",
-           "sf_launch_counter", "sf_strerror", "sf_last_error", "sf_version")
+           "sf_launch_counter", "sf_strerror", "sf_last_error", "sf_version", "sf_profile_enable",
+           "sf_profile_collect")
 
 
 def _check(rc):
@@ -108,6 +113,17 @@ def flush_count(n, s):
 
 def launch_counter():
     return int(lib().sf_launch_counter())
+
+
+def profile_enable(on=True):
+    lib().sf_profile_enable(1 if on else 0)
+
+
+def profile_collect():
+    """{kind: (ms, count, flops)} for kinds 'update', 'panel', 'qr_r' since the last collect."""
+    ms = (ctypes.c_double * 3)(); cnt = (ctypes.c_int64 * 3)(); fl = (ctypes.c_double * 3)()
+    _check(lib().sf_profile_collect(ctypes.addressof(ms), ctypes.addressof(cnt), ctypes.addressof(fl)))
+    return {k: (ms[i], cnt[i], fl[i]) for i, k in enumerate(("update", "panel", "qr_r"))}
 
 
 # ----------------------------------------------------------------------- raw column-major API

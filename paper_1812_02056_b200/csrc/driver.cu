@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "../../include/stepfact.h"
 #include "kernels.h"
@@ -28,6 +29,32 @@ static std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 static thread_local char g_last_error[512] = "";
+
+// ------------------------------------------------------------------ profiling hook
+// When enabled, CUDA event pairs are recorded on the factorization stream around every
+// flush (trailing update) and every panel, so a benchmark can measure the update
+// kernels' own device time inside its timed region (sf_profile_collect).
+struct ProfRec { cudaEvent_t a, b; int kind; double flops; };
+static bool g_prof = false;
+static std::vector<ProfRec> g_prof_recs;
+static std::vector<cudaEvent_t> g_event_pool;
+static cudaEvent_t pool_event() {
+  if (!g_event_pool.empty()) { cudaEvent_t e = g_event_pool.back(); g_event_pool.pop_back(); return e; }
+  cudaEvent_t e; cudaEventCreate(&e); return e;
+}
+struct ProfScope {
+  ProfRec r{}; cudaStream_t st; bool on;
+  ProfScope(int kind, double flops, cudaStream_t s) : st(s), on(g_prof) {
+    if (!on) return;
+    r.a = pool_event(); r.b = pool_event(); r.kind = kind; r.flops = flops;
+    cudaEventRecord(r.a, st);
+  }
+  ~ProfScope() {
+    if (!on) return;
+    cudaEventRecord(r.b, st);
+    g_prof_recs.push_back(r);
+  }
+};
 
 static int fail_with(int code, const char* fmt, ...) {
   va_list ap;
@@ -139,9 +166,13 @@ static int chol_run(int64_t n, int64_t s, const T* A, int64_t lda, T* L, int64_t
     const int64_t w = (s < n - z) ? s : n - z, m = n - z;
     const T* src = (z == 0) ? A : L;
     const int64_t lds = (z == 0) ? lda : ldl;
-    SF_CUDA(chol_panel_rec<T>(m, w, src + z + z * lds, lds, L + z + z * ldl, ldl, z, fail, st));
+    {
+      ProfScope ps(1, 0.0, st);
+      SF_CUDA(chol_panel_rec<T>(m, w, src + z + z * lds, lds, L + z + z * ldl, ldl, z, fail, st));
+    }
     const int64_t c = z + w;
     if (c < n) {  // flush: A[c:n,c:n] -= R R^T, R = L[c:n, z:c)
+      ProfScope ps(0, (double)w * (double)(n - c) * (double)(n - c + 1), st);
       SF_CUDA(gemm_sub<T>(n - c, n - c, w, L + c + z * ldl, ldl, 0, L + c + z * ldl, ldl, 0, src + c + c * lds, lds,
                           L + c + c * ldl, ldl, kMaskLower, fail, st));
     }
@@ -186,9 +217,13 @@ static int lu_run(int64_t n, int64_t s, const T* A, int64_t lda, T* LU, int64_t 
     const int64_t w = (s < n - z) ? s : n - z, m = n - z, ncr = n - z - w;
     const T* src = (z == 0) ? A : LU;
     const int64_t lds = (z == 0) ? lda : ldd;
-    SF_CUDA(lu_panel_rec<T>(m, w, ncr, src + z + z * lds, lds, LU + z + z * ldd, ldd, z, tol, fail, st));
+    {
+      ProfScope ps(1, 0.0, st);
+      SF_CUDA(lu_panel_rec<T>(m, w, ncr, src + z + z * lds, lds, LU + z + z * ldd, ldd, z, tol, fail, st));
+    }
     const int64_t c = z + w;
     if (c < n) {  // flush: A[c:n,c:n] -= R_L R_U
+      ProfScope ps(0, 2.0 * (double)w * (double)(n - c) * (double)(n - c), st);
       SF_CUDA(gemm_sub<T>(n - c, n - c, w, LU + c + z * ldd, ldd, 0, LU + z + c * ldd, ldd, 1, src + c + c * lds, lds,
                           LU + c + c * ldd, ldd, kMaskNone, fail, st));
     }
@@ -283,9 +318,13 @@ static int qr_run(int64_t n, int64_t s, const T* A, int64_t lda, T* Q, int64_t l
     const int64_t w = (s < n - z) ? s : n - z;
     const T* src = (z == 0) ? A : Q;           // M := copy of A lives in Q
     const int64_t lds = (z == 0) ? lda : ldq;
-    SF_CUDA(qr_panel<T>(n, w, src + z * lds, lds, Q + z * ldq, ldq, z, tol, mgsw, Cw, split, split_elems, fail, st));
+    {
+      ProfScope ps(1, 0.0, st);
+      SF_CUDA(qr_panel<T>(n, w, src + z * lds, lds, Q + z * ldq, ldq, z, tol, mgsw, Cw, split, split_elems, fail, st));
+    }
     const int64_t c = z + w;
     if (c < n) {  // flush: C = B_Q^T B_M, M[:, c:n] -= B_Q C over all rows
+      ProfScope ps(0, 4.0 * (double)n * (double)w * (double)(n - c), st);
       SF_CUDA(qr_project<T>(n, w, n - c, Q + z * ldq, ldq, src + c * lds, lds, Q + c * ldq, ldq, Cw, split,
                             split_elems, fail, st));
     }
@@ -293,6 +332,7 @@ static int qr_run(int64_t n, int64_t s, const T* A, int64_t lda, T* Q, int64_t l
   // R := Q^T A: upper triangle on the tensor cores, exact zeros below
   SF_CUDA(zero_strict_lower<T>(n, R, ldr, st));
   {
+    ProfScope ps(2, (double)n * (double)n * (double)(n + 1), st);
     Gemm<T> g{n, n, n, Q, ldq, 1, A, lda, 1, nullptr, 0, R, ldr, 1.0, 0, kMaskUpper, 1, nullptr, fail};
     SF_CUDA(run_gemm(g, st));
   }
@@ -368,6 +408,16 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
   const size_t bytes = elt * (size_t)n * (size_t)n;
   cudaStream_t st;
   SF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  {
+    // keep freed device blocks in the stream-ordered pool so repeated calls do not pay
+    // for fresh allocations
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   char* d = nullptr;
   const int nbuf = kind == 2 ? 3 : 1;
   cudaError_t e = cudaMallocAsync((void**)&d, nbuf * bytes + 256, st);
@@ -496,6 +546,23 @@ int64_t sf_flush_count(int64_t n, int64_t s) {
 }
 
 int64_t sf_launch_counter(void) { return g_launches.load(); }
+
+void sf_profile_enable(int on) { g_prof = on != 0; }
+
+int sf_profile_collect(double* ms, int64_t* count, double* flops) {
+  for (int k = 0; k < 3; ++k) { ms[k] = 0.0; count[k] = 0; flops[k] = 0.0; }
+  int rc = SF_OK;
+  for (auto& r : g_prof_recs) {
+    float t = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+    if (e != cudaSuccess) rc = fail_with(SF_ECUDA, "profile events: %s", cudaGetErrorString(e));
+    ms[r.kind] += t; count[r.kind] += 1; flops[r.kind] += r.flops;
+    g_event_pool.push_back(r.a); g_event_pool.push_back(r.b);
+  }
+  g_prof_recs.clear();
+  return rc;
+}
 
 const char* sf_strerror(int status) {
   switch (status) {
