@@ -74,8 +74,8 @@ static int fail_with(int code, const char* fmt, ...) {
 static int leaf_width() {
   static int w = [] {
     const char* e = getenv("SF_LEAF");
-    int v = e ? atoi(e) : 64;
-    if (v != 16 && v != 32 && v != 64) v = 64;
+    int v = e ? atoi(e) : 32;
+    if (v != 16 && v != 32) v = 32;
     return v;
   }();
   return w;
@@ -109,6 +109,46 @@ struct Workspace {
     if (base) cudaFreeAsync(base, st);
   }
 };
+
+// ------------------------------------------------------------------ lookahead streams
+// Panel p+1 is factored on a high-priority side stream while the rest of flush p runs on
+// the caller's stream (classic lookahead): the caller's stream first updates only the
+// columns of panel p+1, signals, then updates the remainder of the trailing matrix.
+static bool lookahead_on() {
+  static int on = [] { const char* e = getenv("SF_LOOKAHEAD"); return e ? atoi(e) : 1; }();
+  return on != 0;
+}
+struct Side {
+  cudaStream_t st = nullptr;
+  std::vector<cudaEvent_t> ev;
+  size_t next = 0;
+  // events are re-recorded round-robin: a stream wait captures the event's state at the
+  // time cudaStreamWaitEvent is called, so re-recording afterwards is safe
+  cudaEvent_t event() { return ev[next++ % ev.size()]; }
+};
+static cudaError_t side_stream(Side*& out) {
+  static Side sides[16];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  Side& sd = sides[dev & 15];
+  if (!sd.st) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    e = cudaStreamCreateWithPriority(&sd.st, cudaStreamNonBlocking, hi);
+    if (e != cudaSuccess) return e;
+    for (int i = 0; i < 8; ++i) { cudaEvent_t ev; cudaEventCreateWithFlags(&ev, cudaEventDisableTiming); sd.ev.push_back(ev); }
+  }
+  out = &sd;
+  return cudaSuccess;
+}
+// record on `from`, make `to` wait
+static cudaError_t fork_join(Side& sd, cudaStream_t from, cudaStream_t to) {
+  cudaEvent_t e = sd.event();
+  cudaError_t r = cudaEventRecord(e, from);
+  if (r != cudaSuccess) return r;
+  return cudaStreamWaitEvent(to, e, 0);
+}
 
 // ------------------------------------------------------------------ GEMM dispatch per dtype
 template <typename T>
@@ -160,21 +200,49 @@ static int chol_run(int64_t n, int64_t s, const T* A, int64_t lda, T* L, int64_t
                     cudaStream_t st) {
   Workspace ws;
   SF_CUDA(ws.init(4096, st));
-  long long* fail = ws.take<long long>(1);
+  long long* fail = ws.take<long long>(2);   // [0] first failed column, [1] leaf counter
   SF_CUDA(init_fail(fail, st));
+  Side* sd = nullptr;
+  const bool la = lookahead_on() && s < n;
+  if (la) SF_CUDA(side_stream(sd));
+  {
+    ProfScope ps(1, 0.0, st);
+    const int64_t w0 = s < n ? s : n;
+    SF_CUDA(chol_panel_rec<T>(n, w0, A, lda, L, ldl, 0, fail, st));
+  }
   for (int64_t z = 0; z < n; z += s) {
-    const int64_t w = (s < n - z) ? s : n - z, m = n - z;
+    const int64_t w = (s < n - z) ? s : n - z, c = z + w;
+    if (c >= n) break;
+    const int64_t w2 = (s < n - c) ? s : n - c, m = n - c;
     const T* src = (z == 0) ? A : L;
     const int64_t lds = (z == 0) ? lda : ldl;
-    {
+    const T* R = L + c + z * ldl;   // R = L[c:n, z:c)
+    if (la) {
+      {  // flush, part 1: the columns of the next panel
+        ProfScope ps(0, (double)w * ((double)m * (m + 1) - (double)(m - w2) * (m - w2 + 1)), st);
+        SF_CUDA(gemm_sub<T>(m, w2, w, R, ldl, 0, R, ldl, 0, src + c + c * lds, lds, L + c + c * ldl, ldl, kMaskLower,
+                            fail, st));
+      }
+      SF_CUDA(fork_join(*sd, st, sd->st));
+      {
+        ProfScope ps(1, 0.0, sd->st);
+        SF_CUDA(chol_panel_rec<T>(m, w2, L + c + c * ldl, ldl, L + c + c * ldl, ldl, c, fail, sd->st));
+      }
+      if (m > w2) {  // flush, part 2: the rest of the trailing matrix, concurrently with the panel
+        const int64_t c2 = c + w2;
+        ProfScope ps(0, (double)w * (double)(m - w2) * (double)(m - w2 + 1), st);
+        SF_CUDA(gemm_sub<T>(m - w2, m - w2, w, R + w2, ldl, 0, R + w2, ldl, 0, src + c2 + c2 * lds, lds,
+                            L + c2 + c2 * ldl, ldl, kMaskLower, fail, st));
+      }
+      SF_CUDA(fork_join(*sd, sd->st, st));
+    } else {
+      {  // flush: A[c:n,c:n] -= R R^T
+        ProfScope ps(0, (double)w * (double)m * (double)(m + 1), st);
+        SF_CUDA(gemm_sub<T>(m, m, w, R, ldl, 0, R, ldl, 0, src + c + c * lds, lds, L + c + c * ldl, ldl, kMaskLower,
+                            fail, st));
+      }
       ProfScope ps(1, 0.0, st);
-      SF_CUDA(chol_panel_rec<T>(m, w, src + z + z * lds, lds, L + z + z * ldl, ldl, z, fail, st));
-    }
-    const int64_t c = z + w;
-    if (c < n) {  // flush: A[c:n,c:n] -= R R^T, R = L[c:n, z:c)
-      ProfScope ps(0, (double)w * (double)(n - c) * (double)(n - c + 1), st);
-      SF_CUDA(gemm_sub<T>(n - c, n - c, w, L + c + z * ldl, ldl, 0, L + c + z * ldl, ldl, 0, src + c + c * lds, lds,
-                          L + c + c * ldl, ldl, kMaskLower, fail, st));
+      SF_CUDA(chol_panel_rec<T>(m, w2, L + c + c * ldl, ldl, L + c + c * ldl, ldl, c, fail, st));
     }
   }
   SF_CUDA(finish_info(fail, d_info, st));
@@ -208,24 +276,56 @@ static int lu_run(int64_t n, int64_t s, const T* A, int64_t lda, T* LU, int64_t 
                   cudaStream_t st) {
   Workspace ws;
   SF_CUDA(ws.init(16384, st));
-  long long* fail = ws.take<long long>(1);
+  long long* fail = ws.take<long long>(2);   // [0] first failed column, [1] leaf counter
   T* tol = ws.take<T>(1);
   double* part = ws.take<double>(512);
   SF_CUDA(init_fail(fail, st));
   SF_CUDA(frob_norm_tol<T>(n, A, lda, tol, part, st));
+  Side* sd = nullptr;
+  const bool la = lookahead_on() && s < n;
+  if (la) SF_CUDA(side_stream(sd));
+  {
+    ProfScope ps(1, 0.0, st);
+    const int64_t w0 = s < n ? s : n;
+    SF_CUDA(lu_panel_rec<T>(n, w0, n - w0, A, lda, LU, ldd, 0, tol, fail, st));
+  }
   for (int64_t z = 0; z < n; z += s) {
-    const int64_t w = (s < n - z) ? s : n - z, m = n - z, ncr = n - z - w;
+    const int64_t w = (s < n - z) ? s : n - z, c = z + w;
+    if (c >= n) break;
+    const int64_t w2 = (s < n - c) ? s : n - c, m = n - c;
     const T* src = (z == 0) ? A : LU;
     const int64_t lds = (z == 0) ? lda : ldd;
-    {
-      ProfScope ps(1, 0.0, st);
-      SF_CUDA(lu_panel_rec<T>(m, w, ncr, src + z + z * lds, lds, LU + z + z * ldd, ldd, z, tol, fail, st));
+    const T* RL = LU + c + z * ldd;   // R_L = L[c:n, z:c)
+    const T* RU = LU + z + c * ldd;   // R_U = U[z:c, c:n)
+    cudaStream_t pst = la ? sd->st : st;
+    if (la) {
+      ProfScope ps(0, 2.0 * w * ((double)m * m - (double)(m - w2) * (m - w2)), st);
+      // flush, part 1: columns [c, c+w2) (all rows >= c) and rows [c, c+w2) right of them
+      SF_CUDA(gemm_sub<T>(m, w2, w, RL, ldd, 0, RU, ldd, 1, src + c + c * lds, lds, LU + c + c * ldd, ldd, kMaskNone,
+                          fail, st));
+      if (m > w2) {
+        const int64_t c2 = c + w2;
+        SF_CUDA(gemm_sub<T>(w2, m - w2, w, RL, ldd, 0, RU + w2 * ldd, ldd, 1, src + c + c2 * lds, lds,
+                            LU + c + c2 * ldd, ldd, kMaskNone, fail, st));
+      }
+      SF_CUDA(fork_join(*sd, st, pst));
+    } else {
+      ProfScope ps(0, 2.0 * w * (double)m * (double)m, st);
+      SF_CUDA(gemm_sub<T>(m, m, w, RL, ldd, 0, RU, ldd, 1, src + c + c * lds, lds, LU + c + c * ldd, ldd, kMaskNone,
+                          fail, st));
     }
-    const int64_t c = z + w;
-    if (c < n) {  // flush: A[c:n,c:n] -= R_L R_U
-      ProfScope ps(0, 2.0 * (double)w * (double)(n - c) * (double)(n - c), st);
-      SF_CUDA(gemm_sub<T>(n - c, n - c, w, LU + c + z * ldd, ldd, 0, LU + z + c * ldd, ldd, 1, src + c + c * lds, lds,
-                          LU + c + c * ldd, ldd, kMaskNone, fail, st));
+    {
+      ProfScope ps(1, 0.0, pst);
+      SF_CUDA(lu_panel_rec<T>(m, w2, m - w2, LU + c + c * ldd, ldd, LU + c + c * ldd, ldd, c, tol, fail, pst));
+    }
+    if (la) {
+      if (m > w2) {  // flush, part 2: the remaining trailing block, concurrently with the panel
+        const int64_t c2 = c + w2;
+        ProfScope ps(0, 2.0 * w * (double)(m - w2) * (double)(m - w2), st);
+        SF_CUDA(gemm_sub<T>(m - w2, m - w2, w, RL + w2, ldd, 0, RU + w2 * ldd, ldd, 1, src + c2 + c2 * lds, lds,
+                            LU + c2 + c2 * ldd, ldd, kMaskNone, fail, st));
+      }
+      SF_CUDA(fork_join(*sd, pst, st));
     }
   }
   SF_CUDA(finish_info(fail, d_info, st));
@@ -306,7 +406,7 @@ static int qr_run(int64_t n, int64_t s, const T* A, int64_t lda, T* Q, int64_t l
   }
   Workspace ws;
   SF_CUDA(ws.init(sizeof(T) * (mgs_elems + cw_elems + split_elems) + 16384 + 4 * 256, st));
-  long long* fail = ws.take<long long>(1);
+  long long* fail = ws.take<long long>(2);   // [0] first failed column, [1] leaf counter
   T* tol = ws.take<T>(1);
   double* part = ws.take<double>(512);
   T* mgsw = ws.take<T>(mgs_elems);
@@ -470,7 +570,7 @@ int sf_chol_panel(int64_t m, int64_t w, int dtype, void* dP, int64_t ld, int64_t
   cudaStream_t st = (cudaStream_t)stream;
   Workspace ws;
   SF_CUDA(ws.init(256, st));
-  long long* fail = ws.take<long long>(1);
+  long long* fail = ws.take<long long>(2);   // [0] first failed column, [1] leaf counter
   SF_CUDA(init_fail(fail, st));
   SF_CUDA(chol_panel_rec<double>(m, w, (double*)dP, ld, (double*)dP, ld, col0, fail, st));
   SF_CUDA(finish_info(fail, d_info, st));
@@ -502,7 +602,7 @@ int sf_lu_panel(int64_t m, int64_t w, int64_t ncr, int dtype, void* dP, int64_t 
   cudaStream_t st = (cudaStream_t)stream;
   Workspace ws;
   SF_CUDA(ws.init(512, st));
-  long long* fail = ws.take<long long>(1);
+  long long* fail = ws.take<long long>(2);   // [0] first failed column, [1] leaf counter
   double* dtol = ws.take<double>(1);
   SF_CUDA(init_fail(fail, st));
   SF_CUDA(cudaMemcpyAsync(dtol, &tol, sizeof(double), cudaMemcpyHostToDevice, st));
@@ -524,7 +624,7 @@ int sf_qr_panel(int64_t n, int64_t w, int dtype, void* dV, int64_t ld, int64_t c
   const size_t mgs = qr_mgs_work_elems(n, (int)wcap) + 64;
   Workspace ws;
   SF_CUDA(ws.init(8 * (mgs + w * wcap + split_elems) + 4096, st));
-  long long* fail = ws.take<long long>(1);
+  long long* fail = ws.take<long long>(2);   // [0] first failed column, [1] leaf counter
   double* dtol = ws.take<double>(1);
   double* mgsw = ws.take<double>(mgs);
   double* Cw = ws.take<double>(w * wcap);

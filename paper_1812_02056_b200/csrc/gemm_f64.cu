@@ -6,69 +6,70 @@
 //   LU flush         A[c:n,c:n] -= R_L R_U
 //   QR flush         C = B_Q^T B_M ; M[:,c:n] -= B_Q C
 //   QR R             R = Q^T A  (upper tiles only)
-//   in-panel corrections of the nested sub-panels (same formulas, narrower N).
-// The product S is never materialised: each 128x128 tile of C is read, decremented by
-// the register accumulator and written once (Cin may differ from C: out-of-place first
-// step).  MASK restricts work to the lower (Cholesky) or upper (R) triangle of C.
+//   in-panel corrections of the recursive panel (same formulas, narrower N).
+// The product S is never materialised: each 128x128 tile of C is read, decremented by the
+// accumulator and written once (Cin may differ from C: out-of-place first step).  MASK
+// restricts work to the lower (Cholesky) or upper (R) triangle of C.
 //
 // Design (DESIGN.md §5 K1/K2): 256 threads = 8 warps as 2 (i) x 4 (j); warp tile 64x32 =
-// 8x4 DMMA atoms; 4-stage cp.async pipeline of 128x16 operand slices; smem layouts padded
-// so every fragment load is bank-conflict free; C tile prefetched into L2 during the
-// mainloop.  The D fragment is used transposed (D = C^T) so each lane owns two
-// consecutive rows of a column-major C.
+// 8x4 DMMA atoms (64 fp64 accumulators per lane); 3-stage cp.async pipeline of 128x32
+// operand slices (smem layouts padded so every fragment load is bank-conflict free); the
+// D fragment is used transposed (D = C^T).  Epilogue: the accumulator tile is parked in
+// the (now idle) pipeline shared memory, then every warp streams whole 1 KB columns of C:
+// all loads of a thread are issued before the first store, in 16-byte vectors, so the
+// read-modify-write costs about one L2/HBM round trip per tile instead of one per atom.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace sf {
 
 namespace g64 {
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 256;
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, THREADS = 256;
 constexpr int PAD_IK = BM + 4;    // smem row stride (doubles) for idx-contiguous slices
-constexpr int PAD_KI = BK + 4;    // smem row stride for k-contiguous slices
-constexpr int OPER = (BK * PAD_IK > BM * PAD_KI) ? BK * PAD_IK : BM * PAD_KI;  // 2560
-constexpr size_t SMEM = sizeof(double) * (size_t)OPER * 2 * STAGES;           // 160 KiB
+constexpr int PAD_KI = BK + 4;    // smem row stride for k-contiguous slices (== 4 mod 16)
+constexpr int OPER = (BK * PAD_IK > BM * PAD_KI) ? BK * PAD_IK : BM * PAD_KI;  // 4608
+constexpr int CPAD = BM + 2;      // epilogue staging column stride
+constexpr size_t SMEM_PIPE = sizeof(double) * (size_t)OPER * 2 * STAGES;      // 216 KiB
+constexpr size_t SMEM_EPI = sizeof(double) * (size_t)BN * CPAD;              // 130 KiB
+constexpr size_t SMEM = SMEM_PIPE > SMEM_EPI ? SMEM_PIPE : SMEM_EPI;
+constexpr int CHUNKS = BM * BK / 2 / THREADS;   // 16-byte chunks per thread per operand slice
 }  // namespace g64
 
-// Load a 128 (idx) x 16 (k) slice of op(X) into shared memory.
+// Load a 128 (idx) x 32 (k) slice of op(X) into shared memory.
 //  KC=false: op(X)(idx,k) = X[idx + k*ld]  (idx contiguous)  -> Xs[k*PAD_IK + idx]
 //  KC=true : op(X)(idx,k) = X[k + idx*ld]  (k contiguous)    -> Xs[idx*PAD_KI + k]
 template <bool KC, bool V16>
 __device__ __forceinline__ void load_slice(double* Xs, const double* __restrict__ X, int64_t ld,
-                                           int64_t idx0, int64_t nidx, int64_t k0, int64_t K,
-                                           int tid) {
+                                           int64_t idx0, int64_t nidx, int64_t k0, int64_t K, int tid) {
   using namespace g64;
-  if (!KC) {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int id = tid + r * THREADS;
-      const int kk = id >> 6, ch = id & 63;
-      const int64_t idx = idx0 + 2 * ch, kg = k0 + kk;
-      double* dst = Xs + kk * PAD_IK + 2 * ch;
+  for (int r = 0; r < CHUNKS; ++r) {
+    const int id = tid + r * THREADS;
+    int64_t idx, kg;
+    double* dst;
+    if (!KC) {
+      const int kk = id / (BM / 2), ch = id % (BM / 2);
+      idx = idx0 + 2 * ch; kg = k0 + kk;
+      dst = Xs + kk * PAD_IK + 2 * ch;
       const bool kin = kg < K;
       if (V16) {
-        int bytes = (!kin || idx >= nidx) ? 0 : (idx + 1 >= nidx ? 8 : 16);
-        const double* src = bytes ? X + idx + kg * ld : X;
-        cp_async16(dst, src, bytes);
+        const int bytes = (!kin || idx >= nidx) ? 0 : (idx + 1 >= nidx ? 8 : 16);
+        cp_async16(dst, bytes ? X + idx + kg * ld : X, bytes);
       } else {
-        int b0 = (kin && idx < nidx) ? 8 : 0, b1 = (kin && idx + 1 < nidx) ? 8 : 0;
+        const int b0 = (kin && idx < nidx) ? 8 : 0, b1 = (kin && idx + 1 < nidx) ? 8 : 0;
         cp_async8(dst, b0 ? X + idx + kg * ld : X, b0);
         cp_async8(dst + 1, b1 ? X + idx + 1 + kg * ld : X, b1);
       }
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int id = tid + r * THREADS;
-      const int ii = id >> 3, ch = id & 7;
-      const int64_t idx = idx0 + ii, kg = k0 + 2 * ch;
-      double* dst = Xs + ii * PAD_KI + 2 * ch;
+    } else {
+      const int ii = id / (BK / 2), ch = id % (BK / 2);
+      idx = idx0 + ii; kg = k0 + 2 * ch;
+      dst = Xs + ii * PAD_KI + 2 * ch;
       const bool iin = idx < nidx;
       if (V16) {
-        int bytes = (!iin || kg >= K) ? 0 : (kg + 1 >= K ? 8 : 16);
-        const double* src = bytes ? X + kg + idx * ld : X;
-        cp_async16(dst, src, bytes);
+        const int bytes = (!iin || kg >= K) ? 0 : (kg + 1 >= K ? 8 : 16);
+        cp_async16(dst, bytes ? X + kg + idx * ld : X, bytes);
       } else {
-        int b0 = (iin && kg < K) ? 8 : 0, b1 = (iin && kg + 1 < K) ? 8 : 0;
+        const int b0 = (iin && kg < K) ? 8 : 0, b1 = (iin && kg + 1 < K) ? 8 : 0;
         cp_async8(dst, b0 ? X + kg + idx * ld : X, b0);
         cp_async8(dst + 1, b1 ? X + kg + 1 + idx * ld : X, b1);
       }
@@ -99,7 +100,7 @@ __device__ __forceinline__ void tile_of(int bid, int TM, int TN, int& ti, int& t
 }
 
 template <bool AK, bool BKC, bool V16, int MASK>
-__global__ void __launch_bounds__(g64::THREADS, 1) gemm_f64_kernel(GemmF64 p) {
+__global__ void __launch_bounds__(g64::THREADS, 1) gemm_f64_kernel(GemmF64 p, int vecC) {
   using namespace g64;
   if (p.fail && failed(p.fail)) return;
   extern __shared__ __align__(16) double smem[];
@@ -156,43 +157,101 @@ __global__ void __launch_bounds__(g64::THREADS, 1) gemm_f64_kernel(GemmF64 p) {
     issue(kb + STAGES - 1);
     const double* as = As + (kb % STAGES) * OPER;
     const double* bs = Bs + (kb % STAGES) * OPER;
+    double fa[2][8], fb[2][4];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) fa[0][a] = frag<AK>(as, wm * 64 + a * 8, 0, lane);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) fb[0][b] = frag<BKC>(bs, wn * 32 + b * 8, 0, lane);
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
-      double fa[8], fb[4];
+      const int cur = kk & 1, nxt = cur ^ 1;
+      if (kk + 1 < BK / 4) {
 #pragma unroll
-      for (int a = 0; a < 8; ++a) fa[a] = frag<AK>(as, wm * 64 + a * 8, kk, lane);
+        for (int a = 0; a < 8; ++a) fa[nxt][a] = frag<AK>(as, wm * 64 + a * 8, kk + 1, lane);
 #pragma unroll
-      for (int b = 0; b < 4; ++b) fb[b] = frag<BKC>(bs, wn * 32 + b * 8, kk, lane);
+        for (int b = 0; b < 4; ++b) fb[nxt][b] = frag<BKC>(bs, wn * 32 + b * 8, kk + 1, lane);
+      }
 #pragma unroll
       for (int a = 0; a < 8; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b)
           // D = C^T: the MMA's A operand is op(B) (rows j), its B operand is op(A) (cols i)
-          dmma_8x8x4(acc[a][b][0], acc[a][b][1], fb[b], fa[a]);
+          dmma_8x8x4(acc[a][b][0], acc[a][b][1], fb[cur][b], fa[cur][a]);
     }
   }
   cp_async_wait<0>();
+  __syncthreads();
 
-  // Epilogue: lane owns C(i, j) for i = ibase + {0,1}, j = jbase.
+  // ---- epilogue, step 1: park the accumulator tile in shared memory, Cs[j*CPAD + i]
+  double* Cs = smem;
 #pragma unroll
   for (int a = 0; a < 8; ++a) {
-    const int64_t i = i0 + wm * 64 + a * 8 + 2 * (lane & 3);
+    const int il = wm * 64 + a * 8 + 2 * (lane & 3);
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int64_t j = j0 + wn * 32 + b * 8 + (lane >> 2);
-      if (j >= p.N) continue;
+      const int jl = wn * 32 + b * 8 + (lane >> 2);
+      *reinterpret_cast<double2*>(Cs + jl * CPAD + il) = make_double2(acc[a][b][0], acc[a][b][1]);
+    }
+  }
+  __syncthreads();
+
+  // ---- step 2: each warp streams 16 whole columns; lane owns rows 2*lane+{0,1} and
+  //      64+2*lane+{0,1} (each warp instruction covers 512 contiguous bytes of a column)
+  constexpr int COLS = BN / 8;
+  if (p.splits > 1) {
+    double* W = p.work + (int64_t)sp * p.M * p.N;
+    for (int q = 0; q < COLS; ++q) {
+      const int jl = warp * COLS + q;
+      const int64_t j = j0 + jl;
+      if (j >= p.N) break;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int64_t ie = i + e;
-        if (ie >= p.M) continue;
-        if (MASK == kMaskLower && ie < j) continue;
-        if (MASK == kMaskUpper && ie > j) continue;
-        if (p.splits > 1) {
-          p.work[(int64_t)sp * p.M * p.N + j * p.M + ie] = acc[a][b][e];
-        } else {
-          const double v = p.alpha * acc[a][b][e];
-          p.C[ie + j * p.ldc] = p.beta ? p.Cin[ie + j * p.ldcin] + v : v;
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int il = 64 * h + 2 * lane + e;
+          if (i0 + il < p.M) W[j * p.M + i0 + il] = Cs[jl * CPAD + il];
         }
+    }
+    return;
+  }
+  double cin[COLS][2][2];
+  if (p.beta) {
+#pragma unroll
+    for (int q = 0; q < COLS; ++q) {
+      const int64_t j = j0 + warp * COLS + q;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t i = i0 + 64 * h + 2 * lane;
+        const double* src = p.Cin + i + j * p.ldcin;
+        if (vecC && j < p.N && i + 1 < p.M) {
+          const double2 v = __ldcs(reinterpret_cast<const double2*>(src));
+          cin[q][h][0] = v.x; cin[q][h][1] = v.y;
+        } else {
+          cin[q][h][0] = (j < p.N && i < p.M) ? src[0] : 0.0;
+          cin[q][h][1] = (j < p.N && i + 1 < p.M) ? src[1] : 0.0;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < COLS; ++q) {
+    const int jl = warp * COLS + q;
+    const int64_t j = j0 + jl;
+    if (j >= p.N) break;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int il = 64 * h + 2 * lane;
+      const int64_t i = i0 + il;
+      const double2 d = *reinterpret_cast<const double2*>(Cs + jl * CPAD + il);
+      double v0 = p.alpha * d.x, v1 = p.alpha * d.y;
+      if (p.beta) { v0 += cin[q][h][0]; v1 += cin[q][h][1]; }
+      double* dst = p.C + i + j * p.ldc;
+      const bool pair_in = (i + 1 < p.M) && (MASK == kMaskNone || (MASK == kMaskLower ? i >= j : i + 1 <= j));
+      if (pair_in && vecC) {
+        __stcs(reinterpret_cast<double2*>(dst), make_double2(v0, v1));
+      } else {
+        if (i < p.M && (MASK == kMaskNone || (MASK == kMaskLower ? i >= j : i <= j))) dst[0] = v0;
+        if (i + 1 < p.M && (MASK == kMaskNone || (MASK == kMaskLower ? i + 1 >= j : i + 1 <= j))) dst[1] = v1;
       }
     }
   }
@@ -213,7 +272,7 @@ __global__ void splitk_reduce_f64(GemmF64 p) {
 }
 
 template <bool AK, bool BKC, bool V16, int MASK>
-static cudaError_t launch_t(const GemmF64& p, int ntiles, cudaStream_t st) {
+static cudaError_t launch_t(const GemmF64& p, int ntiles, int vecC, cudaStream_t st) {
   auto k = gemm_f64_kernel<AK, BKC, V16, MASK>;
   static bool attr_set = false;  // per template instance
   if (!attr_set) {
@@ -222,16 +281,17 @@ static cudaError_t launch_t(const GemmF64& p, int ntiles, cudaStream_t st) {
     attr_set = true;
   }
   dim3 grid(ntiles, p.splits);
-  k<<<grid, g64::THREADS, g64::SMEM, st>>>(p); count_launch();
+  k<<<grid, g64::THREADS, g64::SMEM, st>>>(p, vecC);
+  count_launch();
   return cudaGetLastError();
 }
 
 template <bool AK, bool BKC, bool V16>
-static cudaError_t launch_mask(const GemmF64& p, int mask, int ntiles, cudaStream_t st) {
+static cudaError_t launch_mask(const GemmF64& p, int mask, int ntiles, int vecC, cudaStream_t st) {
   switch (mask) {
-    case kMaskLower: return launch_t<AK, BKC, V16, kMaskLower>(p, ntiles, st);
-    case kMaskUpper: return launch_t<AK, BKC, V16, kMaskUpper>(p, ntiles, st);
-    default: return launch_t<AK, BKC, V16, kMaskNone>(p, ntiles, st);
+    case kMaskLower: return launch_t<AK, BKC, V16, kMaskLower>(p, ntiles, vecC, st);
+    case kMaskUpper: return launch_t<AK, BKC, V16, kMaskUpper>(p, ntiles, vecC, st);
+    default: return launch_t<AK, BKC, V16, kMaskNone>(p, ntiles, vecC, st);
   }
 }
 
@@ -254,23 +314,25 @@ cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStre
   else ntiles = TM * TN;
   if (ntiles == 0) return cudaSuccess;
   const bool v16 = aligned16(p.A, p.lda) && aligned16(p.B, p.ldb);
+  const int vecC = aligned16(p.C, p.ldc) && (!p.beta || aligned16(p.Cin, p.ldcin));
   cudaError_t e;
   const int key = (a_kcontig ? 1 : 0) | (b_kcontig ? 2 : 0) | (v16 ? 4 : 0);
   switch (key) {
-    case 0: e = launch_mask<false, false, false>(p, mask, ntiles, st); break;
-    case 1: e = launch_mask<true, false, false>(p, mask, ntiles, st); break;
-    case 2: e = launch_mask<false, true, false>(p, mask, ntiles, st); break;
-    case 3: e = launch_mask<true, true, false>(p, mask, ntiles, st); break;
-    case 4: e = launch_mask<false, false, true>(p, mask, ntiles, st); break;
-    case 5: e = launch_mask<true, false, true>(p, mask, ntiles, st); break;
-    case 6: e = launch_mask<false, true, true>(p, mask, ntiles, st); break;
-    default: e = launch_mask<true, true, true>(p, mask, ntiles, st); break;
+    case 0: e = launch_mask<false, false, false>(p, mask, ntiles, vecC, st); break;
+    case 1: e = launch_mask<true, false, false>(p, mask, ntiles, vecC, st); break;
+    case 2: e = launch_mask<false, true, false>(p, mask, ntiles, vecC, st); break;
+    case 3: e = launch_mask<true, true, false>(p, mask, ntiles, vecC, st); break;
+    case 4: e = launch_mask<false, false, true>(p, mask, ntiles, vecC, st); break;
+    case 5: e = launch_mask<true, false, true>(p, mask, ntiles, vecC, st); break;
+    case 6: e = launch_mask<false, true, true>(p, mask, ntiles, vecC, st); break;
+    default: e = launch_mask<true, true, true>(p, mask, ntiles, vecC, st); break;
   }
   if (e != cudaSuccess || p.splits == 1) return e;
   const int64_t total = p.M * p.N;
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  splitk_reduce_f64<<<blocks, 256, 0, st>>>(p); count_launch();
+  splitk_reduce_f64<<<blocks, 256, 0, st>>>(p);
+  count_launch();
   return cudaGetLastError();
 }
 

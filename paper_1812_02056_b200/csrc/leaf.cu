@@ -1,0 +1,281 @@
+// leaf.cu — the innermost panel recurrences (W <= 32 columns) of Algorithms 1 and 2.
+//
+// Cholesky, for each column c of the leaf:
+//     L_cc = sqrt(A_cc - sum_{k<c} L_ck^2),    L_ic = (A_ic - sum_{k<c} L_ik L_ck) / L_cc
+// LU, Crout form, for each column/row c:
+//     L_ic = A_ic - sum_{k<c} L_ik U_kc   (i >= c),   U_ci = (A_ci - sum_{k<c} L_ck U_ki) / L_cc  (i > c)
+// (the sums over earlier columns of the same panel / earlier panels were already applied by
+// the driver's grouped corrections and by the flushes).
+//
+// GPU structure.  Every CTA first factors the w x w diagonal block with ONE warp, lane i
+// holding row i (and for LU also column i) in registers; the k-sums read the pivot row's
+// entries with warp shuffles, so a column step costs c shuffles + FMAs and one sqrt /
+// division, with no shared-memory round trips or barriers.  The finished block is
+// published to shared memory and then every thread of the CTA runs an independent
+// substitution for one row below the block (coalesced: the matrix is column-major) — or,
+// for LU's U part, for one column to the right (staged through shared memory so the
+// column's w contiguous entries are loaded and stored coalesced).
+// The diagonal factorization is repeated by every CTA (~1-2 us) instead of a grid-wide
+// dependency; CTA 0 writes it out.
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace sf {
+
+constexpr int kLeafT = 128;
+constexpr int kUCols = 64;   // U columns per CTA (static smem budget)
+constexpr unsigned kFull = 0xffffffffu;
+
+template <typename T> __device__ __forceinline__ T leaf_sqrt(T x);
+template <> __device__ __forceinline__ double leaf_sqrt<double>(double x) { return sqrt(x); }
+template <> __device__ __forceinline__ float leaf_sqrt<float>(float x) { return sqrtf(x); }
+
+__device__ __forceinline__ void leaf_fail(long long* fail, long long col1) {
+  atomicMin((unsigned long long*)fail, (unsigned long long)col1);
+}
+
+// True in exactly one CTA of the grid: the last one to arrive (all others have finished
+// reading the diagonal block).  Resets the counter for the next launch on the stream.
+__device__ __forceinline__ bool last_reader(long long* counter) {
+  __shared__ int last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long old = atomicAdd((unsigned long long*)counter, 1ull);
+    last = (old == gridDim.x - 1);
+    if (last) *counter = 0;
+  }
+  __syncthreads();
+  return last;
+}
+
+// ------------------------------------------------------------------ Cholesky
+template <typename T, int W>
+__global__ void __launch_bounds__(kLeafT) chol_leaf_kernel(int64_t m, int w, const T* __restrict__ src, int64_t lds,
+                                                           T* __restrict__ dst, int64_t ldd, int64_t col0,
+                                                           long long* fail) {
+  if (failed(fail)) return;
+  __shared__ T Ls[W][W + 1];
+  __shared__ T inv[W];
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 32) {
+    T x[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) x[k] = (lane < w && k <= lane && k < w) ? src[lane + (int64_t)k * lds] : T(0);
+    int ok = 1;
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      if (c < w && ok) {
+        T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
+#pragma unroll
+        for (int k = 0; k < c; ++k) {
+          const T lck = __shfl_sync(kFull, x[k], c);
+          if ((k & 3) == 0) a0 = fma(-x[k], lck, a0);
+          else if ((k & 3) == 1) a1 = fma(-x[k], lck, a1);
+          else if ((k & 3) == 2) a2 = fma(-x[k], lck, a2);
+          else a3 = fma(-x[k], lck, a3);
+        }
+        const T t = (a0 + a1) + (a2 + a3);
+        const T d = __shfl_sync(kFull, t, c);
+        if (!(d > T(0))) {
+          ok = 0;
+          if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
+        } else {
+          const T Lcc = leaf_sqrt(d);
+          if (lane == c) x[c] = Lcc;
+          else if (lane > c) x[c] = t / Lcc;
+          if (lane == 0) inv[c] = T(1) / Lcc;
+        }
+      }
+    }
+#pragma unroll
+    if (lane < W)
+      for (int k = 0; k < W; ++k) Ls[lane][k] = x[k];
+    if (lane == 0) bad = !ok;
+  }
+  __syncthreads();
+  if (bad) return;
+  // The diagonal block is read by every CTA (redundant factorization) and may be
+  // overwritten in place: the LAST CTA to have read it writes the result out.
+  if (last_reader(fail + 1)) {
+    for (int idx = tid; idx < w * w; idx += kLeafT) {
+      const int i = idx % w, k = idx / w;
+      if (k <= i) dst[i + (int64_t)k * ldd] = Ls[i][k];
+    }
+  }
+  const int64_t r = w + (int64_t)blockIdx.x * kLeafT + tid;
+  if (r >= m) return;
+  T x[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) x[k] = (k < w) ? src[r + (int64_t)k * lds] : T(0);
+#pragma unroll
+  for (int c = 0; c < W; ++c) {
+    T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
+#pragma unroll
+    for (int k = 0; k < c; ++k) {
+      if ((k & 3) == 0) a0 = fma(-x[k], Ls[c][k], a0);
+      else if ((k & 3) == 1) a1 = fma(-x[k], Ls[c][k], a1);
+      else if ((k & 3) == 2) a2 = fma(-x[k], Ls[c][k], a2);
+      else a3 = fma(-x[k], Ls[c][k], a3);
+    }
+    x[c] = ((a0 + a1) + (a2 + a3)) * inv[c];
+  }
+#pragma unroll
+  for (int k = 0; k < W; ++k)
+    if (k < w) dst[r + (int64_t)k * ldd] = x[k];
+}
+
+template <typename T>
+cudaError_t chol_leaf(int64_t m, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
+                      long long* fail, cudaStream_t st) {
+  if (w <= 0 || m <= 0) return cudaSuccess;
+  const int64_t below = m - w;
+  const int grid = below > 0 ? (int)((below + kLeafT - 1) / kLeafT) : 1;
+  if (w <= 16) chol_leaf_kernel<T, 16><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+  else if (w <= 32) chol_leaf_kernel<T, 32><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+  else return cudaErrorInvalidValue;
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ LU
+template <typename T, int W>
+__global__ void __launch_bounds__(kLeafT) lu_leaf_kernel(int64_t m, int64_t ncr, int w, const T* __restrict__ src,
+                                                         int64_t lds, T* __restrict__ dst, int64_t ldd, int64_t col0,
+                                                         const T* tolp, long long* fail, int nrow_blocks) {
+  if (failed(fail)) return;
+  __shared__ T Ls[W][W + 1];     // L11 (row-major: Ls[c][k] = L_ck)
+  __shared__ T Us[W][W + 1];     // U11 (Us[k][c] = U_kc)
+  __shared__ T inv[W];
+  __shared__ T S[kUCols][W + 1]; // staging for the U columns
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 32) {
+    const T tol = *tolp;
+    T x[W], y[W];   // lane i: row i (x) and column i (y) of the diagonal block
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const bool in = lane < w && k < w;
+      x[k] = in ? src[lane + (int64_t)k * lds] : T(0);
+      y[k] = in ? src[k + (int64_t)lane * lds] : T(0);
+    }
+    int ok = 1;
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      if (c < w && ok) {
+        T a0 = x[c], a1 = T(0), b0 = y[c], b1 = T(0);
+#pragma unroll
+        for (int k = 0; k < c; ++k) {
+          const T ukc = __shfl_sync(kFull, y[k], c);   // U_kc: column c lives in lane c
+          const T lck = __shfl_sync(kFull, x[k], c);   // L_ck: row c lives in lane c
+          if (k & 1) { a1 = fma(-x[k], ukc, a1); b1 = fma(-lck, y[k], b1); }
+          else { a0 = fma(-x[k], ukc, a0); b0 = fma(-lck, y[k], b0); }
+        }
+        const T t = a0 + a1, u = b0 + b1;
+        const T Lcc = __shfl_sync(kFull, t, c);
+        if (!(fabs(Lcc) >= tol)) {
+          ok = 0;
+          if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
+        } else {
+          if (lane >= c) x[c] = t;
+          if (lane > c) y[c] = u / Lcc;
+          if (lane == 0) inv[c] = T(1) / Lcc;
+        }
+      }
+    }
+#pragma unroll
+    if (lane < W)
+      for (int k = 0; k < W; ++k) { Ls[lane][k] = x[k]; Us[k][lane] = y[k]; }
+    if (lane == 0) bad = !ok;
+  }
+  __syncthreads();
+  if (bad) return;
+  if (last_reader(fail + 1)) {   // see chol_leaf_kernel
+    for (int idx = tid; idx < w * w; idx += kLeafT) {
+      const int i = idx % w, k = idx / w;
+      dst[i + (int64_t)k * ldd] = (k <= i) ? Ls[i][k] : Us[i][k];   // L incl. diagonal / U strict upper
+    }
+  }
+  if ((int)blockIdx.x < nrow_blocks) {
+    // L rows below: L_rc = A_rc - sum_{k<c} L_rk U_kc
+    const int64_t r = w + (int64_t)blockIdx.x * kLeafT + tid;
+    if (r >= m) return;
+    T x[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) x[k] = (k < w) ? src[r + (int64_t)k * lds] : T(0);
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
+#pragma unroll
+      for (int k = 0; k < c; ++k) {
+        if ((k & 3) == 0) a0 = fma(-x[k], Us[k][c], a0);
+        else if ((k & 3) == 1) a1 = fma(-x[k], Us[k][c], a1);
+        else if ((k & 3) == 2) a2 = fma(-x[k], Us[k][c], a2);
+        else a3 = fma(-x[k], Us[k][c], a3);
+      }
+      x[c] = (a0 + a1) + (a2 + a3);
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+      if (k < w) dst[r + (int64_t)k * ldd] = x[k];
+    return;
+  }
+  // U columns to the right: U_cj = (A_cj - sum_{k<c} L_ck U_kj) / L_cc
+  const int64_t j0 = w + (int64_t)(blockIdx.x - nrow_blocks) * kUCols;
+  const int ncols = (int)((w + ncr - j0) < kUCols ? (w + ncr - j0) : kUCols);
+  const int warp = tid >> 5;
+  for (int jj = warp; jj < ncols; jj += kLeafT / 32)
+    if (lane < w) S[jj][lane] = src[lane + (j0 + jj) * lds];
+  __syncthreads();
+  if (tid < ncols) {
+    T y[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) y[k] = (k < w) ? S[tid][k] : T(0);
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      T a0 = y[c], a1 = T(0), a2 = T(0), a3 = T(0);
+#pragma unroll
+      for (int k = 0; k < c; ++k) {
+        if ((k & 3) == 0) a0 = fma(-Ls[c][k], y[k], a0);
+        else if ((k & 3) == 1) a1 = fma(-Ls[c][k], y[k], a1);
+        else if ((k & 3) == 2) a2 = fma(-Ls[c][k], y[k], a2);
+        else a3 = fma(-Ls[c][k], y[k], a3);
+      }
+      y[c] = ((a0 + a1) + (a2 + a3)) * inv[c];
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) S[tid][k] = y[k];
+  }
+  __syncthreads();
+  for (int jj = warp; jj < ncols; jj += kLeafT / 32)
+    if (lane < w) dst[lane + (j0 + jj) * ldd] = S[jj][lane];
+}
+
+template <typename T>
+cudaError_t lu_leaf(int64_t m, int64_t ncr, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
+                    const T* tol, long long* fail, cudaStream_t st) {
+  if (w <= 0 || m <= 0) return cudaSuccess;
+  const int64_t below = m - w;
+  const int nrb = below > 0 ? (int)((below + kLeafT - 1) / kLeafT) : 0;
+  const int ncb = ncr > 0 ? (int)((ncr + kUCols - 1) / kUCols) : 0;
+  int grid = nrb + ncb;
+  if (grid == 0) grid = 1;
+  if (w <= 16) lu_leaf_kernel<T, 16><<<grid, kLeafT, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
+  else if (w <= 32) lu_leaf_kernel<T, 32><<<grid, kLeafT, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
+  else return cudaErrorInvalidValue;
+  count_launch();
+  return cudaGetLastError();
+}
+
+template cudaError_t chol_leaf<double>(int64_t, int, const double*, int64_t, double*, int64_t, int64_t, long long*,
+                                       cudaStream_t);
+template cudaError_t chol_leaf<float>(int64_t, int, const float*, int64_t, float*, int64_t, int64_t, long long*,
+                                      cudaStream_t);
+template cudaError_t lu_leaf<double>(int64_t, int64_t, int, const double*, int64_t, double*, int64_t, int64_t,
+                                     const double*, long long*, cudaStream_t);
+template cudaError_t lu_leaf<float>(int64_t, int64_t, int, const float*, int64_t, float*, int64_t, int64_t,
+                                    const float*, long long*, cudaStream_t);
+
+}  // namespace sf

@@ -38,249 +38,6 @@ __device__ __forceinline__ void record_fail(long long* fail, long long col1) {
   atomicMin((unsigned long long*)fail, (unsigned long long)col1);
 }
 
-// =============================================================== Cholesky leaf
-constexpr int kLeafThreads = 128;
-
-template <typename T, int W>
-__global__ void __launch_bounds__(kLeafThreads) chol_leaf_kernel(int64_t m, int w, const T* __restrict__ src,
-                                                                 int64_t lds, T* __restrict__ dst, int64_t ldd,
-                                                                 int64_t col0, long long* fail) {
-  if (failed(fail)) return;
-  __shared__ T D[W][W + 1];
-  __shared__ T inv[W];
-  __shared__ int bad;
-  const int tid = threadIdx.x, lane = tid & 31;
-  if (tid == 0) bad = 0;
-  for (int idx = tid; idx < w * w; idx += kLeafThreads) {
-    const int i = idx % w, j = idx / w;
-    if (i >= j) D[i][j] = src[i + (int64_t)j * lds];
-  }
-  __syncthreads();
-  if (tid < 32) {
-    // one warp; lane owns rows lane and lane+32 (W <= 64)
-    for (int c = 0; c < w; ++c) {
-      T t[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int i = lane + 32 * h;
-        t[h] = T(0);
-        if (i >= c && i < w) {
-          T a0 = D[i][c], a1 = T(0), a2 = T(0), a3 = T(0);
-          int k = 0;
-          for (; k + 4 <= c; k += 4) {
-            a0 = fma(-D[i][k], D[c][k], a0);
-            a1 = fma(-D[i][k + 1], D[c][k + 1], a1);
-            a2 = fma(-D[i][k + 2], D[c][k + 2], a2);
-            a3 = fma(-D[i][k + 3], D[c][k + 3], a3);
-          }
-          for (; k < c; ++k) a0 = fma(-D[i][k], D[c][k], a0);
-          t[h] = (a0 + a1) + (a2 + a3);
-        }
-      }
-      const T d = __shfl_sync(0xffffffffu, (c >> 5) ? t[1] : t[0], c & 31);
-      if (!(d > T(0))) {  // not positive definite (or NaN) at column col0 + c
-        if (lane == 0) { bad = 1; if (blockIdx.x == 0) record_fail(fail, col0 + c + 1); }
-        break;
-      }
-      const T Lcc = dsqrt(d);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int i = lane + 32 * h;
-        if (i == c) D[c][c] = Lcc;
-        else if (i > c && i < w) D[i][c] = t[h] / Lcc;
-      }
-      if (lane == 0) inv[c] = T(1) / Lcc;
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  if (bad) return;
-  if (blockIdx.x == 0) {
-    for (int idx = tid; idx < w * w; idx += kLeafThreads) {
-      const int i = idx % w, j = idx / w;
-      if (i >= j) dst[i + (int64_t)j * ldd] = D[i][j];
-    }
-  }
-  // rows below the diagonal block: independent forward substitutions
-  const int64_t r = w + (int64_t)blockIdx.x * kLeafThreads + tid;
-  if (r >= m) return;
-  T x[W];
-#pragma unroll
-  for (int k = 0; k < W; ++k) x[k] = (k < w) ? src[r + (int64_t)k * lds] : T(0);
-#pragma unroll
-  for (int c = 0; c < W; ++c) {
-    if (c < w) {
-      T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
-#pragma unroll
-      for (int k = 0; k + 4 <= c; k += 4) {
-        a0 = fma(-x[k], D[c][k], a0);
-        a1 = fma(-x[k + 1], D[c][k + 1], a1);
-        a2 = fma(-x[k + 2], D[c][k + 2], a2);
-        a3 = fma(-x[k + 3], D[c][k + 3], a3);
-      }
-#pragma unroll
-      for (int k = c & ~3; k < c; ++k) a0 = fma(-x[k], D[c][k], a0);
-      x[c] = ((a0 + a1) + (a2 + a3)) * inv[c];
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < W; ++k)
-    if (k < w) dst[r + (int64_t)k * ldd] = x[k];
-}
-
-template <typename T>
-cudaError_t chol_leaf(int64_t m, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
-                      long long* fail, cudaStream_t st) {
-  if (w <= 0 || m <= 0) return cudaSuccess;
-  const int64_t below = m - w;
-  const int grid = below > 0 ? (int)((below + kLeafThreads - 1) / kLeafThreads) : 1;
-  if (w <= 16) chol_leaf_kernel<T, 16><<<grid, kLeafThreads, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-  else if (w <= 32) chol_leaf_kernel<T, 32><<<grid, kLeafThreads, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-  else if (w <= 64) chol_leaf_kernel<T, 64><<<grid, kLeafThreads, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-  else return cudaErrorInvalidValue;
-  count_launch();
-  return cudaGetLastError();
-}
-
-// =============================================================== LU leaf
-template <typename T, int W>
-__global__ void __launch_bounds__(kLeafThreads) lu_leaf_kernel(int64_t m, int64_t ncr, int w,
-                                                               const T* __restrict__ src, int64_t lds,
-                                                               T* __restrict__ dst, int64_t ldd, int64_t col0,
-                                                               const T* tolp, long long* fail, int nrow_blocks) {
-  if (failed(fail)) return;
-  __shared__ T D[W][W + 1];
-  __shared__ T inv[W];
-  __shared__ int bad;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const T tol = *tolp;
-  if (tid == 0) bad = 0;
-  for (int idx = tid; idx < w * w; idx += kLeafThreads) {
-    const int i = idx % w, j = idx / w;
-    D[i][j] = src[i + (int64_t)j * lds];
-  }
-  __syncthreads();
-  if (tid < 32) {
-    for (int c = 0; c < w; ++c) {
-      T tl[2], tu[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int i = lane + 32 * h;
-        tl[h] = T(0); tu[h] = T(0);
-        if (i >= c && i < w) {
-          // L_ic = A_ic - sum_k L_ik U_kc
-          T a0 = D[i][c], a1 = T(0);
-          int k = 0;
-          for (; k + 2 <= c; k += 2) { a0 = fma(-D[i][k], D[k][c], a0); a1 = fma(-D[i][k + 1], D[k + 1][c], a1); }
-          if (k < c) a0 = fma(-D[i][k], D[k][c], a0);
-          tl[h] = a0 + a1;
-        }
-        if (i > c && i < w) {
-          // U_ci * L_cc = A_ci - sum_k L_ck U_ki
-          T a0 = D[c][i], a1 = T(0);
-          int k = 0;
-          for (; k + 2 <= c; k += 2) { a0 = fma(-D[c][k], D[k][i], a0); a1 = fma(-D[c][k + 1], D[k + 1][i], a1); }
-          if (k < c) a0 = fma(-D[c][k], D[k][i], a0);
-          tu[h] = a0 + a1;
-        }
-      }
-      const T Lcc = __shfl_sync(0xffffffffu, (c >> 5) ? tl[1] : tl[0], c & 31);
-      if (!(fabs(Lcc) >= tol)) {
-        if (lane == 0) { bad = 1; if (blockIdx.x == 0) record_fail(fail, col0 + c + 1); }
-        break;
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int i = lane + 32 * h;
-        if (i >= c && i < w) D[i][c] = tl[h];
-        if (i > c && i < w) D[c][i] = tu[h] / Lcc;
-      }
-      if (lane == 0) inv[c] = T(1) / Lcc;
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  if (bad) return;
-  if (blockIdx.x == 0) {
-    for (int idx = tid; idx < w * w; idx += kLeafThreads) {
-      const int i = idx % w, j = idx / w;
-      dst[i + (int64_t)j * ldd] = D[i][j];
-    }
-  }
-  if ((int)blockIdx.x < nrow_blocks) {
-    // L rows below: L_rc = A_rc - sum_{k<c} L_rk U_kc
-    const int64_t r = w + (int64_t)blockIdx.x * kLeafThreads + tid;
-    if (r >= m) return;
-    T x[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) x[k] = (k < w) ? src[r + (int64_t)k * lds] : T(0);
-#pragma unroll
-    for (int c = 0; c < W; ++c) {
-      if (c < w) {
-        T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
-#pragma unroll
-        for (int k = 0; k + 4 <= c; k += 4) {
-          a0 = fma(-x[k], D[k][c], a0);
-          a1 = fma(-x[k + 1], D[k + 1][c], a1);
-          a2 = fma(-x[k + 2], D[k + 2][c], a2);
-          a3 = fma(-x[k + 3], D[k + 3][c], a3);
-        }
-#pragma unroll
-        for (int k = c & ~3; k < c; ++k) a0 = fma(-x[k], D[k][c], a0);
-        x[c] = (a0 + a1) + (a2 + a3);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < W; ++k)
-      if (k < w) dst[r + (int64_t)k * ldd] = x[k];
-  } else {
-    // U columns to the right: U_cj = (A_cj - sum_{k<c} L_ck U_kj) / L_cc
-    const int64_t j = w + (int64_t)(blockIdx.x - nrow_blocks) * kLeafThreads + tid;
-    if (j >= w + ncr) return;
-    const T* col = src + j * lds;
-    T y[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) y[k] = (k < w) ? col[k] : T(0);
-#pragma unroll
-    for (int c = 0; c < W; ++c) {
-      if (c < w) {
-        T a0 = y[c], a1 = T(0), a2 = T(0), a3 = T(0);
-#pragma unroll
-        for (int k = 0; k + 4 <= c; k += 4) {
-          a0 = fma(-D[c][k], y[k], a0);
-          a1 = fma(-D[c][k + 1], y[k + 1], a1);
-          a2 = fma(-D[c][k + 2], y[k + 2], a2);
-          a3 = fma(-D[c][k + 3], y[k + 3], a3);
-        }
-#pragma unroll
-        for (int k = c & ~3; k < c; ++k) a0 = fma(-D[c][k], y[k], a0);
-        y[c] = ((a0 + a1) + (a2 + a3)) * inv[c];
-      }
-    }
-    T* out = dst + j * ldd;
-#pragma unroll
-    for (int k = 0; k < W; ++k)
-      if (k < w) out[k] = y[k];
-  }
-}
-
-template <typename T>
-cudaError_t lu_leaf(int64_t m, int64_t ncr, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
-                    const T* tol, long long* fail, cudaStream_t st) {
-  if (w <= 0 || m <= 0) return cudaSuccess;
-  const int64_t below = m - w;
-  const int nrb = below > 0 ? (int)((below + kLeafThreads - 1) / kLeafThreads) : 0;
-  const int ncb = ncr > 0 ? (int)((ncr + kLeafThreads - 1) / kLeafThreads) : 0;
-  int grid = nrb + ncb;
-  if (grid == 0) grid = 1;
-  if (w <= 16) lu_leaf_kernel<T, 16><<<grid, kLeafThreads, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
-  else if (w <= 32) lu_leaf_kernel<T, 32><<<grid, kLeafThreads, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
-  else if (w <= 64) lu_leaf_kernel<T, 64><<<grid, kLeafThreads, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
-  else return cudaErrorInvalidValue;
-  count_launch();
-  return cudaGetLastError();
-}
-
 // =============================================================== QR MGS panel
 constexpr int kMgsThreads = 256;
 
@@ -430,7 +187,7 @@ cudaError_t frob_norm_tol(int64_t n, const T* A, int64_t lda, T* tol_out, double
   return cudaGetLastError();
 }
 
-__global__ void init_fail_kernel(long long* fail) { *fail = kNoFail; }
+__global__ void init_fail_kernel(long long* fail) { fail[0] = kNoFail; fail[1] = 0; }
 __global__ void finish_info_kernel(const long long* fail, int64_t* info) {
   const long long f = *fail;
   *info = (f == kNoFail) ? 0 : (int64_t)f;
@@ -470,10 +227,6 @@ cudaError_t copy_matrix(int64_t m, int64_t n, const T* src, int64_t lds, T* dst,
 }
 
 #define SF_INST(T)                                                                                             \
-  template cudaError_t chol_leaf<T>(int64_t, int, const T*, int64_t, T*, int64_t, int64_t, long long*,        \
-                                    cudaStream_t);                                                            \
-  template cudaError_t lu_leaf<T>(int64_t, int64_t, int, const T*, int64_t, T*, int64_t, int64_t, const T*,  \
-                                  long long*, cudaStream_t);                                                  \
   template cudaError_t qr_mgs_panel<T>(int64_t, int, const T*, int64_t, T*, int64_t, int64_t, const T*, T*,  \
                                        long long*, cudaStream_t);                                             \
   template cudaError_t frob_norm_tol<T>(int64_t, const T*, int64_t, T*, double*, cudaStream_t);                   \
