@@ -405,28 +405,57 @@ static int qr_run(int64_t n, int64_t s, const T* A, int64_t lda, T* Q, int64_t l
     if ((int64_t)sp * s * wmax > split_elems) split_elems = (int64_t)sp * s * wmax;
   }
   Workspace ws;
-  SF_CUDA(ws.init(sizeof(T) * (mgs_elems + cw_elems + split_elems) + 16384 + 4 * 256, st));
+  SF_CUDA(ws.init(sizeof(T) * (mgs_elems + 2 * cw_elems + 2 * split_elems) + 16384 + 8 * 256, st));
   long long* fail = ws.take<long long>(2);   // [0] first failed column, [1] leaf counter
   T* tol = ws.take<T>(1);
   double* part = ws.take<double>(512);
   T* mgsw = ws.take<T>(mgs_elems);
   T* Cw = ws.take<T>(cw_elems);
   T* split = ws.take<T>(split_elems > 0 ? split_elems : 1);
+  // the side stream's wide-panel chunk projections get their own scratch
+  T* Cw2 = s > wmax ? ws.take<T>(cw_elems) : Cw;
+  T* split2 = s > wmax ? ws.take<T>(split_elems > 0 ? split_elems : 1) : split;
   SF_CUDA(init_fail(fail, st));
+  SF_CUDA(cudaMemsetAsync(mgsw, 0, sizeof(T) * mgs_elems, st));   // MGS flags (epochs start at 0)
   SF_CUDA(frob_norm_tol<T>(n, A, lda, tol, part, st));
+  Side* sd = nullptr;
+  const bool la = lookahead_on() && s < n;
+  if (la) SF_CUDA(side_stream(sd));
+  {
+    ProfScope ps(1, 0.0, st);
+    const int64_t w0 = s < n ? s : n;
+    SF_CUDA(qr_panel<T>(n, w0, A, lda, Q, ldq, 0, tol, mgsw, Cw, split, split_elems, fail, st));
+  }
   for (int64_t z = 0; z < n; z += s) {
-    const int64_t w = (s < n - z) ? s : n - z;
+    const int64_t w = (s < n - z) ? s : n - z, c = z + w;
+    if (c >= n) break;
+    const int64_t w2 = (s < n - c) ? s : n - c, m = n - c;
     const T* src = (z == 0) ? A : Q;           // M := copy of A lives in Q
     const int64_t lds = (z == 0) ? lda : ldq;
+    const T* BQ = Q + z * ldq;                 // B_Q = Q[:, z:c)
+    // flush: C = B_Q^T B_M, M[:, c:n] -= B_Q C over all rows.  With
+    // lookahead the columns of the next panel go first, the rest overlaps that panel.
+    const int64_t first = la ? w2 : m;
     {
-      ProfScope ps(1, 0.0, st);
-      SF_CUDA(qr_panel<T>(n, w, src + z * lds, lds, Q + z * ldq, ldq, z, tol, mgsw, Cw, split, split_elems, fail, st));
+      ProfScope ps(0, 4.0 * (double)n * (double)w * (double)first, st);
+      SF_CUDA(qr_project<T>(n, w, first, BQ, ldq, src + c * lds, lds, Q + c * ldq, ldq, Cw, split, split_elems,
+                            fail, st));
     }
-    const int64_t c = z + w;
-    if (c < n) {  // flush: C = B_Q^T B_M, M[:, c:n] -= B_Q C over all rows
-      ProfScope ps(0, 4.0 * (double)n * (double)w * (double)(n - c), st);
-      SF_CUDA(qr_project<T>(n, w, n - c, Q + z * ldq, ldq, src + c * lds, lds, Q + c * ldq, ldq, Cw, split,
-                            split_elems, fail, st));
+    cudaStream_t pst = st;
+    if (la) { SF_CUDA(fork_join(*sd, st, sd->st)); pst = sd->st; }
+    {
+      ProfScope ps(1, 0.0, pst);
+      SF_CUDA(qr_panel<T>(n, w2, Q + c * ldq, ldq, Q + c * ldq, ldq, c, tol, mgsw, Cw2, split2, split_elems, fail,
+                          pst));
+    }
+    if (la) {
+      if (m > w2) {
+        const int64_t c2 = c + w2;
+        ProfScope ps(0, 4.0 * (double)n * (double)w * (double)(m - w2), st);
+        SF_CUDA(qr_project<T>(n, w, m - w2, BQ, ldq, src + c2 * lds, lds, Q + c2 * ldq, ldq, Cw, split, split_elems,
+                              fail, st));
+      }
+      SF_CUDA(fork_join(*sd, sd->st, st));
     }
   }
   // R := Q^T A: upper triangle on the tensor cores, exact zeros below
@@ -630,6 +659,7 @@ int sf_qr_panel(int64_t n, int64_t w, int dtype, void* dV, int64_t ld, int64_t c
   double* Cw = ws.take<double>(w * wcap);
   double* split = ws.take<double>(split_elems);
   SF_CUDA(init_fail(fail, st));
+  SF_CUDA(cudaMemsetAsync(mgsw, 0, sizeof(double) * mgs, st));
   SF_CUDA(cudaMemcpyAsync(dtol, &tol, sizeof(double), cudaMemcpyHostToDevice, st));
   SF_CUDA(qr_panel<double>(n, w, (double*)dV, ld, (double*)dV, ld, col0, dtol, mgsw, Cw, split, split_elems, fail, st));
   SF_CUDA(finish_info(fail, d_info, st));

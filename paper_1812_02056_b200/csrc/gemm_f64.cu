@@ -57,8 +57,8 @@ __device__ __forceinline__ void load_slice(double* Xs, const double* __restrict_
         cp_async16(dst, bytes ? X + idx + kg * ld : X, bytes);
       } else {
         const int b0 = (kin && idx < nidx) ? 8 : 0, b1 = (kin && idx + 1 < nidx) ? 8 : 0;
-        cp_async8(dst, b0 ? X + idx + kg * ld : X, b0);
-        cp_async8(dst + 1, b1 ? X + idx + 1 + kg * ld : X, b1);
+        dst[0] = b0 ? __ldcg(X + idx + kg * ld) : 0.0;       // unaligned operand: L2-only loads
+        dst[1] = b1 ? __ldcg(X + idx + 1 + kg * ld) : 0.0;
       }
     } else {
       const int ii = id / (BK / 2), ch = id % (BK / 2);
@@ -70,8 +70,8 @@ __device__ __forceinline__ void load_slice(double* Xs, const double* __restrict_
         cp_async16(dst, bytes ? X + kg + idx * ld : X, bytes);
       } else {
         const int b0 = (iin && kg < K) ? 8 : 0, b1 = (iin && kg + 1 < K) ? 8 : 0;
-        cp_async8(dst, b0 ? X + kg + idx * ld : X, b0);
-        cp_async8(dst + 1, b1 ? X + kg + 1 + idx * ld : X, b1);
+        dst[0] = b0 ? __ldcg(X + kg + idx * ld) : 0.0;
+        dst[1] = b1 ? __ldcg(X + kg + 1 + idx * ld) : 0.0;
       }
     }
   }
@@ -224,11 +224,11 @@ __global__ void __launch_bounds__(g64::THREADS, 1) gemm_f64_kernel(GemmF64 p, in
         const int64_t i = i0 + 64 * h + 2 * lane;
         const double* src = p.Cin + i + j * p.ldcin;
         if (vecC && j < p.N && i + 1 < p.M) {
-          const double2 v = __ldcs(reinterpret_cast<const double2*>(src));
+          const double2 v = __ldcg(reinterpret_cast<const double2*>(src));
           cin[q][h][0] = v.x; cin[q][h][1] = v.y;
         } else {
-          cin[q][h][0] = (j < p.N && i < p.M) ? src[0] : 0.0;
-          cin[q][h][1] = (j < p.N && i + 1 < p.M) ? src[1] : 0.0;
+          cin[q][h][0] = (j < p.N && i < p.M) ? __ldcg(src) : 0.0;
+          cin[q][h][1] = (j < p.N && i + 1 < p.M) ? __ldcg(src + 1) : 0.0;
         }
       }
     }
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(g64::THREADS, 1) gemm_f64_kernel(GemmF64 p, in
       double* dst = p.C + i + j * p.ldc;
       const bool pair_in = (i + 1 < p.M) && (MASK == kMaskNone || (MASK == kMaskLower ? i >= j : i + 1 <= j));
       if (pair_in && vecC) {
-        __stcs(reinterpret_cast<double2*>(dst), make_double2(v0, v1));
+        __stcg(reinterpret_cast<double2*>(dst), make_double2(v0, v1));
       } else {
         if (i < p.M && (MASK == kMaskNone || (MASK == kMaskLower ? i >= j : i <= j))) dst[0] = v0;
         if (i + 1 < p.M && (MASK == kMaskNone || (MASK == kMaskLower ? i + 1 >= j : i + 1 <= j))) dst[1] = v1;

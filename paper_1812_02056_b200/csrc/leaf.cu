@@ -16,7 +16,10 @@
 // for LU's U part, for one column to the right (staged through shared memory so the
 // column's w contiguous entries are loaded and stored coalesced).
 // The diagonal factorization is repeated by every CTA (~1-2 us) instead of a grid-wide
-// dependency; CTA 0 writes it out.
+// dependency; the last CTA to have read it writes it out.
+// All loads of data produced by other kernels bypass L1 (ld.global.cg): with the
+// lookahead stream two kernels share SMs, and an SM's L1 may hold lines another kernel
+// read before a third one rewrote them.
 #include <math.h>
 
 #include "common.cuh"
@@ -63,7 +66,7 @@ __global__ void __launch_bounds__(kLeafT) chol_leaf_kernel(int64_t m, int w, con
   if (tid < 32) {
     T x[W];
 #pragma unroll
-    for (int k = 0; k < W; ++k) x[k] = (lane < w && k <= lane && k < w) ? src[lane + (int64_t)k * lds] : T(0);
+    for (int k = 0; k < W; ++k) x[k] = (lane < w && k <= lane && k < w) ? __ldcg(src + lane + (int64_t)k * lds) : T(0);
     int ok = 1;
 #pragma unroll
     for (int c = 0; c < W; ++c) {
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(kLeafT) chol_leaf_kernel(int64_t m, int w, con
   if (r >= m) return;
   T x[W];
 #pragma unroll
-  for (int k = 0; k < W; ++k) x[k] = (k < w) ? src[r + (int64_t)k * lds] : T(0);
+  for (int k = 0; k < W; ++k) x[k] = (k < w) ? __ldcg(src + r + (int64_t)k * lds) : T(0);
 #pragma unroll
   for (int c = 0; c < W; ++c) {
     T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
@@ -153,13 +156,13 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_kernel(int64_t m, int64_t ncr,
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid < 32) {
-    const T tol = *tolp;
+    const T tol = __ldcg(tolp);
     T x[W], y[W];   // lane i: row i (x) and column i (y) of the diagonal block
 #pragma unroll
     for (int k = 0; k < W; ++k) {
       const bool in = lane < w && k < w;
-      x[k] = in ? src[lane + (int64_t)k * lds] : T(0);
-      y[k] = in ? src[k + (int64_t)lane * lds] : T(0);
+      x[k] = in ? __ldcg(src + lane + (int64_t)k * lds) : T(0);
+      y[k] = in ? __ldcg(src + k + (int64_t)lane * lds) : T(0);
     }
     int ok = 1;
 #pragma unroll
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_kernel(int64_t m, int64_t ncr,
     if (r >= m) return;
     T x[W];
 #pragma unroll
-    for (int k = 0; k < W; ++k) x[k] = (k < w) ? src[r + (int64_t)k * lds] : T(0);
+    for (int k = 0; k < W; ++k) x[k] = (k < w) ? __ldcg(src + r + (int64_t)k * lds) : T(0);
 #pragma unroll
     for (int c = 0; c < W; ++c) {
       T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_kernel(int64_t m, int64_t ncr,
   const int ncols = (int)((w + ncr - j0) < kUCols ? (w + ncr - j0) : kUCols);
   const int warp = tid >> 5;
   for (int jj = warp; jj < ncols; jj += kLeafT / 32)
-    if (lane < w) S[jj][lane] = src[lane + (j0 + jj) * lds];
+    if (lane < w) S[jj][lane] = __ldcg(src + lane + (j0 + jj) * lds);
   __syncthreads();
   if (tid < ncols) {
     T y[W];

@@ -20,13 +20,11 @@
 // is done every later panel column is projected once.  The norm of v_c and its dot
 // products with the later columns come from ONE grid-wide reduction (Gram row), so the
 // persistent cooperative kernel needs one grid barrier per column.
-#include <cooperative_groups.h>
 #include <math.h>
 
 #include "common.cuh"
 #include "kernels.h"
 
-namespace cg = cooperative_groups;
 
 namespace sf {
 
@@ -48,7 +46,7 @@ static MgsGeom mgs_geom(int64_t n, int w, int elt) {
   int dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   MgsGeom g;
-  g.G = (int)((n + 63) / 64);
+  g.G = (int)((n + 127) / 128);
   if (g.G > sms) g.G = sms;
   if (g.G < 1) g.G = 1;
   g.RB = (int)((n + g.G - 1) / g.G);
@@ -58,8 +56,25 @@ static MgsGeom mgs_geom(int64_t n, int w, int elt) {
 
 size_t qr_mgs_work_elems(int64_t n, int w) {
   MgsGeom g = mgs_geom(n, w, 8);
-  return 2 * (size_t)g.G * (size_t)w;
+  return (size_t)g.G + 2 * (size_t)g.G * (size_t)w + 2;   // flags[2][G] + partials[2][w][G]
 }
+
+// Inter-CTA exchange for a cooperative (co-resident) grid, without atomics: CTA g publishes
+// its partial Gram row for column c into slot part[c&1] and then raises flag[c&1][g] = c+1
+// (release); readers poll all G flags of that parity (acquire) and then read the partials
+// bypassing L1.  Double buffering by column parity is safe: a CTA writes parity c&1 again
+// only at column c+2, after it has seen every CTA's flag for column c+1, i.e. after every
+// CTA finished reading the column-c partials.
+__device__ __forceinline__ int ld_acquire_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_s32(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+constexpr int kMgsMaxT = 16;   // columns per warp whose partial sums are fetched together
 
 template <typename T>
 __global__ void __launch_bounds__(kMgsThreads) qr_mgs_kernel(int64_t n, int w, int RB, const T* __restrict__ src,
@@ -67,7 +82,6 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_kernel(int64_t n, int w, i
                                                              int64_t col0, const T* tolp, T* work,
                                                              long long* fail) {
   if (failed(fail)) return;
-  cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smraw[];
   T* V = reinterpret_cast<T*>(smraw);          // V[c * RB + r]: this CTA's rows of the panel
   T* gsum = V + (size_t)RB * w;                // reduced Gram row for the current column
@@ -76,32 +90,62 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_kernel(int64_t n, int w, i
   const int G = gridDim.x, g = blockIdx.x;
   const int64_t r0 = (int64_t)g * RB;
   const int rows = (int)((r0 + RB <= n) ? RB : (n > r0 ? n - r0 : 0));
-  const T tol = *tolp;
+  const T tol = __ldcg(tolp);
+  int* flags = reinterpret_cast<int*>(work);                                   // flags[2][G]
+  T* partbase = work + (2 * G * sizeof(int) + sizeof(T) - 1) / sizeof(T);     // part[2][w][G]
 
   for (int idx = tid; idx < RB * w; idx += kMgsThreads) {
     const int r = idx % RB, c = idx / RB;
-    V[idx] = (r < rows) ? src[r0 + r + (int64_t)c * lds] : T(0);
+    V[idx] = (r < rows) ? __ldcg(src + r0 + r + (int64_t)c * lds) : T(0);   // L2, never a stale L1 line
   }
   __syncthreads();
 
   bool ok = true;
   for (int c = 0; c < w; ++c) {
-    T* part = work + (size_t)(c & 1) * G * w;
-    // 1) partial Gram row: <v_c, v_c'> over this CTA's rows, c' in [c, w)
+    const int buf = c & 1;
+    T* part = partbase + (size_t)buf * G * w;
+    // 1) partial Gram row over this CTA's rows: <v_c, v_c'> for c' in [c, w)
     const T* vc = V + (size_t)c * RB;
     for (int cp = c + warp; cp < w; cp += nwarps) {
       const T* v2 = V + (size_t)cp * RB;
       T acc = T(0);
       for (int r = lane; r < RB; r += 32) acc = fma(vc[r], v2[r], acc);
       acc = warp_sum(acc);
-      if (lane == 0) part[(size_t)g * w + cp] = acc;
+      if (lane == 0) part[(size_t)cp * G + g] = acc;
     }
-    grid.sync();
-    // 2) every CTA reduces the partials in the same fixed order
-    for (int cp = c + tid; cp < w; cp += kMgsThreads) {
-      T s = T(0);
-      for (int h = 0; h < G; ++h) s += part[(size_t)h * w + cp];
-      gsum[cp] = s;
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release_s32(flags + buf * G + g, (int)(col0 + c + 1));   // epochs grow across launches
+    }
+    // 2) wait until every CTA has published column c
+    if (warp == 0) {
+      for (;;) {
+        bool mine = true;
+        for (int h = lane; h < G; h += 32) mine &= (ld_acquire_s32(flags + buf * G + h) >= (int)(col0 + c + 1));
+        if (__all_sync(0xffffffffu, mine)) break;
+      }
+    }
+    __syncthreads();
+    // 3) every CTA reduces the partials in the same fixed order (warp per column,
+    //    coalesced over the CTA index; deterministic shuffle tree), all loads in flight
+    for (int cb = c + warp; cb < w; cb += nwarps * kMgsMaxT) {
+      T acc[kMgsMaxT];
+#pragma unroll
+      for (int t = 0; t < kMgsMaxT; ++t) acc[t] = T(0);
+      for (int h = lane; h < G; h += 32) {
+#pragma unroll
+        for (int t = 0; t < kMgsMaxT; ++t) {
+          const int cp = cb + t * nwarps;
+          if (cp < w) acc[t] += __ldcg(part + (size_t)cp * G + h);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < kMgsMaxT; ++t) {
+        const int cp = cb + t * nwarps;
+        const T v = warp_sum(acc[t]);
+        if (lane == 0 && cp < w) gsum[cp] = v;
+      }
     }
     __syncthreads();
     const T nv = dsqrt(gsum[c]);
@@ -113,7 +157,7 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_kernel(int64_t n, int w, i
     for (int cp = c + 1 + tid; cp < w; cp += kMgsThreads) dcoef[cp] = gsum[cp] / nv;   // q_c^T v_c'
     for (int r = tid; r < RB; r += kMgsThreads) V[(size_t)c * RB + r] = vc[r] / nv;     // q_c = v_c/||v_c||
     __syncthreads();
-    // 3) project q_c out of every later panel column
+    // 4) project q_c out of every later panel column
     const int rem = w - c - 1;
     for (int idx = tid; idx < RB * rem; idx += kMgsThreads) {
       const int r = idx % RB, cp = c + 1 + idx / RB;
@@ -217,7 +261,7 @@ template <typename T>
 __global__ void copy_kernel(int64_t m, int64_t n, const T* src, int64_t lds, T* dst, int64_t ldd) {
   for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-      dst[i + j * ldd] = src[i + j * lds];
+      dst[i + j * ldd] = __ldcg(src + i + j * lds);
 }
 template <typename T>
 cudaError_t copy_matrix(int64_t m, int64_t n, const T* src, int64_t lds, T* dst, int64_t ldd, cudaStream_t st) {

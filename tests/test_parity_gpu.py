@@ -283,3 +283,25 @@ def test_host_entry_points():
     out, info = sf.lu_host(hB, s)
     Lo, Uo, _ = oracle.lu(B, s)
     assert info == 0 and synth.r2_error(np.tril(out), Lo) <= TOL64
+
+
+@pytest.mark.parametrize("s", [2, 4, 8])
+def test_lookahead_repeatable(s):
+    """Regression for a cross-stream stale-L1 race (DESIGN.md §5 'memory visibility'): the
+    lookahead panel stream and the update stream share SMs; every run must match the oracle
+    and every other run bit for bit."""
+    n = 256
+    A = synth.gen_numpy("gaussian", n, seed=n)
+    Qo, Ro, _, _ = oracle.qr(A, s)
+    first = None
+    for _ in range(4):
+        Qg, Rg, info = run_qr(A, s)
+        assert info == 0 and np.abs(Qg - Qo).max() < 1e-12
+        if first is None:
+            first = Qg
+        assert np.array_equal(Qg, first)
+    B = synth.gen_numpy("diag_dominant", 300, seed=1)
+    Lo, Uo, _ = oracle.lu(B, s)
+    for _ in range(3):
+        Lg, Ug, info = run_lu(B, s)
+        assert info == 0 and synth.r2_error(Lg, Lo) <= TOL64 and synth.r2_error(Ug, Uo) <= TOL64
