@@ -21,6 +21,7 @@
 // products with the later columns come from ONE grid-wide reduction (Gram row), so the
 // persistent cooperative kernel needs one grid barrier per column.
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -50,7 +51,7 @@ static MgsGeom mgs_geom(int64_t n, int w, int elt) {
   if (g.G > sms) g.G = sms;
   if (g.G < 1) g.G = 1;
   g.RB = (int)((n + g.G - 1) / g.G);
-  g.smem = (size_t)elt * ((size_t)g.RB * w + 2 * (size_t)w + 64);
+  g.smem = (size_t)elt * ((size_t)g.RB * w + (size_t)w + 64);
   return g;
 }
 
@@ -73,8 +74,29 @@ __device__ __forceinline__ int ld_acquire_s32(const int* p) {
 __device__ __forceinline__ void st_release_s32(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ int ld_relaxed_s32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Wait until flags[0..G) >= epoch (warp 0 of the CTA polls; relaxed loads with a short
+// back-off, one acquire fence at the end), then make the CTA wait for warp 0.
+__device__ __forceinline__ void wait_flags(const int* flags, int G, int epoch) {
+  if ((threadIdx.x >> 5) == 0) {
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+      bool all = true;
+      for (int hh = lane; hh < G; hh += 32) all &= (ld_relaxed_s32(flags + hh) >= epoch);
+      if (__all_sync(0xffffffffu, all)) break;
+      __nanosleep(64);
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
+  __syncthreads();
+}
 
 constexpr int kMgsMaxT = 16;   // columns per warp whose partial sums are fetched together
+constexpr int kMgsRJ = 16;     // max rows per lane (RB <= 512, i.e. n <= 75776 on 148 SMs)
 
 template <typename T>
 __global__ void __launch_bounds__(kMgsThreads) qr_mgs_kernel(int64_t n, int w, int RB, const T* __restrict__ src,
@@ -85,7 +107,6 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_kernel(int64_t n, int w, i
   extern __shared__ __align__(16) unsigned char smraw[];
   T* V = reinterpret_cast<T*>(smraw);          // V[c * RB + r]: this CTA's rows of the panel
   T* gsum = V + (size_t)RB * w;                // reduced Gram row for the current column
-  T* dcoef = gsum + w;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kMgsThreads / 32;
   const int G = gridDim.x, g = blockIdx.x;
   const int64_t r0 = (int64_t)g * RB;
@@ -93,6 +114,7 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_kernel(int64_t n, int w, i
   const T tol = __ldcg(tolp);
   int* flags = reinterpret_cast<int*>(work);                                   // flags[2][G]
   T* partbase = work + (2 * G * sizeof(int) + sizeof(T) - 1) / sizeof(T);     // part[2][w][G]
+  const int RJ = (RB + 31) / 32;               // rows per lane (RB <= 32 * kMgsRJ)
 
   for (int idx = tid; idx < RB * w; idx += kMgsThreads) {
     const int r = idx % RB, c = idx / RB;
@@ -100,35 +122,30 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_kernel(int64_t n, int w, i
   }
   __syncthreads();
 
+  // partial Gram row of column 0: <v_0, v_cp> over this CTA's rows
+  {
+    T v0[kMgsRJ];
+#pragma unroll
+    for (int j = 0; j < kMgsRJ; ++j) v0[j] = (j < RJ && lane + 32 * j < RB) ? V[lane + 32 * j] : T(0);
+    for (int cp = warp; cp < w; cp += nwarps) {
+      T acc = T(0);
+#pragma unroll
+      for (int j = 0; j < kMgsRJ; ++j)
+        if (j < RJ && lane + 32 * j < RB) acc = fma(v0[j], V[(size_t)cp * RB + lane + 32 * j], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) partbase[(size_t)cp * G + g] = acc;
+    }
+  }
+
   bool ok = true;
   for (int c = 0; c < w; ++c) {
     const int buf = c & 1;
     T* part = partbase + (size_t)buf * G * w;
-    // 1) partial Gram row over this CTA's rows: <v_c, v_c'> for c' in [c, w)
-    const T* vc = V + (size_t)c * RB;
-    for (int cp = c + warp; cp < w; cp += nwarps) {
-      const T* v2 = V + (size_t)cp * RB;
-      T acc = T(0);
-      for (int r = lane; r < RB; r += 32) acc = fma(vc[r], v2[r], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) part[(size_t)cp * G + g] = acc;
-    }
+    // 1) publish this CTA's partial Gram row of column c, wait for everybody's
     __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_release_s32(flags + buf * G + g, (int)(col0 + c + 1));   // epochs grow across launches
-    }
-    // 2) wait until every CTA has published column c
-    if (warp == 0) {
-      for (;;) {
-        bool mine = true;
-        for (int h = lane; h < G; h += 32) mine &= (ld_acquire_s32(flags + buf * G + h) >= (int)(col0 + c + 1));
-        if (__all_sync(0xffffffffu, mine)) break;
-      }
-    }
-    __syncthreads();
-    // 3) every CTA reduces the partials in the same fixed order (warp per column,
-    //    coalesced over the CTA index; deterministic shuffle tree), all loads in flight
+    if (tid == 0) { __threadfence(); st_release_s32(flags + buf * G + g, (int)(col0 + c + 1)); }   // epochs grow across launches
+    wait_flags(flags + buf * G, G, (int)(col0 + c + 1));
+    // 2) fixed-order reduction of the partials (warp per column, coalesced over CTAs)
     for (int cb = c + warp; cb < w; cb += nwarps * kMgsMaxT) {
       T acc[kMgsMaxT];
 #pragma unroll
@@ -154,21 +171,160 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_kernel(int64_t n, int w, i
       ok = false;
       break;
     }
-    for (int cp = c + 1 + tid; cp < w; cp += kMgsThreads) dcoef[cp] = gsum[cp] / nv;   // q_c^T v_c'
-    for (int r = tid; r < RB; r += kMgsThreads) V[(size_t)c * RB + r] = vc[r] / nv;     // q_c = v_c/||v_c||
-    __syncthreads();
-    // 4) project q_c out of every later panel column
-    const int rem = w - c - 1;
-    for (int idx = tid; idx < RB * rem; idx += kMgsThreads) {
-      const int r = idx % RB, cp = c + 1 + idx / RB;
-      V[(size_t)cp * RB + r] = fma(-vc[r], dcoef[cp], V[(size_t)cp * RB + r]);
+    // 3) q_c = v_c / ||v_c|| (every warp keeps its lane's rows in registers), the next
+    //    column updated first (redundantly in every warp), then each warp projects q_c out
+    //    of its columns and immediately forms their partial dot with v_{c+1}: the update
+    //    of column c and the partial Gram row of column c+1 are one pass over shared memory.
+    T q[kMgsRJ], vn[kMgsRJ];
+    const T cn = (c + 1 < w) ? gsum[c + 1] / nv : T(0);
+#pragma unroll
+    for (int j = 0; j < kMgsRJ; ++j) {
+      const int r = lane + 32 * j;
+      const bool in = j < RJ && r < RB;
+      q[j] = in ? V[(size_t)c * RB + r] / nv : T(0);
+      vn[j] = (in && c + 1 < w) ? fma(-q[j], cn, V[(size_t)(c + 1) * RB + r]) : T(0);
     }
-    __syncthreads();
+    __syncthreads();   // everybody has read v_c and v_{c+1}
+    if (warp == 0) {
+#pragma unroll
+      for (int j = 0; j < kMgsRJ; ++j) {
+        const int r = lane + 32 * j;
+        if (j < RJ && r < RB) V[(size_t)c * RB + r] = q[j];
+      }
+    }
+    T* pnext = partbase + (size_t)(buf ^ 1) * G * w;
+    for (int cp = c + 1 + warp; cp < w; cp += nwarps) {
+      const T coef = gsum[cp] / nv;                 // q_c^T v_cp
+      T acc = T(0);
+#pragma unroll
+      for (int j = 0; j < kMgsRJ; ++j) {
+        const int r = lane + 32 * j;
+        if (j < RJ && r < RB) {
+          const T nvp = (cp == c + 1) ? vn[j] : fma(-q[j], coef, V[(size_t)cp * RB + r]);
+          V[(size_t)cp * RB + r] = nvp;
+          acc = fma(vn[j], nvp, acc);
+        }
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) pnext[(size_t)cp * G + g] = acc;
+    }
   }
   if (!ok) return;
+  __syncthreads();
   for (int idx = tid; idx < RB * w; idx += kMgsThreads) {
     const int r = idx % RB, c = idx / RB;
     if (r < rows) dst[r0 + r + (int64_t)c * ldd] = V[idx];
+  }
+}
+
+// Register-resident variant for the common case w <= 128, RB <= 2*kMgsRPT: thread t owns
+// column t>>1 and half t&1 of this CTA's rows (kMgsRPT values in registers), so a column
+// step is one pass of register FMAs against two broadcast vectors in shared memory (q_c and
+// v_{c+1}), with the two halves of each dot combined by a shuffle.
+constexpr int kMgsRPT = 64;
+
+template <typename T>
+__global__ void __launch_bounds__(kMgsThreads) qr_mgs_reg_kernel(int64_t n, int w, int RB, const T* __restrict__ src,
+                                                                 int64_t lds, T* __restrict__ dst, int64_t ldd,
+                                                                 int64_t col0, const T* tolp, T* work,
+                                                                 long long* fail) {
+  if (failed(fail)) return;
+  constexpr int QP = kMgsRPT + 2;              // half stride in the broadcast vectors (bank spread)
+  __shared__ T qs[2 * QP], vs[2 * QP];
+  __shared__ T gsum[128];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kMgsThreads / 32;
+  const int G = gridDim.x, g = blockIdx.x;
+  const int64_t r0 = (int64_t)g * RB;
+  const int rows = (int)((r0 + RB <= n) ? RB : (n > r0 ? n - r0 : 0));
+  const T tol = __ldcg(tolp);
+  int* flags = reinterpret_cast<int*>(work);
+  T* partbase = work + (2 * G * sizeof(int) + sizeof(T) - 1) / sizeof(T);
+  const int cp = tid >> 1, h = tid & 1;        // my column and half
+  const int rbase = h * kMgsRPT;
+  const bool mine = cp < w;
+  T x[kMgsRPT];
+#pragma unroll
+  for (int r = 0; r < kMgsRPT; ++r) {
+    const int rr = rbase + r;
+    x[r] = (mine && rr < rows) ? __ldcg(src + r0 + rr + (int64_t)cp * lds) : T(0);
+  }
+  // partial Gram row of column 0
+  if (cp == 0) {
+#pragma unroll
+    for (int r = 0; r < kMgsRPT; ++r) vs[h * QP + r] = x[r];
+  }
+  __syncthreads();
+  {
+    T acc = T(0);
+#pragma unroll
+    for (int r = 0; r < kMgsRPT; ++r) acc = fma(vs[h * QP + r], x[r], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (mine && h == 0) partbase[(size_t)cp * G + g] = acc;
+  }
+
+  bool ok = true;
+  for (int c = 0; c < w; ++c) {
+    const int buf = c & 1;
+    T* part = partbase + (size_t)buf * G * w;
+    __syncthreads();
+    if (tid == 0) { __threadfence(); st_release_s32(flags + buf * G + g, (int)(col0 + c + 1)); }
+    wait_flags(flags + buf * G, G, (int)(col0 + c + 1));
+    for (int cb = c + warp; cb < w; cb += nwarps * kMgsMaxT) {
+      T acc[kMgsMaxT];
+#pragma unroll
+      for (int t = 0; t < kMgsMaxT; ++t) acc[t] = T(0);
+      for (int hh = lane; hh < G; hh += 32) {
+#pragma unroll
+        for (int t = 0; t < kMgsMaxT; ++t) {
+          const int cc = cb + t * nwarps;
+          if (cc < w) acc[t] += __ldcg(part + (size_t)cc * G + hh);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < kMgsMaxT; ++t) {
+        const int cc = cb + t * nwarps;
+        const T v = warp_sum(acc[t]);
+        if (lane == 0 && cc < w) gsum[cc] = v;
+      }
+    }
+    __syncthreads();
+    const T nv = dsqrt(gsum[c]);
+    if (!(nv >= tol)) {
+      if (g == 0 && tid == 0) record_fail(fail, col0 + c + 1);
+      ok = false;
+      break;
+    }
+    // q_c = v_c / ||v_c|| (owner threads), v_{c+1} before its update (owner threads)
+    const T rnv = T(1) / nv;   // q_c = v_c * (1/||v_c||): one division per CTA instead of one per row
+    if (cp == c) {
+#pragma unroll
+      for (int r = 0; r < kMgsRPT; ++r) { x[r] = x[r] * rnv; qs[h * QP + r] = x[r]; }
+    }
+    if (cp == c + 1) {
+#pragma unroll
+      for (int r = 0; r < kMgsRPT; ++r) vs[h * QP + r] = x[r];
+    }
+    __syncthreads();
+    const bool act = mine && cp > c;
+    T acc = T(0);
+    if (act) {
+      const T coef = gsum[cp] * rnv;                        // q_c^T v_cp
+      const T cn = (c + 1 < w) ? gsum[c + 1] * rnv : T(0);  // q_c^T v_{c+1}
+#pragma unroll
+      for (int r = 0; r < kMgsRPT; ++r) {
+        const T qr = qs[h * QP + r];
+        x[r] = fma(-qr, coef, x[r]);                         // v_cp -= q_c (q_c^T v_cp)
+        acc = fma(fma(-qr, cn, vs[h * QP + r]), x[r], acc);  // <v_{c+1}, v_cp> (both updated)
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);             // all lanes take part
+    if (act && h == 0 && c + 1 < w) partbase[(size_t)(buf ^ 1) * G * w + (size_t)cp * G + g] = acc;
+  }
+  if (!ok || !mine) return;
+#pragma unroll
+  for (int r = 0; r < kMgsRPT; ++r) {
+    const int rr = rbase + r;
+    if (rr < rows) dst[r0 + rr + (int64_t)cp * ldd] = x[r];
   }
 }
 
@@ -178,14 +334,17 @@ cudaError_t qr_mgs_panel(int64_t n, int w, const T* src, int64_t lds, T* dst, in
   if (w <= 0) return cudaSuccess;
   MgsGeom g = mgs_geom(n, w, (int)sizeof(T));
   if (g.smem > 220 * 1024) return cudaErrorInvalidValue;   // caller splits wider panels
-  auto k = qr_mgs_kernel<T>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+  if (g.RB > 32 * kMgsRJ) return cudaErrorNotSupported;     // rows per CTA beyond the register budget
+  const bool reg = w <= 128 && g.RB <= 2 * kMgsRPT && getenv("SF_MGS_SMEM") == nullptr;
+  auto k = reg ? qr_mgs_reg_kernel<T> : qr_mgs_kernel<T>;
+  const size_t dyn = reg ? 0 : g.smem;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
   int RB = g.RB;
   void* args[] = {(void*)&n, (void*)&w, (void*)&RB, (void*)&src, (void*)&lds, (void*)&dst, (void*)&ldd,
                   (void*)&col0, (void*)&tol, (void*)&work, (void*)&fail};
   count_launch();
-  return cudaLaunchCooperativeKernel((const void*)k, dim3(g.G), dim3(kMgsThreads), args, g.smem, st);
+  return cudaLaunchCooperativeKernel((const void*)k, dim3(g.G), dim3(kMgsThreads), args, dyn, st);
 }
 
 int qr_mgs_max_width(int64_t n, int elt) {
