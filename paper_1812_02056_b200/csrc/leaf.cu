@@ -63,43 +63,41 @@ __global__ void __launch_bounds__(kLeafT) chol_leaf_kernel(int64_t m, int w, con
   __shared__ T inv[W];
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31;
-  if (tid < 32) {
-    T x[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) x[k] = (lane < w && k <= lane && k < w) ? __ldcg(src + lane + (int64_t)k * lds) : T(0);
-    int ok = 1;
-#pragma unroll
-    for (int c = 0; c < W; ++c) {
-      if (c < w && ok) {
-        T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
-#pragma unroll
-        for (int k = 0; k < c; ++k) {
-          const T lck = __shfl_sync(kFull, x[k], c);
-          if ((k & 3) == 0) a0 = fma(-x[k], lck, a0);
-          else if ((k & 3) == 1) a1 = fma(-x[k], lck, a1);
-          else if ((k & 3) == 2) a2 = fma(-x[k], lck, a2);
-          else a3 = fma(-x[k], lck, a3);
-        }
-        const T t = (a0 + a1) + (a2 + a3);
-        const T d = __shfl_sync(kFull, t, c);
-        if (!(d > T(0))) {
-          ok = 0;
-          if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
+  // Diagonal block: Crout in shared memory, all threads, rolled loops (small code: the
+  // kernel runs once per CTA, so instruction fetch dominates any fully unrolled variant).
+  // Column c: thread (row i = c + tid/4, part = tid%4) sums k = part, part+4, ... < c.
+  for (int idx = tid; idx < W * W; idx += kLeafT) {
+    const int i = idx % W, k = idx / W;
+    Ls[i][k] = (i < w && k <= i) ? __ldcg(src + i + (int64_t)k * lds) : T(0);
+  }
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  {
+    const int part = tid & 3;
+    for (int c = 0; c < w; ++c) {
+      const int i = c + (tid >> 2);
+      T s = T(0);
+      if (i < w)
+        for (int k = part; k < c; k += 4) s = fma(Ls[i][k], Ls[c][k], s);
+      s += __shfl_xor_sync(kFull, s, 1);
+      s += __shfl_xor_sync(kFull, s, 2);
+      const T t = (i < w) ? Ls[i][c] - s : T(0);
+      if (i == c && part == 0) {
+        if (!(t > T(0))) {
+          bad = 1;
+          if (blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
         } else {
-          const T Lcc = leaf_sqrt(d);
-          if (lane == c) x[c] = Lcc;
-          else if (lane > c) x[c] = t / Lcc;
-          if (lane == 0) inv[c] = T(1) / Lcc;
+          const T Lcc = leaf_sqrt(t);
+          Ls[c][c] = Lcc;
+          inv[c] = T(1) / Lcc;
         }
       }
+      __syncthreads();
+      if (bad) return;
+      if (i > c && i < w && part == 0) Ls[i][c] = t / Ls[c][c];
+      __syncthreads();
     }
-#pragma unroll
-    if (lane < W)
-      for (int k = 0; k < W; ++k) Ls[lane][k] = x[k];
-    if (lane == 0) bad = !ok;
   }
-  __syncthreads();
-  if (bad) return;
   // The diagonal block is read by every CTA (redundant factorization) and may be
   // overwritten in place: the LAST CTA to have read it writes the result out.
   if (last_reader(fail + 1)) {
