@@ -334,8 +334,8 @@ static int lu_run(int64_t n, int64_t s, const T* A, int64_t lda, T* LU, int64_t 
 
 // ------------------------------------------------------------------ QR
 static int splitk_for(int64_t M, int64_t N, int64_t K) {
-  const int64_t tiles = ((M + 127) / 128) * ((N + 127) / 128);
-  int64_t sp = (2 * 148 + tiles - 1) / tiles;
+  const int64_t tiles = ((M + 127) / 128) * ((N + 63) / 64);   // gemm_f64 CTA tile 128 x 64, 2 CTAs/SM
+  int64_t sp = (4 * 148 + tiles - 1) / tiles;
   const int64_t maxsp = K / 256 > 1 ? K / 256 : 1;
   if (sp > maxsp) sp = maxsp;
   if (sp > 16) sp = 16;

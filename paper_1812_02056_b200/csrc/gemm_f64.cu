@@ -7,13 +7,14 @@
 //   QR flush         C = B_Q^T B_M ; M[:,c:n] -= B_Q C
 //   QR R             R = Q^T A  (upper tiles only)
 //   in-panel corrections of the recursive panel (same formulas, narrower N).
-// The product S is never materialised: each 128x128 tile of C is read, decremented by the
+// The product S is never materialised: each 128x64 tile of C is read, decremented by the
 // accumulator and written once (Cin may differ from C: out-of-place first step).  MASK
 // restricts work to the lower (Cholesky) or upper (R) triangle of C.
 //
-// Design (DESIGN.md §5 K1/K2): 256 threads = 8 warps as 2 (i) x 4 (j); warp tile 64x32 =
-// 8x4 DMMA atoms (64 fp64 accumulators per lane); 3-stage cp.async pipeline of 128x32
-// operand slices (smem layouts padded so every fragment load is bank-conflict free); the
+// Design (DESIGN.md §5 K1/K2): 128x64 CTA tile, 128 threads = 4 warps as 2 (i) x 2 (j); warp
+// tile 64x32 = 8x4 DMMA atoms (64 fp64 accumulators per lane); 3-stage cp.async pipeline of
+// BK=16 operand slices (smem layouts padded so every fragment load is bank-conflict free);
+// two CTAs per SM (92 KB smem each) so one CTA's epilogue overlaps the other's MMAs; the
 // D fragment is used transposed (D = C^T).  Epilogue: the accumulator tile is parked in
 // the (now idle) pipeline shared memory, then every warp streams whole 1 KB columns of C:
 // all loads of a thread are issued before the first store, in 16-byte vectors, so the
@@ -24,33 +25,43 @@
 namespace sf {
 
 namespace g64 {
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, THREADS = 256;
-constexpr int PAD_IK = BM + 4;    // smem row stride (doubles) for idx-contiguous slices
-constexpr int PAD_KI = BK + 4;    // smem row stride for k-contiguous slices (== 4 mod 16)
-constexpr int OPER = (BK * PAD_IK > BM * PAD_KI) ? BK * PAD_IK : BM * PAD_KI;  // 4608
+// CTA tile BM (i) x BN (j), 4 warps as 2 (i) x 2 (j), warp tile 64 x 32.  ~92 KB of shared
+// memory and <= 255 registers per thread, so TWO CTAs share an SM: one CTA's prologue /
+// epilogue overlaps the other's DMMA main loop (a single 1-CTA/SM kernel leaves the tensor
+// pipe idle during every epilogue).
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, THREADS = 128;
+constexpr int PAD_KI = BK + 4;    // smem row stride (doubles) for k-contiguous slices (== 4 mod 16)
+template <int NIDX> struct Slice {
+  static constexpr int PAD_IK = NIDX + 4;   // row stride for idx-contiguous slices (== 4 mod 16)
+  static constexpr int ELEMS = (BK * PAD_IK > NIDX * PAD_KI) ? BK * PAD_IK : NIDX * PAD_KI;
+  static constexpr int CHUNKS = NIDX * BK / 2 / THREADS;   // 16-byte chunks per thread
+};
+constexpr int OPER_A = Slice<BM>::ELEMS, OPER_B = Slice<BN>::ELEMS;
+constexpr int STAGE = OPER_A + OPER_B;
 constexpr int CPAD = BM + 2;      // epilogue staging column stride
-constexpr size_t SMEM_PIPE = sizeof(double) * (size_t)OPER * 2 * STAGES;      // 216 KiB
-constexpr size_t SMEM_EPI = sizeof(double) * (size_t)BN * CPAD;              // 130 KiB
+constexpr size_t SMEM_PIPE = sizeof(double) * (size_t)STAGE * STAGES;
+constexpr size_t SMEM_EPI = sizeof(double) * (size_t)BN * CPAD;
 constexpr size_t SMEM = SMEM_PIPE > SMEM_EPI ? SMEM_PIPE : SMEM_EPI;
-constexpr int CHUNKS = BM * BK / 2 / THREADS;   // 16-byte chunks per thread per operand slice
+static_assert(2 * SMEM <= 227 * 1024, "two CTAs per SM");
 }  // namespace g64
 
-// Load a 128 (idx) x 32 (k) slice of op(X) into shared memory.
+// Load an NIDX (idx) x BK (k) slice of op(X) into shared memory.
 //  KC=false: op(X)(idx,k) = X[idx + k*ld]  (idx contiguous)  -> Xs[k*PAD_IK + idx]
 //  KC=true : op(X)(idx,k) = X[k + idx*ld]  (k contiguous)    -> Xs[idx*PAD_KI + k]
-template <bool KC, bool V16>
+template <int NIDX, bool KC, bool V16>
 __device__ __forceinline__ void load_slice(double* Xs, const double* __restrict__ X, int64_t ld,
                                            int64_t idx0, int64_t nidx, int64_t k0, int64_t K, int tid) {
   using namespace g64;
+  using S = Slice<NIDX>;
 #pragma unroll
-  for (int r = 0; r < CHUNKS; ++r) {
+  for (int r = 0; r < S::CHUNKS; ++r) {
     const int id = tid + r * THREADS;
     int64_t idx, kg;
     double* dst;
     if (!KC) {
-      const int kk = id / (BM / 2), ch = id % (BM / 2);
+      const int kk = id / (NIDX / 2), ch = id % (NIDX / 2);
       idx = idx0 + 2 * ch; kg = k0 + kk;
-      dst = Xs + kk * PAD_IK + 2 * ch;
+      dst = Xs + kk * S::PAD_IK + 2 * ch;
       const bool kin = kg < K;
       if (V16) {
         const int bytes = (!kin || idx >= nidx) ? 0 : (idx + 1 >= nidx ? 8 : 16);
@@ -77,35 +88,42 @@ __device__ __forceinline__ void load_slice(double* Xs, const double* __restrict_
   }
 }
 
-template <bool KC>
+template <int NIDX, bool KC>
 __device__ __forceinline__ double frag(const double* Xs, int base, int kk, int lane) {
   using namespace g64;
-  if (!KC) return Xs[(kk * 4 + (lane & 3)) * PAD_IK + base + (lane >> 2)];
+  if (!KC) return Xs[(kk * 4 + (lane & 3)) * Slice<NIDX>::PAD_IK + base + (lane >> 2)];
   return Xs[(base + (lane >> 2)) * PAD_KI + kk * 4 + (lane & 3)];
 }
 
 // Map the linear CTA index to a (tile-row, tile-col) pair, visiting only the tiles that
 // intersect the masked triangle.  Tiles are enumerated column by column.
+// Tile column tj covers C columns [tj*BN, tj*BN+BN); tile row ti rows [ti*BM, ti*BM+BM).
+//   lower (i >= j): rows ti >= first_lower(tj) = tj*BN/BM;  upper (i <= j): ti < count_upper(tj).
+__host__ __device__ __forceinline__ int first_lower(int tj) { return (tj * g64::BN) / g64::BM; }
+__host__ __device__ __forceinline__ int count_upper(int tj, int TM) {
+  const int c = (tj * g64::BN + g64::BN - 1) / g64::BM + 1;
+  return c < TM ? c : TM;
+}
 template <int MASK>
 __device__ __forceinline__ void tile_of(int bid, int TM, int TN, int& ti, int& tj) {
   if (MASK == kMaskNone) { ti = bid % TM; tj = bid / TM; return; }
   int j = 0;
   for (; j < TN; ++j) {
-    const int cnt = (MASK == kMaskLower) ? (TM - j) : (j + 1 < TM ? j + 1 : TM);
+    const int cnt = (MASK == kMaskLower) ? (TM - first_lower(j)) : count_upper(j, TM);
     if (bid < cnt) break;
     bid -= cnt;
   }
   tj = j;
-  ti = (MASK == kMaskLower) ? j + bid : bid;
+  ti = (MASK == kMaskLower) ? first_lower(j) + bid : bid;
 }
 
 template <bool AK, bool BKC, bool V16, int MASK>
-__global__ void __launch_bounds__(g64::THREADS, 1) gemm_f64_kernel(GemmF64 p, int vecC) {
+__global__ void __launch_bounds__(g64::THREADS, 2) gemm_f64_kernel(GemmF64 p, int vecC) {
   using namespace g64;
   if (p.fail && failed(p.fail)) return;
   extern __shared__ __align__(16) double smem[];
-  double* As = smem;                       // [STAGES][OPER]
-  double* Bs = smem + STAGES * OPER;       // [STAGES][OPER]
+  double* As = smem;                       // [STAGES][OPER_A]
+  double* Bs = smem + STAGES * OPER_A;     // [STAGES][OPER_B]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;
@@ -125,8 +143,8 @@ __global__ void __launch_bounds__(g64::THREADS, 1) gemm_f64_kernel(GemmF64 p, in
   // Warm L2 with the C tile we will read-modify-write in the epilogue.
   if (p.beta && p.splits == 1) {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int id = tid + r * THREADS;      // 1024 lines: 128 columns x 8 lines of 128 B
+    for (int r = 0; r < BN * 8 / THREADS; ++r) {
+      const int id = tid + r * THREADS;      // BN columns x 8 lines of 128 B
       const int64_t jj = j0 + (id >> 3), ii = i0 + (id & 7) * 16;
       if (jj < p.N && ii < p.M) prefetch_l2(p.Cin + ii + jj * p.ldcin);
     }
@@ -142,8 +160,8 @@ __global__ void __launch_bounds__(g64::THREADS, 1) gemm_f64_kernel(GemmF64 p, in
     if (kb < nk) {
       const int slot = kb % STAGES;
       const int64_t k0 = kbeg + (int64_t)kb * BK;
-      load_slice<AK, V16>(As + slot * OPER, p.A, p.lda, i0, p.M, k0, kend, tid);
-      load_slice<BKC, V16>(Bs + slot * OPER, p.B, p.ldb, j0, p.N, k0, kend, tid);
+      load_slice<BM, AK, V16>(As + slot * OPER_A, p.A, p.lda, i0, p.M, k0, kend, tid);
+      load_slice<BN, BKC, V16>(Bs + slot * OPER_B, p.B, p.ldb, j0, p.N, k0, kend, tid);
     }
     cp_async_commit();
   };
@@ -155,21 +173,21 @@ __global__ void __launch_bounds__(g64::THREADS, 1) gemm_f64_kernel(GemmF64 p, in
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     issue(kb + STAGES - 1);
-    const double* as = As + (kb % STAGES) * OPER;
-    const double* bs = Bs + (kb % STAGES) * OPER;
+    const double* as = As + (kb % STAGES) * OPER_A;
+    const double* bs = Bs + (kb % STAGES) * OPER_B;
     double fa[2][8], fb[2][4];
 #pragma unroll
-    for (int a = 0; a < 8; ++a) fa[0][a] = frag<AK>(as, wm * 64 + a * 8, 0, lane);
+    for (int a = 0; a < 8; ++a) fa[0][a] = frag<BM, AK>(as, wm * 64 + a * 8, 0, lane);
 #pragma unroll
-    for (int b = 0; b < 4; ++b) fb[0][b] = frag<BKC>(bs, wn * 32 + b * 8, 0, lane);
+    for (int b = 0; b < 4; ++b) fb[0][b] = frag<BN, BKC>(bs, wn * 32 + b * 8, 0, lane);
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
       const int cur = kk & 1, nxt = cur ^ 1;
       if (kk + 1 < BK / 4) {
 #pragma unroll
-        for (int a = 0; a < 8; ++a) fa[nxt][a] = frag<AK>(as, wm * 64 + a * 8, kk + 1, lane);
+        for (int a = 0; a < 8; ++a) fa[nxt][a] = frag<BM, AK>(as, wm * 64 + a * 8, kk + 1, lane);
 #pragma unroll
-        for (int b = 0; b < 4; ++b) fb[nxt][b] = frag<BKC>(bs, wn * 32 + b * 8, kk + 1, lane);
+        for (int b = 0; b < 4; ++b) fb[nxt][b] = frag<BN, BKC>(bs, wn * 32 + b * 8, kk + 1, lane);
       }
 #pragma unroll
       for (int a = 0; a < 8; ++a)
@@ -195,9 +213,9 @@ __global__ void __launch_bounds__(g64::THREADS, 1) gemm_f64_kernel(GemmF64 p, in
   }
   __syncthreads();
 
-  // ---- step 2: each warp streams 16 whole columns; lane owns rows 2*lane+{0,1} and
+  // ---- step 2: each warp streams BN/4 whole columns; lane owns rows 2*lane+{0,1} and
   //      64+2*lane+{0,1} (each warp instruction covers 512 contiguous bytes of a column)
-  constexpr int COLS = BN / 8;
+  constexpr int COLS = BN / (THREADS / 32);
   if (p.splits > 1) {
     double* W = p.work + (int64_t)sp * p.M * p.N;
     for (int q = 0; q < COLS; ++q) {
@@ -309,8 +327,8 @@ cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStre
   if (p.splits < 1) p.splits = 1;
   const int TM = (int)((p.M + g64::BM - 1) / g64::BM), TN = (int)((p.N + g64::BN - 1) / g64::BN);
   int ntiles = 0;
-  if (mask == kMaskLower) { for (int j = 0; j < TN; ++j) ntiles += (TM - j > 0 ? TM - j : 0); }
-  else if (mask == kMaskUpper) { for (int j = 0; j < TN; ++j) ntiles += (j + 1 < TM ? j + 1 : TM); }
+  if (mask == kMaskLower) { for (int j = 0; j < TN; ++j) ntiles += (TM - first_lower(j) > 0 ? TM - first_lower(j) : 0); }
+  else if (mask == kMaskUpper) { for (int j = 0; j < TN; ++j) ntiles += count_upper(j, TM); }
   else ntiles = TM * TN;
   if (ntiles == 0) return cudaSuccess;
   const bool v16 = aligned16(p.A, p.lda) && aligned16(p.B, p.ldb);
