@@ -112,6 +112,51 @@ int sf_lu_panel(int64_t m, int64_t w, int64_t ncols_right, int dtype, void* dP, 
 int sf_qr_panel(int64_t n, int64_t w, int dtype, void* dV, int64_t ld, int64_t col0, double tol,
                 int64_t* d_info, void* stream);
 
+/* ---------------------------------------------------------------------------------------
+ * Multi-GPU, one process per GPU (BASELINE.json north_star (3)).
+ *
+ * Block-cyclic column layout: panel p (columns [p*s, min((p+1)*s, n)), the paper's step,
+ * PAPER.md:31) lives on rank p % nranks at local slot p / nranks; a rank stores its panels
+ * full height, column-major, side by side: local column (slot*s + k) is global column
+ * (p*s + k), ld_local >= n, sf_local_cols(n, s, nranks, rank) columns in total.  Per panel
+ * the owner factors it and broadcasts it; each rank then
+ * applies the flush to the local columns right of it.
+ * The results are the single-GPU results, distributed the same way.
+ *
+ * Communicators: sf_comm_init wraps an NCCL communicator (collective over the nranks
+ * processes; rank 0 makes the id with sf_get_unique_id and ships it, e.g. through
+ * torch.distributed).  sf_comm_init_loopback makes ONE process drive all nranks ranks on
+ * its current device (each rank with its own buffers and streams; the broadcast is a device
+ * copy) — the single-GPU test harness of the distributed schedule.
+ *
+ * Pointer arrays: the dist entry points take arrays with sf_comm_local_ranks(comm) entries
+ * (1 for an NCCL communicator: this process's rank; nranks for loopback: rank 0..nranks-1),
+ * each a DEVICE pointer to that rank's local storage or info word.  A rank with no columns
+ * (nranks > number of panels) may pass NULL matrices.  d_info receives the GLOBAL first
+ * failing column (all-reduce min over ranks), 0 on success.  Ownership, stream semantics
+ * and error returns as for the single-GPU calls; NCCL failures return SF_ENCCL.
+ * ------------------------------------------------------------------------------------- */
+typedef struct sf_comm_* sf_comm_t;
+int sf_get_unique_id(uint8_t id[128]);                                          /* NCCL id, rank 0 */
+int sf_comm_init(sf_comm_t* comm, int nranks, int rank, const uint8_t id[128]);  /* collective; current device */
+int sf_comm_init_loopback(sf_comm_t* comm, int nranks);
+int sf_comm_destroy(sf_comm_t comm);
+int sf_comm_size(sf_comm_t comm);
+int sf_comm_local_ranks(sf_comm_t comm);
+int64_t sf_local_cols(int64_t n, int64_t s, int nranks, int rank);
+
+/* Algorithm 1 distributed: dA_local[i] (input, lower triangle of the local columns read)
+ * and dL_local[i] (output L, lower triangle; may equal dA_local[i] for in place). */
+int chol_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* const* dA_local, void* const* dL_local,
+                     int64_t ld_local, int64_t* const* d_info, void* stream);
+/* Algorithm 2 distributed, Crout L (with diagonal) / unit U, packed as in lu_factor. */
+int lu_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* const* dA_local, void* const* dLU_local,
+                   int64_t ld_local, int64_t* const* d_info, void* stream);
+/* Algorithm 3 distributed: local columns of Q and of R = Q^T A (exact zeros below the
+ * diagonal).  Every rank keeps a full n x n copy of Q as workspace (R needs all of it). */
+int qr_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* const* dA_local, void* const* dQ_local,
+                   void* const* dR_local, int64_t ld_local, int64_t* const* d_info, void* stream);
+
 /* Number of flushes the c = z+s schedule performs: floor((n-1)/s). */
 int64_t sf_flush_count(int64_t n, int64_t s);
 /* Cumulative number of kernel launches this library has enqueued in this process

@@ -58,6 +58,24 @@ def lib():
         f = getattr(L, name)
         f.argtypes = args
         f.restype = i32
+    pp = ctypes.POINTER(ctypes.c_void_p)
+    dist_sig = {
+        "chol_factor_dist": [p, i64, i64, i32, pp, pp, i64, pp, p],
+        "lu_factor_dist": [p, i64, i64, i32, pp, pp, i64, pp, p],
+        "qr_factor_dist": [p, i64, i64, i32, pp, pp, pp, i64, pp, p],
+        "sf_get_unique_id": [p],
+        "sf_comm_init": [p, i32, i32, p],
+        "sf_comm_init_loopback": [p, i32],
+        "sf_comm_destroy": [p],
+        "sf_comm_size": [p],
+        "sf_comm_local_ranks": [p],
+    }
+    for name, args in dist_sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = i32
+    L.sf_local_cols.argtypes = [i64, i64, i32, i32]
+    L.sf_local_cols.restype = i64
     L.sf_flush_count.argtypes = [i64, i64]
     L.sf_flush_count.restype = i64
     L.sf_launch_counter.argtypes = []
@@ -78,7 +96,9 @@ def lib():
 EXPORTS = ("chol_factor", "lu_factor", "qr_factor", "chol_factor_host", "lu_factor_host", "qr_factor_host",
            "sf_chol_panel", "sf_syrk_sub", "sf_gemm_sub", "sf_lu_panel", "sf_qr_panel", "sf_flush_count",
            "sf_launch_counter", "sf_strerror", "sf_last_error", "sf_version", "sf_profile_enable",
-           "sf_profile_collect")
+           "sf_profile_collect", "sf_get_unique_id", "sf_comm_init", "sf_comm_init_loopback", "sf_comm_destroy",
+           "sf_comm_size", "sf_comm_local_ranks", "sf_local_cols", "chol_factor_dist", "lu_factor_dist",
+           "qr_factor_dist")
 
 
 def _check(rc):
@@ -223,3 +243,90 @@ def qr_host(hA, s, hQ, hR, dtype=SF_F64):
     _check(lib().qr_factor_host(n, s, dtype, _host_ptr(hA), n, _host_ptr(hQ), n, _host_ptr(hR), n,
                                 ctypes.addressof(info)))
     return hQ, hR, info.value
+
+
+# ----------------------------------------------------------------------- multi-GPU (block-cyclic)
+
+def local_cols(n, s, nranks, rank):
+    """Columns rank `rank` stores: panels p = rank, rank + nranks, ... of width s (the last ragged)."""
+    return int(lib().sf_local_cols(n, s, nranks, rank))
+
+
+def global_columns(n, s, nranks, rank):
+    """Global column index of each local column of `rank` (block-cyclic by s-column panels)."""
+    cols = []
+    for p in range(rank, (n + s - 1) // s, nranks):
+        cols.extend(range(p * s, min((p + 1) * s, n)))
+    return cols
+
+
+class Comm:
+    """A libstepfact communicator: NCCL (one process per GPU) or loopback (all ranks here)."""
+
+    def __init__(self, handle, nranks, local_ranks):
+        self.handle = handle
+        self.nranks = nranks
+        self.local_ranks = local_ranks
+
+    @classmethod
+    def nccl(cls, nranks, rank, uid):
+        h = ctypes.c_void_p()
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(bytes(uid))
+        _check(lib().sf_comm_init(ctypes.byref(h), nranks, rank, buf))
+        return cls(h, nranks, [rank])
+
+    @classmethod
+    def loopback(cls, nranks):
+        h = ctypes.c_void_p()
+        _check(lib().sf_comm_init_loopback(ctypes.byref(h), nranks))
+        return cls(h, nranks, list(range(nranks)))
+
+    def destroy(self):
+        if self.handle is not None:
+            _check(lib().sf_comm_destroy(self.handle))
+            self.handle = None
+
+
+def unique_id():
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().sf_get_unique_id(buf))
+    return bytes(buf)
+
+
+def _ptr_array(xs):
+    arr = (ctypes.c_void_p * len(xs))()
+    for i, x in enumerate(xs):
+        arr[i] = None if x is None else (x.data_ptr() if hasattr(x, "data_ptr") else int(x))
+    return arr
+
+
+def chol_dist(comm, n, s, dA, dL, ld, d_info, dtype=SF_F64, stream=None):
+    """chol_factor_dist: lists (one entry per local rank) of column-major local buffers."""
+    _check(lib().chol_factor_dist(comm.handle, n, s, dtype, _ptr_array(dA), _ptr_array(dL), ld, _ptr_array(d_info),
+                                  _stream(stream)))
+
+
+def lu_dist(comm, n, s, dA, dLU, ld, d_info, dtype=SF_F64, stream=None):
+    _check(lib().lu_factor_dist(comm.handle, n, s, dtype, _ptr_array(dA), _ptr_array(dLU), ld, _ptr_array(d_info),
+                                _stream(stream)))
+
+
+def qr_dist(comm, n, s, dA, dQ, dR, ld, d_info, dtype=SF_F64, stream=None):
+    _check(lib().qr_factor_dist(comm.handle, n, s, dtype, _ptr_array(dA), _ptr_array(dQ), _ptr_array(dR), ld,
+                                _ptr_array(d_info), _stream(stream)))
+
+
+def scatter_cyclic(B, n, s, nranks, rank):
+    """Local block-cyclic storage of `rank` from a column-major buffer B (torch, B[j] = column
+    j): a (local_cols, n) tensor, i.e. column-major local columns with ld = n."""
+    cols = global_columns(n, s, nranks, rank)
+    return B[cols].contiguous()
+
+
+def gather_cyclic(locals_, n, s, nranks, out):
+    """Inverse of scatter_cyclic: write each rank's local columns into the column-major out."""
+    for r, X in enumerate(locals_):
+        cols = global_columns(n, s, nranks, r)
+        if cols:
+            out[cols] = X
+    return out

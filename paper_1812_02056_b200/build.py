@@ -9,6 +9,23 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libstepfact.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dir():
+    """The NCCL that torch itself loads (nvidia-nccl wheel, libnccl.so.2: same soname, so one
+    copy per process), else the system one."""
+    if os.environ.get("SF_NCCL_DIR"):
+        return os.environ["SF_NCCL_DIR"]
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        return list(spec.submodule_search_locations)[0]
+    return "/usr"
+
+
+NCCL_DIR = _nccl_dir()
+NCCL_INC = os.path.join(NCCL_DIR, "include")
+NCCL_LIB = os.path.join(NCCL_DIR, "lib") if NCCL_DIR != "/usr" else "/usr/lib/x86_64-linux-gnu"
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"]
 
@@ -37,7 +54,7 @@ def build(force=False, verbose=False):
     for src in sources():
         obj = os.path.join(PKG, "build", os.path.basename(src) + ".o")
         cmd = [NVCC, *ARCH, *[f for f in FLAGS if f != "-shared"], "-dc" if False else "-c",
-               "-I", os.path.join(ROOT, "include"), "-o", obj, src]
+               "-I", os.path.join(ROOT, "include"), "-I", NCCL_INC, "-o", obj, src]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
@@ -45,7 +62,8 @@ def build(force=False, verbose=False):
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", LIB, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
+    cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", LIB, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread",
+           "-L" + NCCL_LIB, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + NCCL_LIB]
     subprocess.check_call(cmd)
     return LIB
 

@@ -20,8 +20,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/stepfact.h"
-#include "kernels.h"
+#include "drv.cuh"
 
 namespace sf {
 
@@ -30,33 +29,17 @@ void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 static thread_local char g_last_error[512] = "";
 
-// ------------------------------------------------------------------ profiling hook
-// When enabled, CUDA event pairs are recorded on the factorization stream around every
-// flush (trailing update) and every panel, so a benchmark can measure the update
-// kernels' own device time inside its timed region (sf_profile_collect).
-struct ProfRec { cudaEvent_t a, b; int kind; double flops; };
-static bool g_prof = false;
-static std::vector<ProfRec> g_prof_recs;
+// profiling hook state (drv.cuh ProfScope)
+bool g_prof = false;
+std::vector<ProfRec> g_prof_recs;
 static std::vector<cudaEvent_t> g_event_pool;
-static cudaEvent_t pool_event() {
+cudaEvent_t pool_event() {
   if (!g_event_pool.empty()) { cudaEvent_t e = g_event_pool.back(); g_event_pool.pop_back(); return e; }
   cudaEvent_t e; cudaEventCreate(&e); return e;
 }
-struct ProfScope {
-  ProfRec r{}; cudaStream_t st; bool on;
-  ProfScope(int kind, double flops, cudaStream_t s) : st(s), on(g_prof) {
-    if (!on) return;
-    r.a = pool_event(); r.b = pool_event(); r.kind = kind; r.flops = flops;
-    cudaEventRecord(r.a, st);
-  }
-  ~ProfScope() {
-    if (!on) return;
-    cudaEventRecord(r.b, st);
-    g_prof_recs.push_back(r);
-  }
-};
 
-static int fail_with(int code, const char* fmt, ...) {
+
+int fail_with(int code, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
   vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
@@ -64,136 +47,10 @@ static int fail_with(int code, const char* fmt, ...) {
   return code;
 }
 
-#define SF_CUDA(expr)                                                                               \
-  do {                                                                                              \
-    cudaError_t _e = (expr);                                                                        \
-    if (_e != cudaSuccess) return fail_with(SF_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
-                                           __FILE__, __LINE__);                                     \
-  } while (0)
 
-static int leaf_width() {
-  static int w = [] {
-    const char* e = getenv("SF_LEAF");
-    int v = e ? atoi(e) : 32;
-    if (v != 16 && v != 32) v = 32;
-    return v;
-  }();
-  return w;
-}
 
-static int64_t half_of(int64_t w, int leaf) {
-  int64_t h = (w / 2 + leaf - 1) / leaf * leaf;
-  if (h >= w) h = w - leaf;
-  if (h <= 0) h = w / 2;
-  return h;
-}
 
-// ------------------------------------------------------------------ workspace
-struct Workspace {
-  char* base = nullptr;
-  size_t off = 0, cap = 0;
-  cudaStream_t st = nullptr;
-  cudaError_t init(size_t bytes, cudaStream_t s) {
-    st = s;
-    cap = bytes;
-    return cudaMallocAsync((void**)&base, bytes, s);
-  }
-  template <typename U>
-  U* take(size_t n) {
-    off = (off + 255) & ~(size_t)255;
-    U* p = (U*)(base + off);
-    off += n * sizeof(U);
-    return p;
-  }
-  ~Workspace() {
-    if (base) cudaFreeAsync(base, st);
-  }
-};
 
-// ------------------------------------------------------------------ lookahead streams
-// Panel p+1 is factored on a high-priority side stream while the rest of flush p runs on
-// the caller's stream (classic lookahead): the caller's stream first updates only the
-// columns of panel p+1, signals, then updates the remainder of the trailing matrix.
-static bool lookahead_on() {
-  static int on = [] { const char* e = getenv("SF_LOOKAHEAD"); return e ? atoi(e) : 1; }();
-  return on != 0;
-}
-struct Side {
-  cudaStream_t st = nullptr;
-  std::vector<cudaEvent_t> ev;
-  size_t next = 0;
-  // events are re-recorded round-robin: a stream wait captures the event's state at the
-  // time cudaStreamWaitEvent is called, so re-recording afterwards is safe
-  cudaEvent_t event() { return ev[next++ % ev.size()]; }
-};
-static cudaError_t side_stream(Side*& out) {
-  static Side sides[16];
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  Side& sd = sides[dev & 15];
-  if (!sd.st) {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    e = cudaStreamCreateWithPriority(&sd.st, cudaStreamNonBlocking, hi);
-    if (e != cudaSuccess) return e;
-    for (int i = 0; i < 8; ++i) { cudaEvent_t ev; cudaEventCreateWithFlags(&ev, cudaEventDisableTiming); sd.ev.push_back(ev); }
-  }
-  out = &sd;
-  return cudaSuccess;
-}
-// record on `from`, make `to` wait
-static cudaError_t fork_join(Side& sd, cudaStream_t from, cudaStream_t to) {
-  cudaEvent_t e = sd.event();
-  cudaError_t r = cudaEventRecord(e, from);
-  if (r != cudaSuccess) return r;
-  return cudaStreamWaitEvent(to, e, 0);
-}
-
-// ------------------------------------------------------------------ GEMM dispatch per dtype
-template <typename T>
-struct Gemm {
-  int64_t M, N, K;
-  const T* A; int64_t lda; int ak;
-  const T* B; int64_t ldb; int bk;
-  const T* Cin; int64_t ldcin;
-  T* C; int64_t ldc;
-  double alpha; int beta; int mask;
-  int splits; T* work;
-  const long long* fail;
-};
-
-static cudaError_t run_gemm(const Gemm<double>& g, cudaStream_t st) {
-  GemmF64 p{g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, g.Cin, g.ldcin, g.C, g.ldc,
-            g.alpha, g.beta, g.splits, g.work, g.fail};
-  return gemm_f64(p, g.ak, g.bk, g.mask, st);
-}
-static cudaError_t run_gemm(const Gemm<float>&, cudaStream_t) { return cudaErrorNotSupported; }
-
-// C -= op(A) op(B) with C read from Cin (may differ) : common "subtract" form
-template <typename T>
-static cudaError_t gemm_sub(int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, int ak, const T* B,
-                            int64_t ldb, int bk, const T* Cin, int64_t ldcin, T* C, int64_t ldc, int mask,
-                            const long long* fail, cudaStream_t st) {
-  Gemm<T> g{M, N, K, A, lda, ak, B, ldb, bk, Cin, ldcin, C, ldc, -1.0, 1, mask, 1, nullptr, fail};
-  return run_gemm(g, st);
-}
-
-// ------------------------------------------------------------------ Cholesky
-template <typename T>
-static cudaError_t chol_panel_rec(int64_t m, int64_t w, const T* src, int64_t lds, T* dst, int64_t ldd,
-                                  int64_t col0, long long* fail, cudaStream_t st) {
-  const int leaf = leaf_width();
-  if (w <= leaf) return chol_leaf<T>(m, (int)w, src, lds, dst, ldd, col0, fail, st);
-  const int64_t h = half_of(w, leaf);
-  cudaError_t e = chol_panel_rec<T>(m, h, src, lds, dst, ldd, col0, fail, st);
-  if (e != cudaSuccess) return e;
-  // columns [h, w), rows [h, m):  X -= L[h:m, 0:h] * L[h:w, 0:h]^T  (lower part only)
-  e = gemm_sub<T>(m - h, w - h, h, dst + h, ldd, 0, dst + h, ldd, 0, src + h + h * lds, lds, dst + h + h * ldd, ldd,
-                  kMaskLower, fail, st);
-  if (e != cudaSuccess) return e;
-  return chol_panel_rec<T>(m - h, w - h, dst + h + h * ldd, ldd, dst + h + h * ldd, ldd, col0 + h, fail, st);
-}
 
 template <typename T>
 static int chol_run(int64_t n, int64_t s, const T* A, int64_t lda, T* L, int64_t ldl, int64_t* d_info,
@@ -249,27 +106,6 @@ static int chol_run(int64_t n, int64_t s, const T* A, int64_t lda, T* L, int64_t
   return SF_OK;
 }
 
-// ------------------------------------------------------------------ LU
-template <typename T>
-static cudaError_t lu_panel_rec(int64_t m, int64_t w, int64_t ncr, const T* src, int64_t lds, T* dst, int64_t ldd,
-                                int64_t col0, const T* tol, long long* fail, cudaStream_t st) {
-  const int leaf = leaf_width();
-  if (w <= leaf) return lu_leaf<T>(m, ncr, (int)w, src, lds, dst, ldd, col0, tol, fail, st);
-  const int64_t h = half_of(w, leaf);
-  cudaError_t e = lu_panel_rec<T>(m, h, ncr + (w - h), src, lds, dst, ldd, col0, tol, fail, st);
-  if (e != cudaSuccess) return e;
-  // L part and U11 part of the right half: rows [h, m), cols [h, w) -= L[h:m, 0:h] U[0:h, h:w]
-  e = gemm_sub<T>(m - h, w - h, h, dst + h, ldd, 0, dst + h * ldd, ldd, 1, src + h + h * lds, lds, dst + h + h * ldd,
-                  ldd, kMaskNone, fail, st);
-  if (e != cudaSuccess) return e;
-  // U rows [h, w) of the columns right of the panel: -= L[h:w, 0:h] U[0:h, w:w+ncr]
-  if (ncr > 0) {
-    e = gemm_sub<T>(w - h, ncr, h, dst + h, ldd, 0, dst + w * ldd, ldd, 1, src + h + w * lds, lds, dst + h + w * ldd,
-                    ldd, kMaskNone, fail, st);
-    if (e != cudaSuccess) return e;
-  }
-  return lu_panel_rec<T>(m - h, w - h, ncr, dst + h + h * ldd, ldd, dst + h + h * ldd, ldd, col0 + h, tol, fail, st);
-}
 
 template <typename T>
 static int lu_run(int64_t n, int64_t s, const T* A, int64_t lda, T* LU, int64_t ldd, int64_t* d_info,
@@ -332,58 +168,6 @@ static int lu_run(int64_t n, int64_t s, const T* A, int64_t lda, T* LU, int64_t 
   return SF_OK;
 }
 
-// ------------------------------------------------------------------ QR
-static int splitk_for(int64_t M, int64_t N, int64_t K) {
-  const int64_t tiles = ((M + 127) / 128) * ((N + 63) / 64);   // gemm_f64 CTA tile 128 x 64, 2 CTAs/SM
-  int64_t sp = (4 * 148 + tiles - 1) / tiles;
-  const int64_t maxsp = K / 256 > 1 ? K / 256 : 1;
-  if (sp > maxsp) sp = maxsp;
-  if (sp > 16) sp = 16;
-  return (int)(sp < 1 ? 1 : sp);
-}
-
-struct QrWork {
-  void* cw; void* split; void* mgs;
-  int64_t split_elems;
-};
-
-// Project the columns [0, wc) of V (n rows) against the orthonormal columns Qb (n x k):
-//   C = Qb^T V ; V = Vin - Qb C   (PAPER.md:147-155 restricted to the given columns)
-template <typename T>
-static cudaError_t qr_project(int64_t n, int64_t k, int64_t wc, const T* Qb, int64_t ldq, const T* Vin, int64_t ldvin,
-                              T* V, int64_t ldv, T* Cw, T* split, int64_t split_elems, long long* fail,
-                              cudaStream_t st) {
-  int sp = splitk_for(k, wc, n);
-  while (sp > 1 && (int64_t)sp * k * wc > split_elems) --sp;
-  Gemm<T> g1{k, wc, n, Qb, ldq, 1, Vin, ldvin, 1, nullptr, 0, Cw, k, 1.0, 0, kMaskNone, sp, split, fail};
-  cudaError_t e = run_gemm(g1, st);
-  if (e != cudaSuccess) return e;
-  return gemm_sub<T>(n, wc, k, Qb, ldq, 0, Cw, k, 1, Vin, ldvin, V, ldv, kMaskNone, fail, st);
-}
-
-template <typename T>
-static cudaError_t qr_panel(int64_t n, int64_t w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
-                           const T* tol, T* mgswork, T* Cw, T* split, int64_t split_elems, long long* fail,
-                           cudaStream_t st) {
-  const int64_t wmax = qr_mgs_max_width(n, (int)sizeof(T));
-  if (w <= wmax) return qr_mgs_panel<T>(n, (int)w, src, lds, dst, ldd, col0, tol, mgswork, fail, st);
-  // panel wider than one cooperative MGS launch holds: chunks, projected against the
-  // finished chunks of the same panel ("wide QR panels")
-  for (int64_t z0 = 0; z0 < w; z0 += wmax) {
-    const int64_t wc = (wmax < w - z0) ? wmax : w - z0;
-    const T* vin = src + z0 * lds;
-    int64_t ldvin = lds;
-    if (z0 > 0) {
-      cudaError_t e = qr_project<T>(n, z0, wc, dst, ldd, vin, ldvin, dst + z0 * ldd, ldd, Cw, split, split_elems, fail, st);
-      if (e != cudaSuccess) return e;
-      vin = dst + z0 * ldd;
-      ldvin = ldd;
-    }
-    cudaError_t e = qr_mgs_panel<T>(n, (int)wc, vin, ldvin, dst + z0 * ldd, ldd, col0 + z0, tol, mgswork, fail, st);
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
-}
 
 template <typename T>
 static int qr_run(int64_t n, int64_t s, const T* A, int64_t lda, T* Q, int64_t ldq, T* R, int64_t ldr, int64_t* d_info,

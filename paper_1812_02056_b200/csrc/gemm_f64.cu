@@ -98,29 +98,43 @@ __device__ __forceinline__ double frag(const double* Xs, int base, int kk, int l
 // Map the linear CTA index to a (tile-row, tile-col) pair, visiting only the tiles that
 // intersect the masked triangle.  Tiles are enumerated column by column.
 // Tile column tj covers C columns [tj*BN, tj*BN+BN); tile row ti rows [ti*BM, ti*BM+BM).
-//   lower (i >= j): rows ti >= first_lower(tj) = tj*BN/BM;  upper (i <= j): ti < count_upper(tj).
-__host__ __device__ __forceinline__ int first_lower(int tj) { return (tj * g64::BN) / g64::BM; }
-__host__ __device__ __forceinline__ int count_upper(int tj, int TM) {
-  const int c = (tj * g64::BN + g64::BN - 1) / g64::BM + 1;
-  return c < TM ? c : TM;
+// The mask is relative to a diagonal offset `off` (0 unless a grouped launch places the
+// C origin above the diagonal): lower keeps i >= j + off, upper keeps i <= j + off.
+//   lower: rows ti >= first_lower(tj);  upper: ti < count_upper(tj).
+__host__ __device__ __forceinline__ int first_lower(int tj, int64_t off = 0) {
+  const int64_t r = ((int64_t)tj * g64::BN + off) / g64::BM;
+  return r > 0 ? (int)r : 0;
+}
+__host__ __device__ __forceinline__ int count_upper(int tj, int TM, int64_t off = 0) {
+  const int64_t c = ((int64_t)tj * g64::BN + g64::BN - 1 + off) / g64::BM + 1;
+  return c < TM ? (int)c : TM;
+}
+__host__ __device__ __forceinline__ int masked_tiles(int mask, int TM, int TN, int64_t off) {
+  int nt = 0;
+  for (int j = 0; j < TN; ++j) {
+    if (mask == kMaskLower) nt += TM - first_lower(j, off) > 0 ? TM - first_lower(j, off) : 0;
+    else if (mask == kMaskUpper) nt += count_upper(j, TM, off);
+    else nt += TM;
+  }
+  return nt;
 }
 template <int MASK>
-__device__ __forceinline__ void tile_of(int bid, int TM, int TN, int& ti, int& tj) {
+__device__ __forceinline__ void tile_of(int bid, int TM, int TN, int64_t off, int& ti, int& tj) {
   if (MASK == kMaskNone) { ti = bid % TM; tj = bid / TM; return; }
   int j = 0;
   for (; j < TN; ++j) {
-    const int cnt = (MASK == kMaskLower) ? (TM - first_lower(j)) : count_upper(j, TM);
+    const int fl = first_lower(j, off);
+    const int cnt = (MASK == kMaskLower) ? (TM - fl > 0 ? TM - fl : 0) : count_upper(j, TM, off);
     if (bid < cnt) break;
     bid -= cnt;
   }
   tj = j;
-  ti = (MASK == kMaskLower) ? first_lower(j) + bid : bid;
+  ti = (MASK == kMaskLower) ? first_lower(j, off) + bid : bid;
 }
 
 template <bool AK, bool BKC, bool V16, int MASK>
-__global__ void __launch_bounds__(g64::THREADS, 2) gemm_f64_kernel(GemmF64 p, int vecC) {
+__device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vecC) {
   using namespace g64;
-  if (p.fail && failed(p.fail)) return;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;                       // [STAGES][OPER_A]
   double* Bs = smem + STAGES * OPER_A;     // [STAGES][OPER_B]
@@ -129,7 +143,7 @@ __global__ void __launch_bounds__(g64::THREADS, 2) gemm_f64_kernel(GemmF64 p, in
   const int wm = warp & 1, wn = warp >> 1;
   const int TM = (int)((p.M + BM - 1) / BM), TN = (int)((p.N + BN - 1) / BN);
   int ti, tj;
-  tile_of<MASK>(blockIdx.x, TM, TN, ti, tj);
+  tile_of<MASK>(bid, TM, TN, p.off, ti, tj);
   const int64_t i0 = (int64_t)ti * BM, j0 = (int64_t)tj * BN;
 
   // K range of this split
@@ -264,15 +278,34 @@ __global__ void __launch_bounds__(g64::THREADS, 2) gemm_f64_kernel(GemmF64 p, in
       double v0 = p.alpha * d.x, v1 = p.alpha * d.y;
       if (p.beta) { v0 += cin[q][h][0]; v1 += cin[q][h][1]; }
       double* dst = p.C + i + j * p.ldc;
-      const bool pair_in = (i + 1 < p.M) && (MASK == kMaskNone || (MASK == kMaskLower ? i >= j : i + 1 <= j));
+      const int64_t jd = j + p.off;   // diagonal position of column j
+      const bool pair_in = (i + 1 < p.M) && (MASK == kMaskNone || (MASK == kMaskLower ? i >= jd : i + 1 <= jd));
       if (pair_in && vecC) {
         __stcg(reinterpret_cast<double2*>(dst), make_double2(v0, v1));
       } else {
-        if (i < p.M && (MASK == kMaskNone || (MASK == kMaskLower ? i >= j : i <= j))) dst[0] = v0;
-        if (i + 1 < p.M && (MASK == kMaskNone || (MASK == kMaskLower ? i + 1 >= j : i + 1 <= j))) dst[1] = v1;
+        if (i < p.M && (MASK == kMaskNone || (MASK == kMaskLower ? i >= jd : i <= jd))) dst[0] = v0;
+        if (i + 1 < p.M && (MASK == kMaskNone || (MASK == kMaskLower ? i + 1 >= jd : i + 1 <= jd))) dst[1] = v1;
       }
     }
   }
+}
+
+template <bool AK, bool BKC, bool V16, int MASK>
+__global__ void __launch_bounds__(g64::THREADS, 2) gemm_f64_kernel(GemmF64 p, int vecC) {
+  if (p.fail && failed(p.fail)) return;
+  gemm_f64_body<AK, BKC, V16, MASK>(p, blockIdx.x, vecC);
+}
+
+// Grouped launch: several independent C blocks sharing K, the operand leading dimensions
+// and the mask, one CTA grid (the block-cyclic distributed updates).
+template <bool AK, bool BKC, bool V16, int MASK>
+__global__ void __launch_bounds__(g64::THREADS, 2) gemm_f64_grouped_kernel(GemmF64 p, GemmGroups gs, int vecC) {
+  if (p.fail && failed(p.fail)) return;
+  int g = 0;
+  while (g + 1 < gs.count && (int)blockIdx.x >= gs.g[g + 1].tile0) ++g;
+  p.M = gs.g[g].M; p.N = gs.g[g].N; p.off = gs.g[g].off;
+  p.A = gs.g[g].A; p.B = gs.g[g].B; p.Cin = gs.g[g].Cin; p.C = gs.g[g].C;
+  gemm_f64_body<AK, BKC, V16, MASK>(p, (int)blockIdx.x - gs.g[g].tile0, vecC);
 }
 
 // Fixed-order split-K reduction: C = (beta ? Cin : 0) + alpha * sum_sp work[sp].
@@ -290,31 +323,50 @@ __global__ void splitk_reduce_f64(GemmF64 p) {
 }
 
 template <bool AK, bool BKC, bool V16, int MASK>
-static cudaError_t launch_t(const GemmF64& p, int ntiles, int vecC, cudaStream_t st) {
-  auto k = gemm_f64_kernel<AK, BKC, V16, MASK>;
+static cudaError_t launch_t(const GemmF64& p, const GemmGroups* gs, int ntiles, int vecC, cudaStream_t st) {
   static bool attr_set = false;  // per template instance
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g64::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_f64_kernel<AK, BKC, V16, MASK>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g64::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_f64_grouped_kernel<AK, BKC, V16, MASK>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g64::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   dim3 grid(ntiles, p.splits);
-  k<<<grid, g64::THREADS, g64::SMEM, st>>>(p, vecC);
+  if (gs) gemm_f64_grouped_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, *gs, vecC);
+  else gemm_f64_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, vecC);
   count_launch();
   return cudaGetLastError();
 }
 
 template <bool AK, bool BKC, bool V16>
-static cudaError_t launch_mask(const GemmF64& p, int mask, int ntiles, int vecC, cudaStream_t st) {
+static cudaError_t launch_mask(const GemmF64& p, const GemmGroups* gs, int mask, int ntiles, int vecC, cudaStream_t st) {
   switch (mask) {
-    case kMaskLower: return launch_t<AK, BKC, V16, kMaskLower>(p, ntiles, vecC, st);
-    case kMaskUpper: return launch_t<AK, BKC, V16, kMaskUpper>(p, ntiles, vecC, st);
-    default: return launch_t<AK, BKC, V16, kMaskNone>(p, ntiles, vecC, st);
+    case kMaskLower: return launch_t<AK, BKC, V16, kMaskLower>(p, gs, ntiles, vecC, st);
+    case kMaskUpper: return launch_t<AK, BKC, V16, kMaskUpper>(p, gs, ntiles, vecC, st);
+    default: return launch_t<AK, BKC, V16, kMaskNone>(p, gs, ntiles, vecC, st);
   }
 }
 
 static bool aligned16(const void* ptr, int64_t ld) {
   return (((uintptr_t)ptr) & 15) == 0 && (ld % 2) == 0;
+}
+
+static cudaError_t launch_key(const GemmF64& p, const GemmGroups* gs, int a_kcontig, int b_kcontig, bool v16, int mask,
+                              int ntiles, int vecC, cudaStream_t st) {
+  const int key = (a_kcontig ? 1 : 0) | (b_kcontig ? 2 : 0) | (v16 ? 4 : 0);
+  switch (key) {
+    case 0: return launch_mask<false, false, false>(p, gs, mask, ntiles, vecC, st);
+    case 1: return launch_mask<true, false, false>(p, gs, mask, ntiles, vecC, st);
+    case 2: return launch_mask<false, true, false>(p, gs, mask, ntiles, vecC, st);
+    case 3: return launch_mask<true, true, false>(p, gs, mask, ntiles, vecC, st);
+    case 4: return launch_mask<false, false, true>(p, gs, mask, ntiles, vecC, st);
+    case 5: return launch_mask<true, false, true>(p, gs, mask, ntiles, vecC, st);
+    case 6: return launch_mask<false, true, true>(p, gs, mask, ntiles, vecC, st);
+    default: return launch_mask<true, true, true>(p, gs, mask, ntiles, vecC, st);
+  }
 }
 
 cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStream_t st) {
@@ -326,25 +378,11 @@ cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStre
   }
   if (p.splits < 1) p.splits = 1;
   const int TM = (int)((p.M + g64::BM - 1) / g64::BM), TN = (int)((p.N + g64::BN - 1) / g64::BN);
-  int ntiles = 0;
-  if (mask == kMaskLower) { for (int j = 0; j < TN; ++j) ntiles += (TM - first_lower(j) > 0 ? TM - first_lower(j) : 0); }
-  else if (mask == kMaskUpper) { for (int j = 0; j < TN; ++j) ntiles += count_upper(j, TM); }
-  else ntiles = TM * TN;
+  const int ntiles = masked_tiles(mask, TM, TN, p.off);
   if (ntiles == 0) return cudaSuccess;
   const bool v16 = aligned16(p.A, p.lda) && aligned16(p.B, p.ldb);
   const int vecC = aligned16(p.C, p.ldc) && (!p.beta || aligned16(p.Cin, p.ldcin));
-  cudaError_t e;
-  const int key = (a_kcontig ? 1 : 0) | (b_kcontig ? 2 : 0) | (v16 ? 4 : 0);
-  switch (key) {
-    case 0: e = launch_mask<false, false, false>(p, mask, ntiles, vecC, st); break;
-    case 1: e = launch_mask<true, false, false>(p, mask, ntiles, vecC, st); break;
-    case 2: e = launch_mask<false, true, false>(p, mask, ntiles, vecC, st); break;
-    case 3: e = launch_mask<true, true, false>(p, mask, ntiles, vecC, st); break;
-    case 4: e = launch_mask<false, false, true>(p, mask, ntiles, vecC, st); break;
-    case 5: e = launch_mask<true, false, true>(p, mask, ntiles, vecC, st); break;
-    case 6: e = launch_mask<false, true, true>(p, mask, ntiles, vecC, st); break;
-    default: e = launch_mask<true, true, true>(p, mask, ntiles, vecC, st); break;
-  }
+  cudaError_t e = launch_key(p, nullptr, a_kcontig, b_kcontig, v16, mask, ntiles, vecC, st);
   if (e != cudaSuccess || p.splits == 1) return e;
   const int64_t total = p.M * p.N;
   int blocks = (int)((total + 255) / 256);
@@ -352,6 +390,40 @@ cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStre
   splitk_reduce_f64<<<blocks, 256, 0, st>>>(p);
   count_launch();
   return cudaGetLastError();
+}
+
+cudaError_t gemm_f64_grouped(GemmF64 p, const GemmGroup* groups, int count, int a_kcontig, int b_kcontig, int mask,
+                             cudaStream_t st) {
+  // groups with an empty block are dropped; one launch per kMaxGroups groups
+  if (p.K <= 0) return cudaErrorInvalidValue;
+  bool v16 = (p.lda % 2) == 0 && (p.ldb % 2) == 0;
+  int vecC = (p.ldc % 2) == 0 && (!p.beta || (p.ldcin % 2) == 0);
+  p.splits = 1;
+  GemmGroups gs{};
+  int ntiles = 0;
+  for (int i = 0; i < count; ++i) {
+    const GemmGroup& g = groups[i];
+    if (g.M <= 0 || g.N <= 0) continue;
+    v16 = v16 && aligned16(g.A, p.lda) && aligned16(g.B, p.ldb);
+    vecC = vecC && aligned16(g.C, p.ldc) && (!p.beta || aligned16(g.Cin, p.ldcin));
+  }
+  for (int i = 0; i < count; ++i) {
+    GemmGroup g = groups[i];
+    if (g.M <= 0 || g.N <= 0) continue;
+    const int TM = (int)((g.M + g64::BM - 1) / g64::BM), TN = (int)((g.N + g64::BN - 1) / g64::BN);
+    const int nt = masked_tiles(mask, TM, TN, g.off);
+    if (nt == 0) continue;
+    if (gs.count == kMaxGroups) {
+      cudaError_t e = launch_key(p, &gs, a_kcontig, b_kcontig, v16, mask, ntiles, vecC, st);
+      if (e != cudaSuccess) return e;
+      gs.count = 0; ntiles = 0;
+    }
+    g.tile0 = ntiles;
+    gs.g[gs.count++] = g;
+    ntiles += nt;
+  }
+  if (gs.count == 0) return cudaSuccess;
+  return launch_key(p, &gs, a_kcontig, b_kcontig, v16, mask, ntiles, vecC, st);
 }
 
 }  // namespace sf

@@ -27,8 +27,22 @@ struct GemmF64 {
   int splits;
   double* work;
   const long long* fail;   // device "first failed column" word; kernels exit early if set
+  int64_t off = 0;         // mask diagonal offset: lower keeps i >= j + off, upper i <= j + off
 };
 cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStream_t st);
+
+// Grouped launch: `count` independent blocks C_g(M_g x N_g) = Cin_g + alpha op(A_g) op(B_g),
+// sharing K, lda/ldb/ldc/ldcin, alpha/beta and the mask (each with its own diagonal offset)
+// — one grid for all of them (p's M, N, A, B, Cin, C, off are ignored; splits = 1).
+struct GemmGroup {
+  int64_t M, N, off;
+  const double* A; const double* B; const double* Cin; double* C;
+  int tile0;   // set by the launcher
+};
+constexpr int kMaxGroups = 16;
+struct GemmGroups { int count; GemmGroup g[kMaxGroups]; };
+cudaError_t gemm_f64_grouped(GemmF64 p, const GemmGroup* groups, int count, int a_kcontig, int b_kcontig, int mask,
+                             cudaStream_t st);
 
 // ---------------------------------------------------------------- panels (templated T)
 // Cholesky leaf (Alg. 1 inner loops) on columns [0,w) of the m x w block
@@ -42,6 +56,12 @@ cudaError_t chol_leaf(int64_t m, int w, const T* src, int64_t lds, T* dst, int64
 template <typename T>
 cudaError_t lu_leaf(int64_t m, int64_t ncols_right, int w, const T* src, int64_t lds, T* dst,
                     int64_t ldd, int64_t col0, const T* tol, long long* fail, cudaStream_t st);
+
+// LU U rows only, against an already factored diagonal block L11 (ldl): the U part of
+// lu_leaf for ncols columns (block-cyclic distributed LU).
+template <typename T>
+cudaError_t lu_usolve_leaf(int64_t ncols, int w, const T* l11, int64_t ldl, const T* src, int64_t lds, T* dst,
+                           int64_t ldd, const long long* fail, cudaStream_t st);
 
 // QR panel, modified Gram-Schmidt (Alg. 3) on n x w columns.
 template <typename T>

@@ -270,6 +270,68 @@ cudaError_t lu_leaf(int64_t m, int64_t ncr, int w, const T* src, int64_t lds, T*
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ LU, U rows only
+// The U part of lu_leaf_kernel against an ALREADY FACTORED diagonal block: L11 (w x w,
+// lower incl. diagonal, at `l11`) is read, not recomputed.  Used by the block-cyclic
+// distributed LU (dist.cu), where a rank holds the received L panel but not the original
+// diagonal block: U_cj = (A_cj - sum_{k<c} L_ck U_kj) / L_cc for the
+// ncols columns at src.  Same per-element arithmetic as lu_leaf_kernel's U part.
+template <typename T, int W>
+__global__ void __launch_bounds__(kLeafT) lu_usolve_kernel(int64_t ncols_total, int w, const T* __restrict__ l11,
+                                                           int64_t ldl, const T* __restrict__ src, int64_t lds,
+                                                           T* __restrict__ dst, int64_t ldd, const long long* fail) {
+  if (failed(fail)) return;
+  __shared__ T Ls[W][W + 1];
+  __shared__ T inv[W];
+  __shared__ T S[kUCols][W + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < W * W; idx += kLeafT) {
+    const int c = idx % W, k = idx / W;
+    Ls[c][k] = (c < w && k <= c) ? __ldcg(l11 + c + (int64_t)k * ldl) : T(0);
+  }
+  __syncthreads();
+  if (tid < w) inv[tid] = T(1) / Ls[tid][tid];
+  const int64_t j0 = (int64_t)blockIdx.x * kUCols;
+  const int ncols = (int)((ncols_total - j0) < kUCols ? (ncols_total - j0) : kUCols);
+  for (int jj = warp; jj < ncols; jj += kLeafT / 32)
+    if (lane < w) S[jj][lane] = __ldcg(src + lane + (j0 + jj) * lds);
+  __syncthreads();
+  if (tid < ncols) {
+    T y[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) y[k] = (k < w) ? S[tid][k] : T(0);
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      T a0 = y[c], a1 = T(0), a2 = T(0), a3 = T(0);
+#pragma unroll
+      for (int k = 0; k < c; ++k) {
+        if ((k & 3) == 0) a0 = fma(-Ls[c][k], y[k], a0);
+        else if ((k & 3) == 1) a1 = fma(-Ls[c][k], y[k], a1);
+        else if ((k & 3) == 2) a2 = fma(-Ls[c][k], y[k], a2);
+        else a3 = fma(-Ls[c][k], y[k], a3);
+      }
+      y[c] = ((a0 + a1) + (a2 + a3)) * inv[c];
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) S[tid][k] = y[k];
+  }
+  __syncthreads();
+  for (int jj = warp; jj < ncols; jj += kLeafT / 32)
+    if (lane < w) dst[lane + (j0 + jj) * ldd] = S[jj][lane];
+}
+
+template <typename T>
+cudaError_t lu_usolve_leaf(int64_t ncols, int w, const T* l11, int64_t ldl, const T* src, int64_t lds, T* dst,
+                           int64_t ldd, const long long* fail, cudaStream_t st) {
+  if (w <= 0 || ncols <= 0) return cudaSuccess;
+  const int grid = (int)((ncols + kUCols - 1) / kUCols);
+  if (w <= 16) lu_usolve_kernel<T, 16><<<grid, kLeafT, 0, st>>>(ncols, w, l11, ldl, src, lds, dst, ldd, fail);
+  else if (w <= 32) lu_usolve_kernel<T, 32><<<grid, kLeafT, 0, st>>>(ncols, w, l11, ldl, src, lds, dst, ldd, fail);
+  else return cudaErrorInvalidValue;
+  count_launch();
+  return cudaGetLastError();
+}
+
 template cudaError_t chol_leaf<double>(int64_t, int, const double*, int64_t, double*, int64_t, int64_t, long long*,
                                        cudaStream_t);
 template cudaError_t chol_leaf<float>(int64_t, int, const float*, int64_t, float*, int64_t, int64_t, long long*,
@@ -278,5 +340,10 @@ template cudaError_t lu_leaf<double>(int64_t, int64_t, int, const double*, int64
                                      const double*, long long*, cudaStream_t);
 template cudaError_t lu_leaf<float>(int64_t, int64_t, int, const float*, int64_t, float*, int64_t, int64_t,
                                     const float*, long long*, cudaStream_t);
+
+template cudaError_t lu_usolve_leaf<double>(int64_t, int, const double*, int64_t, const double*, int64_t, double*,
+                                            int64_t, const long long*, cudaStream_t);
+template cudaError_t lu_usolve_leaf<float>(int64_t, int, const float*, int64_t, const float*, int64_t, float*, int64_t,
+                                           const long long*, cudaStream_t);
 
 }  // namespace sf

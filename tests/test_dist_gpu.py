@@ -1,0 +1,169 @@
+"""GPU parity of the block-cyclic multi-GPU drivers.
+
+One B200 is available, so the distributed schedule is exercised through a LOOPBACK
+communicator (include/stepfact.h): one process drives all G ranks, each with its own
+local buffers and streams, the panel broadcast a device copy — the same per-rank code,
+events and lookahead as the NCCL path.  The NCCL path itself runs at G=1 (a real NCCL
+communicator, broadcast and all-reduce included).
+
+Bars: Cholesky distributed == single-GPU bit for bit (same per-element arithmetic, see
+dist.cu); all three against the CPU oracle at the fp64 bar (R2 <= 1e-10, residual,
+QR tail rule) — DESIGN.md §3 P6/P7.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1812_02056_b200 as sf  # noqa: E402
+from tests.test_parity_gpu import EPS, TOL64, check_qr, dev, host, run_chol  # noqa: E402
+
+
+def run_dist(kind, A, s, G, comm=None, inplace=False):
+    n = A.shape[0]
+    B = dev(A)                                   # column-major buffer
+    own = comm is None
+    comm = comm or sf.Comm.loopback(G)
+    try:
+        ranks = comm.local_ranks
+        Aloc = [sf.scatter_cyclic(B, n, s, G, r) for r in ranks]
+        Aref = [a.clone() for a in Aloc]
+        info = [torch.full((1,), -1, dtype=torch.int64, device="cuda") for _ in ranks]
+        if kind == "qr":
+            Q = [torch.full_like(a, 5.0) for a in Aloc]
+            R = [torch.full_like(a, 3.0) for a in Aloc]
+            sf.qr_dist(comm, n, s, Aloc, Q, R, n, info)
+            torch.cuda.synchronize()
+            for a, b in zip(Aloc, Aref):
+                assert torch.equal(a, b), "QR input modified"
+            outs = (Q, R)
+        else:
+            X = Aloc if inplace else [torch.full_like(a, 7.0) for a in Aloc]
+            (sf.chol_dist if kind == "chol" else sf.lu_dist)(comm, n, s, Aloc, X, n, info)
+            torch.cuda.synchronize()
+            if not inplace:
+                for a, b in zip(Aloc, Aref):
+                    assert torch.equal(a, b), "out-of-place input modified"
+            outs = (X,)
+        infos = [int(i.item()) for i in info]
+        assert len(set(infos)) == 1, infos
+        full = []
+        for X in outs:
+            Y = torch.zeros_like(B)
+            sf.gather_cyclic(X, n, s, G, Y)
+            full.append(host(Y))
+        return full, infos[0]
+    finally:
+        if own:
+            comm.destroy()
+
+
+CASES = [(1, 1, 1), (5, 2, 2), (64, 16, 2), (130, 32, 3), (257, 64, 2), (300, 64, 4), (300, 100, 8),
+         (520, 128, 3), (1000, 168, 4), (96, 96, 2)]
+
+
+@pytest.mark.parametrize("n,s,G", CASES)
+def test_chol_dist_loopback(n, s, G):
+    A = synth.gen_numpy("paper_spd", n, seed=n + G)
+    (Lg,), info = run_dist("chol", A, s, G)
+    assert info == 0
+    Lo, io = oracle.chol(A, s)
+    assert io == 0
+    assert synth.r2_error(np.tril(Lg), Lo) <= TOL64
+    # untouched strict upper (out of place: the 7.0 fill survives)
+    assert np.all(Lg[np.triu_indices(n, 1)] == 7.0)
+    # bitwise equal to the single-GPU driver
+    L1, _ = run_chol(A, s, inplace=False)
+    assert np.array_equal(np.tril(Lg), np.tril(L1))
+
+
+@pytest.mark.parametrize("n,s,G", [(300, 64, 2), (1000, 128, 4)])
+def test_chol_dist_inplace_and_planted(n, s, G):
+    Lx = synth.planted_chol(n, seed=n + s)
+    (Lg,), info = run_dist("chol", Lx @ Lx.T, s, G, inplace=True)
+    assert info == 0 and np.array_equal(np.tril(Lg), Lx)
+
+
+def test_chol_dist_not_pd_info():
+    B = synth.gen_numpy("paper_spd", 300, seed=3)
+    B[200, 200] = -5.0
+    io = oracle.chol(B, 64)[1]
+    for G in (1, 2, 3):
+        assert run_dist("chol", B, 64, G)[1] == io == 201
+
+
+@pytest.mark.parametrize("n,s,G", CASES)
+def test_lu_dist_loopback(n, s, G):
+    A = synth.gen_numpy("diag_dominant", n, seed=n + G)
+    (F,), info = run_dist("lu", A, s, G)
+    assert info == 0
+    Lo, Uo, io = oracle.lu(A, s)
+    Lg, Ug = np.tril(F), np.triu(F, 1) + np.eye(n)
+    assert synth.r2_error(Lg, Lo) <= TOL64 and synth.r2_error(Ug, Uo) <= TOL64
+    assert synth.rel_residual(A, Lg, Ug) <= 1e-13 * n
+
+
+def test_lu_dist_planted_and_info():
+    n, s = 700, 64
+    Lx, Ux = synth.planted_lu(n, seed=3)
+    (F,), info = run_dist("lu", Lx @ Ux, s, 3)
+    assert info == 0 and np.array_equal(np.tril(F), Lx) and np.array_equal(np.triu(F, 1) + np.eye(n), Ux)
+    A = np.array([[0.0, 1.0], [1.0, 1.0]])          # SPEC.md:485 zero pivot
+    assert run_dist("lu", A, 1, 2)[1] == 1
+
+
+@pytest.mark.parametrize("n,s,G", [(1, 1, 1), (64, 16, 2), (130, 32, 3), (257, 64, 2), (300, 64, 4), (520, 128, 3)])
+def test_qr_dist_loopback(n, s, G):
+    A = synth.gen_numpy("gaussian", n, seed=n + G)
+    (Qg, Rg), info = run_dist("qr", A, s, G)
+    assert info == 0
+    Qo, Ro, io, _ = oracle.qr(A, s)
+    check_qr(A, s, Qg, Rg, Qo, Ro)
+
+
+def test_qr_dist_planted():
+    n, s = 1024, 128
+    Qx, Rx = synth.planted_qr(n, seed=7)
+    (Qg, Rg), info = run_dist("qr", Qx @ Rx, s, 2)
+    assert info == 0 and np.array_equal(Qg, Qx) and np.array_equal(Rg, Rx)
+
+
+def test_nccl_comm_single_rank():
+    """The real NCCL transport (one rank): broadcast + all-reduce through NCCL."""
+    uid = sf.unique_id()
+    comm = sf.Comm.nccl(1, 0, uid)
+    try:
+        A = synth.gen_numpy("spd_scaled", 600, seed=1)
+        (Lg,), info = run_dist("chol", A, 128, 1, comm=comm)
+        assert info == 0
+        L1, _ = run_chol(A, 128, inplace=False)
+        assert np.array_equal(np.tril(Lg), np.tril(L1))
+        B = synth.gen_numpy("diag_dominant", 500, seed=2)
+        (F,), info = run_dist("lu", B, 96, 1, comm=comm)
+        Lo, Uo, _ = oracle.lu(B, 96)
+        assert info == 0 and synth.r2_error(np.tril(F), Lo) <= TOL64
+        C = synth.gen_numpy("gaussian", 300, seed=3)
+        (Qg, Rg), info = run_dist("qr", C, 64, 1, comm=comm)
+        Qo, Ro, _, _ = oracle.qr(C, 64)
+        assert info == 0
+        check_qr(C, 64, Qg, Rg, Qo, Ro)
+    finally:
+        comm.destroy()
+
+
+def test_chol_dist_cfg5_shape_sampled():
+    """cfg5's layout (s=512, G=8 ranks) at n=8192 on one GPU: the distributed factor equals
+    the single-GPU factor bit for bit and its first columns match the oracle."""
+    n, s, G, K = 8192, 512, 8, 512
+    A = synth.gen_torch("spd_scaled", n, seed=0)
+    An = A.cpu().numpy()
+    (Lg,), info = run_dist("chol", An, s, G)
+    assert info == 0
+    L1, _ = run_chol(An, s, inplace=False)
+    assert np.array_equal(np.tril(Lg), np.tril(L1))
+    Lo, io = oracle.chol(np.asfortranarray(An[:, :K]), s, kcols=K)
+    assert io == 0 and synth.r2_error(np.tril(Lg)[:, :K], Lo[:, :K]) <= TOL64
