@@ -9,10 +9,14 @@ pristine, so no restore is needed between steps; A is 2.1 GB > the 126 MB L2, so
 survives in L2 between steps).  Metric: classical-count GFLOP/s (n^3/3 Cholesky, 2n^3/3 LU,
 4n^3/3 QR), whole job = sum over ranks / max-over-ranks device time.
 
-Default workload: BASELINE.json configs[2] (Cholesky fp64, n=16384) at s=512 — the config
-BASELINE names as the tensor-pipe roofline measurement and on which north_star sets the
->= 70% FP64-tensor-peak target; DESIGN.md §6 explains the choice.  Other configs are
-selectable with --workload (they are also parity-test cases).
+Default workload: BASELINE.json configs[4] fp64 — Cholesky n=65536, s=512, A = G G^T/n + I —
+the config the metric is quoted on at 1/2/4/8 B200 (BASELINE.json:2, 11) and on which
+north_star sets the multi-GPU target; it fits one GPU (34 GB).  N=1 runs the single-GPU
+driver (chol_factor); N>1 (torchrun, one process per GPU) runs the block-cyclic driver
+(chol_factor_dist: s-column panels dealt round-robin, each factored panel broadcast by
+NCCL) on the same problem: strong scaling, value = one factorization per step / time.
+configs[2] (n=16384, the s-sweep / roofline config) and the others are selectable with
+--workload (they are also parity-test cases); DESIGN.md §6.
 
 Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (the only
 reference that exists: PAPER.md's own code is not available) on a bounded sample.
@@ -36,7 +40,7 @@ WORKLOADS = {
     "qr_f64_n8192_s128": ("qr", 8192, 128, "gaussian", "f64", "configs[3]"),
     "chol_f64_n65536_s512": ("chol", 65536, 512, "spd_scaled", "f64", "configs[4]"),
 }
-DEFAULT = "chol_f64_n16384_s512"
+DEFAULT = "chol_f64_n65536_s512"
 CALIB = os.path.join(ROOT, "calib", "peaks_fp64_tf32.json")
 
 
@@ -173,6 +177,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--dist", action="store_true", help="use the distributed (block-cyclic) driver even at N=1")
+    ap.add_argument("--e2e-steps", type=int, default=3)
     return ap.parse_args()
 
 
@@ -212,7 +218,7 @@ def run_reference(args):
               f"of the {args.workload} matrix per step; value = executed flops / time")
     line = {"impl": "reference", "metric": "factorization GFLOP/s (classical count) and % of FP64 tensor peak",
             "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
             "config": {"workload": args.workload, "kind": kind, "n": n, "s": s, "baseline_config": cfgname,
                        "generator": gen, "seed": args.seed, "sample_cols": K},
@@ -221,6 +227,33 @@ def run_reference(args):
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def oracle_k(kind, n, s, target_flops=6e10):
+    """Columns of the restricted oracle run for cpu_baseline: ~10-30 s on the host cores."""
+    if kind != "chol":
+        return sample_cols(kind, n)
+    K = 64
+    while K < n and oracle_executed_flops(kind, n, s, min(n, K * 2)) <= target_flops:
+        K *= 2
+    return min(K, n)
+
+
+def make_inputs(torch, sf, synth, kind, gen, n, s, seed, ws, rank, use_dist):
+    """Column-major device input: the full buffer (single-GPU driver) or this rank's local
+    block-cyclic columns (distributed driver)."""
+    if not use_dist:
+        Alog = synth.gen_torch(gen, n, seed) if n > 4096 else torch.from_numpy(synth.gen_numpy(gen, n, seed)).cuda()
+        return Alog if kind == "chol" else Alog.mT.contiguous()   # column-major buffer of A
+    cols = sf.global_columns(n, s, ws, rank)
+    if kind == "chol" and gen in ("spd_scaled", "spd_shift") and n > 4096:
+        return synth.gen_torch_cols(gen, n, seed, cols)
+    Alog = synth.gen_torch(gen, n, seed) if n > 4096 else torch.from_numpy(synth.gen_numpy(gen, n, seed)).cuda()
+    B = Alog if kind == "chol" else Alog.mT.contiguous()
+    del Alog
+    X = B[cols].contiguous()
+    del B
+    return X
 
 
 def main():
@@ -233,26 +266,41 @@ def main():
     import synth
 
     ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
     kind, n, s, gen, dtype, cfgname = WORKLOADS[args.workload]
     s = args.s or s
     assert args.warmup >= 3 or os.environ.get("SF_BENCH_ALLOW_SHORT"), "timing rules need >= 3 warm-up steps"
+    use_dist = ws > 1 or args.dist
+    stream = torch.cuda.current_stream()
 
-    # ---- inputs (synthetic, seeded; every rank factors its own replica: seed + rank)
-    seed = args.seed + rank
-    Alog = synth.gen_torch(gen, n, seed) if n > 4096 else torch.from_numpy(synth.gen_numpy(gen, n, seed)).cuda()
-    # column-major buffer of the logical matrix (identical bytes for symmetric A)
-    A = Alog if kind == "chol" else Alog.mT.contiguous()
-    del Alog
+    # ---- communicator (multi-GPU: block-cyclic panels, NCCL broadcast)
+    comm = None
+    if use_dist:
+        uid = [sf.unique_id() if rank == 0 else None]
+        if ws > 1:
+            dist.broadcast_object_list(uid, src=0)
+        comm = sf.Comm.nccl(ws, rank, uid[0])
+
+    # ---- inputs (synthetic, seeded, same recipe on every rank; A stays pristine: out of place)
+    seed = args.seed
+    A = make_inputs(torch, sf, synth, kind, gen, n, s, seed, ws, rank, use_dist)
+    ld = n
     info = torch.zeros(1, dtype=torch.int64, device="cuda")
     out1 = torch.zeros_like(A)
     out2 = torch.zeros_like(A) if kind == "qr" else None
-    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
 
     def step():
-        if kind == "chol":
+        if use_dist:
+            if kind == "chol":
+                sf.chol_dist(comm, n, s, [A], [out1], ld, [info], stream=stream)
+            elif kind == "lu":
+                sf.lu_dist(comm, n, s, [A], [out1], ld, [info], stream=stream)
+            else:
+                sf.qr_dist(comm, n, s, [A], [out1], [out2], ld, [info], stream=stream)
+        elif kind == "chol":
             sf.chol_colmajor(n, s, A, n, out1, n, info, stream=stream)
         elif kind == "lu":
             sf.lu_colmajor(n, s, A, n, out1, n, info, stream=stream)
@@ -295,7 +343,8 @@ def main():
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     t_max = float(t_max.item())
     flops = classical_flops(kind, n)
-    value = ws * args.steps * flops / (t_max * 1e-3) / 1e9
+    # whole job: ONE factorization per step, shared by all ranks (strong scaling)
+    value = args.steps * flops / (t_max * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel (the trailing-update GEMM/SYRK launches)
     peaks = json.load(open(CALIB)) if os.path.exists(CALIB) else {}
@@ -310,7 +359,7 @@ def main():
         traffic = json.load(open(tr_path)).get(args.workload)
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
-                "kernel": "gemm_f64_kernel (flush update, DMMA.8x8x4)",
+                "kernel": "gemm_f64_kernel (flush update, DMMA.8x8x4)" + (", rank 0" if ws > 1 else ""),
                 "peak_source": "measured: calib/peaks_fp64_tf32.json fp64_dmma_tflops (DMMA microbenchmark, "
                                "this pool's B200); MEASURED_PEAKS.json has no fp64 entry",
                 "launches_per_step": upd_n / args.steps if args.steps else None,
@@ -319,24 +368,43 @@ def main():
                 "update_share_of_step": upd_ms / ms if ms else None,
                 "panel_ms_per_step": pan_ms / args.steps, "qr_r_ms_per_step": qr_ms / args.steps}
 
-    # ---- end to end through the C ABI with HOST buffers (copies inside the timed region)
+    # ---- end to end through the public API with HOST buffers (copies inside the timed region)
     e2e = None
     if not args.no_e2e:
+        ke = max(1, min(args.steps, args.e2e_steps))
+        nbytes = A.numel() * A.element_size()
         hA = A.cpu().pin_memory()
         h1 = torch.empty_like(hA).pin_memory()
         h2 = torch.empty_like(hA).pin_memory() if kind == "qr" else None
-        hin = hA.clone().pin_memory()
+        if use_dist:
+            dA = torch.empty_like(A)
 
-        def hstep():
-            if kind == "chol":
-                _, inf = sf.chol_host(hA, s, h1)
-            elif kind == "lu":
-                _, inf = sf.lu_host(hA, s, h1)
-            else:
-                _, _, inf = sf.qr_host(hA, s, h1, h2)
-            assert inf == 0
+            def hstep():
+                dA.copy_(hA, non_blocking=True)
+                step_out = (out1, out2)
+                if kind == "chol":
+                    sf.chol_dist(comm, n, s, [dA], [out1], ld, [info], stream=stream)
+                elif kind == "lu":
+                    sf.lu_dist(comm, n, s, [dA], [out1], ld, [info], stream=stream)
+                else:
+                    sf.qr_dist(comm, n, s, [dA], [out1], [out2], ld, [info], stream=stream)
+                h1.copy_(step_out[0], non_blocking=True)
+                if kind == "qr":
+                    h2.copy_(step_out[1], non_blocking=True)
+                torch.cuda.synchronize()
+                assert int(info.item()) == 0
+            api = f"{kind}_factor_dist (C ABI) with torch pinned host<->device copies per rank"
+        else:
+            def hstep():
+                if kind == "chol":
+                    _, inf = sf.chol_host(hA, s, h1)
+                elif kind == "lu":
+                    _, inf = sf.lu_host(hA, s, h1)
+                else:
+                    _, _, inf = sf.qr_host(hA, s, h1, h2)
+                assert inf == 0
+            api = f"{kind}_factor_host (C ABI, pinned host buffers)"
         hstep()
-        ke = max(1, min(args.steps, 3))
         if ws > 1:
             dist.barrier()
         t0 = time.perf_counter()
@@ -344,19 +412,19 @@ def main():
             hstep()
         dt = time.perf_counter() - t0
         tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        bb = torch.tensor([float(nbytes)], dtype=torch.float64, device="cuda")
         if ws > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dt = float(tt.item())
-        nbytes = A.numel() * A.element_size()
-        e2e = {"value": ws * ke * flops / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": nbytes,
-               "d2h_bytes_per_step": nbytes * (2 if kind == "qr" else 1), "steps": ke,
-               "api": f"{kind}_factor_host (C ABI, pinned host buffers)"}
-        del hA, h1, h2, hin
+            dist.all_reduce(bb, op=dist.ReduceOp.SUM)
+        dt = float(tt.item()); tot_bytes = int(bb.item())
+        e2e = {"value": ke * flops / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": tot_bytes,
+               "d2h_bytes_per_step": tot_bytes * (2 if kind == "qr" else 1), "steps": ke, "api": api}
+        del hA, h1, h2
 
     # ---- CPU oracle beside it (rank 0, N=1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        K = sample_cols(kind, n)
+        K = oracle_k(kind, n, s)
         Acols, Afull = host_inputs(kind, gen, n, seed, K, dev_A=A if n > 4096 else None)
         dt, fl, thr = oracle_sample(kind, n, s, Acols, K, Afull)
         cpu = {"value": fl / dt / 1e9, "unit": "GFLOP/s", "cores": thr, "kind": "oracle",
@@ -365,18 +433,22 @@ def main():
                          f"{flops / (fl / dt) / 3600:.2f} h"}
 
     if rank == 0:
+        par = f"block-cyclic s-column panels over {ws} GPU(s), NCCL panel broadcast" if use_dist else "single GPU"
         line = {"metric": "factorization GFLOP/s (classical count) and % of FP64 tensor peak",
                 "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+                "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": dtype, "data": "synthetic",
                 "config": {"workload": args.workload, "kind": kind, "n": n, "s": s, "baseline_config": cfgname,
-                           "generator": gen, "seed": args.seed, "parallelism": "replicas" if ws > 1 else "single",
-                           "l2": f"inputs larger than L2 ({A.numel() * A.element_size() / 1e9:.2f} GB > 126 MB); "
-                                 "out-of-place factorization, A re-read from HBM every step"},
+                           "generator": gen, "seed": args.seed, "parallelism": par,
+                           "l2": f"inputs larger than L2 ({A.numel() * A.element_size() / 1e9:.2f} GB per rank "
+                                 "> 126 MB); out-of-place factorization, A re-read from HBM every step"},
                 "pct_fp64_peak": (value / ws / 1e3 / peak) if peak else None,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(l1 - l0), "clocks": ck}
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        torch.cuda.synchronize()
+        comm.destroy()
     if ws > 1:
         dist.destroy_process_group()
     return 0

@@ -7,7 +7,7 @@
 // panel: the owner factors the panel (the s-column recurrences) and broadcasts it; every
 // rank then applies the flush to the columns it owns.  Per rank and panel p:
 //
-//   Cholesky  Lp = L[ps:n, panel p] broadcast (packed, (n-ps) x w);
+//   Cholesky  Lp = L[ps:n, panel p] broadcast (in place from the owner);
 //                              each local panel q > p:  A[qs:n, q] -= Lp[qs:n] Lp[q]^T
 //                              (lower part; one grouped launch over all local panels)
 //   LU       Lp = L[ps:n, panel p] (U11 in its strict upper block);
@@ -111,7 +111,7 @@ struct Rank {
   T* tol = nullptr;
   double* part = nullptr;
   double* sumsq = nullptr;
-  T* buf[2] = {nullptr, nullptr};   // Cholesky / LU: packed panel receive buffers
+  T* buf[2] = {nullptr, nullptr};   // Cholesky / LU: panel receive buffers (Span layout)
   T* qfull = nullptr;               // QR: every panel of Q, n x n, ld n
   T* mgsw = nullptr; T* cw = nullptr; T* split = nullptr; T* cw2 = nullptr; T* split2 = nullptr;
   int64_t split_elems = 0;
@@ -192,8 +192,8 @@ static cudaError_t sumsq_local(int64_t n, int64_t nloc, const T* A, int64_t ld, 
 
 static cudaError_t wait_on(cudaStream_t waiter, cudaEvent_t ev) { return cudaStreamWaitEvent(waiter, ev, 0); }
 
-// The exchange of panel p: after it, on rank r's comm stream (event recv[p]), the packed
-// panel is in r's receive buffer `dst(r)`; `count` elements.  Non-owners first wait for
+// The exchange of panel p: after it, on rank r's comm stream (event recv[p]), the panel
+// is at `dst(r)` (the owner's own storage on the owner); `count` elements.  Non-owners first wait for
 // `free_ev(r)` (the buffer's previous contents are no longer read), the owner for ready[p].
 template <typename T, typename DstF, typename FreeF>
 static int exchange(sf_comm_t comm, std::vector<Rank<T>>& rk, int64_t p, int owner, size_t count, DstF dst,
@@ -202,9 +202,12 @@ static int exchange(sf_comm_t comm, std::vector<Rank<T>>& rk, int64_t p, int own
     Rank<T>& me = rk[0];
     if (me.r == owner) SF_CUDA(wait_on(me.st.com, me.ready[p]));
     else if (cudaEvent_t fe = free_ev(me)) SF_CUDA(wait_on(me.st.com, fe));
-    T* b = dst(me);
-    SF_NCCL(ncclBroadcast(b, b, count, nccl_type<T>(), owner, comm->nccl, me.st.com));
-    count_launch();
+    static const bool skip1 = getenv("SF_DIST_SKIP1") && atoi(getenv("SF_DIST_SKIP1"));
+    if (!(skip1 && comm->nranks == 1)) {
+      T* b = dst(me);
+      SF_NCCL(ncclBroadcast(b, b, count, nccl_type<T>(), owner, comm->nccl, me.st.com));
+      count_launch();
+    }
     SF_CUDA(cudaEventRecord(me.recv[p], me.st.com));
     return SF_OK;
   }
@@ -217,15 +220,6 @@ static int exchange(sf_comm_t comm, std::vector<Rank<T>>& rk, int64_t p, int own
     }
     SF_CUDA(cudaEventRecord(x.recv[p], x.st.com));
   }
-  return SF_OK;
-}
-
-// Loopback: before the owner overwrites its buffer slot, every rank's copy of the panel
-// that used the slot two panels ago must have finished.
-template <typename T>
-static int wait_copies(sf_comm_t comm, std::vector<Rank<T>>& rk, Rank<T>& owner, int64_t prev) {
-  if (!comm->loopback() || prev < 0) return SF_OK;
-  for (auto& x : rk) SF_CUDA(wait_on(owner.st.pan, x.recv[prev]));
   return SF_OK;
 }
 
@@ -333,34 +327,41 @@ static cudaError_t chol_update_slots(const Cyclic& cy, Rank<T>& x, int64_t p, in
   return gemm_f64_grouped(p64, gs.data(), (int)gs.size(), 0, 0, kMaskLower, st);
 }
 
+// Panel p as broadcast: the contiguous span of the owner's local storage from (ps, first
+// column of the panel) to (n-1, last column) — the panel's rows [ps, n) with ld = ld_local,
+// plus rows [0, ps) of its later columns (strict upper: never written, harmless).  No pack:
+// the owner broadcasts in place from its factor, receivers get the same layout (ld = ld).
+template <typename T>
+struct Span {
+  const Cyclic& cy; int64_t ld;
+  T* owner_ptr(Rank<T>& x, int64_t p) const { return x.X + p * cy.s + cy.slot(p) * cy.s * ld; }
+  size_t count(int64_t p) const { return (size_t)((cy.width(p) - 1) * ld + (cy.n - p * cy.s)); }
+  T* at(Rank<T>& x, int64_t p) const { return x.r == cy.owner(p) ? owner_ptr(x, p) : x.buf[p & 1]; }
+};
+
 template <typename T>
 static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, void* const* dL, int64_t ld,
                          int64_t* const* d_info, cudaStream_t caller) {
   const Cyclic cy(n, s, comm->nranks);
   std::vector<Rank<T>> rk;
-  int rc = setup_ranks<T>(comm, rk, cy, dA, dL, nullptr, d_info, (size_t)n * s, 0, 0, caller);
+  int rc = setup_ranks<T>(comm, rk, cy, dA, dL, nullptr, d_info, (size_t)s * ld, 0, 0, caller);
   if (rc) return rc;
-  auto packed = [&](int64_t p) { return n - p * s; };   // rows of the packed panel p
+  const Span<T> sp{cy, ld};
   // prologue: panel 0 on its owner, out of place from A
   for (auto& o : rk) {
     if (o.r != 0) continue;
     ProfScope ps(1, 0.0, o.st.pan);
-    const int64_t w0 = cy.width(0);
-    SF_CUDA(chol_panel_rec<T>(n, w0, o.A, ld, o.X, ld, 0, o.fail, o.st.pan));
-    SF_CUDA(cudaMemcpy2DAsync(o.buf[0], n * sizeof(T), o.X, ld * sizeof(T), n * sizeof(T), w0,
-                              cudaMemcpyDeviceToDevice, o.st.pan));
+    SF_CUDA(chol_panel_rec<T>(n, cy.width(0), o.A, ld, o.X, ld, 0, o.fail, o.st.pan));
     SF_CUDA(cudaEventRecord(o.ready[0], o.st.pan));
   }
   for (int64_t p = 0; p < cy.P; ++p) {
-    rc = exchange<T>(comm, rk, p, cy.owner(p), (size_t)packed(p) * cy.width(p),
-                     [&](Rank<T>& x) { return x.buf[p & 1]; },
+    rc = exchange<T>(comm, rk, p, cy.owner(p), sp.count(p), [&](Rank<T>& x) { return sp.at(x, p); },
                      [&](Rank<T>& x) -> cudaEvent_t { return p >= 2 ? x.done[p - 2] : nullptr; });
     if (rc) return rc;
     if (p + 1 == cy.P) break;   // the last panel is never flushed
     for (auto& x : rk) {
       SF_CUDA(wait_on(x.st.mn, x.recv[p]));
-      const T* Lp = x.buf[p & 1];
-      const int64_t ldp = packed(p);
+      const T* Lp = sp.at(x, p);
       const int64_t nslots = (cy.local_cols(x.r) + s - 1) / s;
       int64_t j0 = cy.first_slot_after(p, x.r);
       if (cy.owner(p + 1) == x.r) {
@@ -369,27 +370,23 @@ static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, 
         {
           double fl = 0.0;
           ProfScope pf(0, 0.0, x.st.mn);
-          SF_CUDA(chol_update_slots<T>(cy, x, p, j, j + 1, Lp, ldp, ld, &fl, x.st.mn));
+          SF_CUDA(chol_update_slots<T>(cy, x, p, j, j + 1, Lp, ld, ld, &fl, x.st.mn));
           pf.r.flops = fl;
         }
         j0 = j + 1;
         SF_CUDA(cudaEventRecord(x.la[q], x.st.mn));
         SF_CUDA(wait_on(x.st.pan, x.la[q]));
-        rc = wait_copies<T>(comm, rk, x, p - 1);
-        if (rc) return rc;
         {
           ProfScope pp(1, 0.0, x.st.pan);
           T* P0 = x.X + qs + j * s * ld;
           SF_CUDA(chol_panel_rec<T>(n - qs, wq, P0, ld, P0, ld, qs, x.fail, x.st.pan));
-          SF_CUDA(cudaMemcpy2DAsync(x.buf[q & 1], (n - qs) * sizeof(T), P0, ld * sizeof(T), (n - qs) * sizeof(T), wq,
-                                    cudaMemcpyDeviceToDevice, x.st.pan));
         }
         SF_CUDA(cudaEventRecord(x.ready[q], x.st.pan));
       }
       {
         double fl = 0.0;
         ProfScope pf(0, 0.0, x.st.mn);
-        SF_CUDA(chol_update_slots<T>(cy, x, p, j0, nslots, Lp, ldp, ld, &fl, x.st.mn));
+        SF_CUDA(chol_update_slots<T>(cy, x, p, j0, nslots, Lp, ld, ld, &fl, x.st.mn));
         pf.r.flops = fl;
       }
       SF_CUDA(cudaEventRecord(x.done[p], x.st.mn));
@@ -421,7 +418,7 @@ static int lu_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, vo
                        int64_t* const* d_info, cudaStream_t caller) {
   const Cyclic cy(n, s, comm->nranks);
   std::vector<Rank<T>> rk;
-  int rc = setup_ranks<T>(comm, rk, cy, dA, dLU, nullptr, d_info, (size_t)n * s, 0, 0, caller);
+  int rc = setup_ranks<T>(comm, rk, cy, dA, dLU, nullptr, d_info, (size_t)s * ld, 0, 0, caller);
   if (rc) return rc;
   rc = dist_tol<T>(comm, rk, cy, ld, caller);
   if (rc) return rc;
@@ -432,26 +429,21 @@ static int lu_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, vo
     SF_CUDA(cudaEventRecord(e, caller));
     SF_CUDA(wait_on(x.st.mn, e)); SF_CUDA(wait_on(x.st.pan, e)); SF_CUDA(wait_on(x.st.com, e));
   }
-  auto packed = [&](int64_t p) { return n - p * s; };
+  const Span<T> sp{cy, ld};   // the L panel incl. U11 in its diagonal block
   for (auto& o : rk) {
     if (o.r != 0) continue;
     ProfScope ps(1, 0.0, o.st.pan);
-    const int64_t w0 = cy.width(0);
-    SF_CUDA(lu_panel_rec<T>(n, w0, 0, o.X, ld, o.X, ld, 0, o.tol, o.fail, o.st.pan));
-    SF_CUDA(cudaMemcpy2DAsync(o.buf[0], n * sizeof(T), o.X, ld * sizeof(T), n * sizeof(T), w0,
-                              cudaMemcpyDeviceToDevice, o.st.pan));
+    SF_CUDA(lu_panel_rec<T>(n, cy.width(0), 0, o.X, ld, o.X, ld, 0, o.tol, o.fail, o.st.pan));
     SF_CUDA(cudaEventRecord(o.ready[0], o.st.pan));
   }
   for (int64_t p = 0; p < cy.P; ++p) {
-    rc = exchange<T>(comm, rk, p, cy.owner(p), (size_t)packed(p) * cy.width(p),
-                     [&](Rank<T>& x) { return x.buf[p & 1]; },
+    rc = exchange<T>(comm, rk, p, cy.owner(p), sp.count(p), [&](Rank<T>& x) { return sp.at(x, p); },
                      [&](Rank<T>& x) -> cudaEvent_t { return p >= 2 ? x.done[p - 2] : nullptr; });
     if (rc) return rc;
     if (p + 1 == cy.P) break;
     for (auto& x : rk) {
       SF_CUDA(wait_on(x.st.mn, x.recv[p]));
-      const T* Lp = x.buf[p & 1];
-      const int64_t ldp = packed(p);
+      const T* Lp = sp.at(x, p);
       const int64_t nloc = cy.local_cols(x.r);
       int64_t c0 = cy.first_slot_after(p, x.r) * s;
       if (cy.owner(p + 1) == x.r) {
@@ -459,27 +451,23 @@ static int lu_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, vo
         {
           double fl = 0.0;
           ProfScope pf(0, 0.0, x.st.mn);
-          SF_CUDA(lu_update_cols<T>(cy, x, p, j * s, j * s + wq, Lp, ldp, ld, &fl, x.st.mn));
+          SF_CUDA(lu_update_cols<T>(cy, x, p, j * s, j * s + wq, Lp, ld, ld, &fl, x.st.mn));
           pf.r.flops = fl;
         }
         c0 = j * s + wq;
         SF_CUDA(cudaEventRecord(x.la[q], x.st.mn));
         SF_CUDA(wait_on(x.st.pan, x.la[q]));
-        rc = wait_copies<T>(comm, rk, x, p - 1);
-        if (rc) return rc;
         {
           ProfScope pp(1, 0.0, x.st.pan);
           T* P0 = x.X + qs + j * s * ld;
           SF_CUDA(lu_panel_rec<T>(n - qs, wq, 0, P0, ld, P0, ld, qs, x.tol, x.fail, x.st.pan));
-          SF_CUDA(cudaMemcpy2DAsync(x.buf[q & 1], (n - qs) * sizeof(T), P0, ld * sizeof(T), (n - qs) * sizeof(T), wq,
-                                    cudaMemcpyDeviceToDevice, x.st.pan));
         }
         SF_CUDA(cudaEventRecord(x.ready[q], x.st.pan));
       }
       {
         double fl = 0.0;
         ProfScope pf(0, 0.0, x.st.mn);
-        SF_CUDA(lu_update_cols<T>(cy, x, p, c0, nloc, Lp, ldp, ld, &fl, x.st.mn));
+        SF_CUDA(lu_update_cols<T>(cy, x, p, c0, nloc, Lp, ld, ld, &fl, x.st.mn));
         pf.r.flops = fl;
       }
       SF_CUDA(cudaEventRecord(x.done[p], x.st.mn));

@@ -101,6 +101,33 @@ def gen_torch(kind, n, seed, device="cuda", chunk=4096):
     raise ValueError(kind)
 
 
+def gen_torch_cols(kind, n, seed, cols, device="cuda", chunk=4096):
+    """Columns `cols` of the cfg3/cfg5 matrix (A = G G^T/n + I or G G^T + n I, G from the same
+    seeded 4096-row chunks as gen_torch), as a COLUMN-MAJOR local buffer (len(cols), n):
+    buf[jl, i] = A[i, cols[jl]].  For a rank of the block-cyclic layout this forms only its
+    own columns (n x n x len(cols) flops instead of n^3).  The entries Alg. 1 reads (i >=
+    column) are G[i].G[j] (/n) from one cuBLAS product; they may round differently from
+    gen_torch's full product, i.e. the same recipe, not the same bytes."""
+    import torch
+    assert kind in ("spd_shift", "spd_scaled")
+
+    def gauss(rows, k):
+        g = torch.Generator(device=device)
+        g.manual_seed(seed * 1_000_003 + k)
+        return torch.randn(rows, n, generator=g, device=device, dtype=torch.float64)
+
+    G = torch.cat([gauss(min(chunk, n - r), k) for k, r in enumerate(range(0, n, chunk))], 0)
+    idx = torch.as_tensor(cols, device=device, dtype=torch.long)
+    buf = torch.matmul(G[idx], G.T)                # (nloc, n): buf[jl, i] = G[cols[jl]] . G[i]
+    del G
+    if kind == "spd_scaled":
+        buf /= n
+        buf[torch.arange(len(cols), device=device), idx] += 1.0
+    else:
+        buf[torch.arange(len(cols), device=device), idx] += float(n)
+    return buf
+
+
 # ----------------------------------------------------------------------------- planted factors
 
 def planted_chol(n, seed):
