@@ -107,6 +107,68 @@ static int chol_run(int64_t n, int64_t s, const T* A, int64_t lda, T* L, int64_t
 }
 
 
+// fp32 Cholesky: fp32 storage and panel, 3xTF32 tcgen05 flush.  Same
+// schedule and lookahead as chol_run; each panel's split (hi/lo) lives in one of two
+// buffers so the side stream can split panel p+1 while the flush of panel p reads panel p's.
+static int chol_run_f32(int64_t n, int64_t s, const float* A, int64_t lda, float* L, int64_t ldl, int64_t* d_info,
+                        cudaStream_t st) {
+  const int64_t ldk = (s + 3) / 4 * 4;
+  Workspace ws;
+  SF_CUDA(ws.init(4096 + 4 * sizeof(float) * (size_t)n * ldk + 4 * 256, st));
+  long long* fail = ws.take<long long>(2);
+  SplitBuf sb[2];
+  for (int b = 0; b < 2; ++b) {
+    sb[b].h = ws.take<float>((size_t)n * ldk);
+    sb[b].l = ws.take<float>((size_t)n * ldk);
+    sb[b].ldk = ldk;
+  }
+  SF_CUDA(init_fail(fail, st));
+  Side* sd = nullptr;
+  const bool la = lookahead_on() && s < n;
+  if (la) SF_CUDA(side_stream(sd));
+  {
+    ProfScope ps(1, 0.0, st);
+    const int64_t w0 = s < n ? s : n;
+    SF_CUDA(chol_panel_rec_f32(n, w0, A, lda, L, ldl, 0, sb[0], fail, st));
+    if (w0 < n) SF_CUDA(split_tf32(n - w0, w0, L + w0, ldl, sb[0].at(w0, 0).h, sb[0].at(w0, 0).l, ldk, st));
+  }
+  int64_t p = 0;
+  for (int64_t z = 0; z < n; z += s, ++p) {
+    const int64_t w = (s < n - z) ? s : n - z, c = z + w;
+    if (c >= n) break;
+    const int64_t w2 = (s < n - c) ? s : n - c, m = n - c;
+    const float* src = (z == 0) ? A : L;
+    const int64_t lds = (z == 0) ? lda : ldl;
+    const SplitBuf R = sb[p & 1].at(w, 0);       // R = L[c:n, z:c), split
+    SplitBuf& nxt = sb[(p + 1) & 1];
+    cudaStream_t pst = la ? sd->st : st;
+    if (la) {
+      ProfScope ps(0, 3.0 * w * ((double)m * (m + 1) - (double)(m - w2) * (m - w2 + 1)), st);
+      SF_CUDA(syrk_tf32(m, w2, w, R, R, src + c + c * lds, lds, L + c + c * ldl, ldl, fail, st));
+      SF_CUDA(fork_join(*sd, st, pst));
+    } else {
+      ProfScope ps(0, 3.0 * w * (double)m * (double)(m + 1), st);
+      SF_CUDA(syrk_tf32(m, m, w, R, R, src + c + c * lds, lds, L + c + c * ldl, ldl, fail, st));
+    }
+    {
+      ProfScope ps(1, 0.0, pst);
+      SF_CUDA(chol_panel_rec_f32(m, w2, L + c + c * ldl, ldl, L + c + c * ldl, ldl, c, nxt, fail, pst));
+      if (w2 < m) SF_CUDA(split_tf32(m - w2, w2, L + c + w2 + c * ldl, ldl, nxt.at(w2, 0).h, nxt.at(w2, 0).l, ldk, pst));
+    }
+    if (la) {
+      if (m > w2) {
+        const int64_t c2 = c + w2;
+        ProfScope ps(0, 3.0 * w * (double)(m - w2) * (double)(m - w2 + 1), st);
+        SF_CUDA(syrk_tf32(m - w2, m - w2, w, R.at(w2, 0), R.at(w2, 0), src + c2 + c2 * lds, lds, L + c2 + c2 * ldl, ldl,
+                          fail, st));
+      }
+      SF_CUDA(fork_join(*sd, pst, st));
+    }
+  }
+  SF_CUDA(finish_info(fail, d_info, st));
+  return SF_OK;
+}
+
 template <typename T>
 static int lu_run(int64_t n, int64_t s, const T* A, int64_t lda, T* LU, int64_t ldd, int64_t* d_info,
                   cudaStream_t st) {
@@ -287,7 +349,7 @@ int chol_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, vo
   if (!d_info) return fail_with(SF_EINVAL, "null d_info");
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == SF_F64) return chol_run<double>(n, s, (const double*)dA, lda, (double*)dL, ldl, d_info, st);
-  return fail_with(SF_ENOTSUP, "fp32 Cholesky not built yet");
+  return chol_run_f32(n, s, (const float*)dA, lda, (float*)dL, ldl, d_info, st);
 }
 
 int lu_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dLU, int64_t ldlu, int64_t* d_info,
@@ -379,23 +441,42 @@ int qr_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda,
 // ------------------------------------------------------------------ building blocks
 int sf_chol_panel(int64_t m, int64_t w, int dtype, void* dP, int64_t ld, int64_t col0, int64_t* d_info, void* stream) {
   if (m < 1 || w < 1 || w > m || ld < m || !dP || !d_info) return fail_with(SF_EINVAL, "bad panel arguments");
-  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp64 only");
+  if (dtype != SF_F64 && dtype != SF_F32) return fail_with(SF_EINVAL, "unknown dtype %d", dtype);
   cudaStream_t st = (cudaStream_t)stream;
+  const int64_t ldk = (w + 3) / 4 * 4;
   Workspace ws;
-  SF_CUDA(ws.init(256, st));
+  SF_CUDA(ws.init(256 + (dtype == SF_F32 ? 2 * sizeof(float) * (size_t)m * ldk + 512 : 0), st));
   long long* fail = ws.take<long long>(2);   // [0] first failed column, [1] leaf counter
   SF_CUDA(init_fail(fail, st));
-  SF_CUDA(chol_panel_rec<double>(m, w, (double*)dP, ld, (double*)dP, ld, col0, fail, st));
+  if (dtype == SF_F64) {
+    SF_CUDA(chol_panel_rec<double>(m, w, (double*)dP, ld, (double*)dP, ld, col0, fail, st));
+  } else {
+    SplitBuf sb{ws.take<float>((size_t)m * ldk), nullptr, ldk};
+    sb.l = ws.take<float>((size_t)m * ldk);
+    SF_CUDA(chol_panel_rec_f32(m, w, (float*)dP, ld, (float*)dP, ld, col0, sb, fail, st));
+  }
   SF_CUDA(finish_info(fail, d_info, st));
   return SF_OK;
 }
 
 int sf_syrk_sub(int64_t m, int64_t k, int dtype, const void* dR, int64_t ldr, void* dC, int64_t ldc, void* stream) {
   if (m < 0 || k < 0 || !dR || !dC || ldr < m || ldc < m) return fail_with(SF_EINVAL, "bad syrk arguments");
-  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp64 only");
-  const double* R = (const double*)dR;
-  SF_CUDA(gemm_sub<double>(m, m, k, R, ldr, 0, R, ldr, 0, (double*)dC, ldc, (double*)dC, ldc, kMaskLower, nullptr,
-                           (cudaStream_t)stream));
+  if (dtype != SF_F64 && dtype != SF_F32) return fail_with(SF_EINVAL, "unknown dtype %d", dtype);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SF_F64) {
+    const double* R = (const double*)dR;
+    SF_CUDA(gemm_sub<double>(m, m, k, R, ldr, 0, R, ldr, 0, (double*)dC, ldc, (double*)dC, ldc, kMaskLower, nullptr, st));
+    return SF_OK;
+  }
+  if (m == 0 || k == 0) return SF_OK;
+  // fp32: split R once (3xTF32, K-major), then the tcgen05 update
+  const int64_t ldk = (k + 3) / 4 * 4;
+  Workspace ws;
+  SF_CUDA(ws.init(2 * sizeof(float) * (size_t)m * ldk + 1024, st));
+  SplitBuf sb{ws.take<float>((size_t)m * ldk), nullptr, ldk};
+  sb.l = ws.take<float>((size_t)m * ldk);
+  SF_CUDA(split_tf32(m, k, (const float*)dR, ldr, sb.h, sb.l, ldk, st));
+  SF_CUDA(syrk_tf32(m, m, k, sb, sb, (float*)dC, ldc, (float*)dC, ldc, nullptr, st));
   return SF_OK;
 }
 

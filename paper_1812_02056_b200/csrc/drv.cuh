@@ -169,6 +169,40 @@ inline cudaError_t chol_panel_rec(int64_t m, int64_t w, const T* src, int64_t ld
   return chol_panel_rec<T>(m - h, w - h, dst + h + h * ldd, ldd, dst + h + h * ldd, ldd, col0 + h, fail, st);
 }
 
+// ------------------------------------------------------------------ fp32 Cholesky panel
+// K-major 3xTF32 split of one panel (hi / lo), row r / column k relative to the panel's
+// top-left entry: element at h[r*ldk + k].
+struct SplitBuf {
+  float* h; float* l; int64_t ldk;
+  SplitBuf at(int64_t r, int64_t k) const { return SplitBuf{h + r * ldk + k, l + r * ldk + k, ldk}; }
+};
+
+inline cudaError_t syrk_tf32(int64_t M, int64_t N, int64_t K, const SplitBuf& a, const SplitBuf& b, const float* Cin,
+                             int64_t ldcin, float* C, int64_t ldc, const long long* fail, cudaStream_t st) {
+  Tf32Gemm g{M, N, K, a.h, a.l, a.ldk, b.h, b.l, b.ldk, Cin, ldcin, C, ldc, kMaskLower, 0, fail};
+  return gemm_tf32x3(g, st);
+}
+
+// Same recursion as chol_panel_rec; the left half's columns are split (hi/lo, K-major) into
+// `sb` before the 3xTF32 correction of the right half.  On return the panel's columns are
+// split for rows [w, m) only up to the last left half: the caller splits the whole panel
+// for the flush.
+inline cudaError_t chol_panel_rec_f32(int64_t m, int64_t w, const float* src, int64_t lds, float* dst, int64_t ldd,
+                                      int64_t col0, SplitBuf sb, long long* fail, cudaStream_t st) {
+  const int leaf = leaf_width();
+  if (w <= leaf) return chol_leaf<float>(m, (int)w, src, lds, dst, ldd, col0, fail, st);
+  const int64_t h = half_of(w, leaf);
+  cudaError_t e = chol_panel_rec_f32(m, h, src, lds, dst, ldd, col0, sb, fail, st);
+  if (e != cudaSuccess) return e;
+  e = split_tf32(m - h, h, dst + h, ldd, sb.at(h, 0).h, sb.at(h, 0).l, sb.ldk, st);
+  if (e != cudaSuccess) return e;
+  const SplitBuf lh = sb.at(h, 0);
+  e = syrk_tf32(m - h, w - h, h, lh, lh, src + h + h * lds, lds, dst + h + h * ldd, ldd, fail, st);
+  if (e != cudaSuccess) return e;
+  return chol_panel_rec_f32(m - h, w - h, dst + h + h * ldd, ldd, dst + h + h * ldd, ldd, col0 + h, sb.at(h, h), fail,
+                            st);
+}
+
 // ------------------------------------------------------------------ LU
 template <typename T>
 inline cudaError_t lu_panel_rec(int64_t m, int64_t w, int64_t ncr, const T* src, int64_t lds, T* dst, int64_t ldd,

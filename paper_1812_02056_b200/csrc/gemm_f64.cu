@@ -21,6 +21,7 @@
 // read-modify-write costs about one L2/HBM round trip per tile instead of one per atom.
 #include "common.cuh"
 #include "kernels.h"
+#include "tiles.cuh"
 
 namespace sf {
 
@@ -95,69 +96,10 @@ __device__ __forceinline__ double frag(const double* Xs, int base, int kk, int l
   return Xs[(base + (lane >> 2)) * PAD_KI + kk * 4 + (lane & 3)];
 }
 
-// Map the linear CTA index to a (tile-row, tile-col) pair, visiting only the tiles that
-// intersect the masked triangle.  Tiles are enumerated column by column.
-// Tile column tj covers C columns [tj*BN, tj*BN+BN); tile row ti rows [ti*BM, ti*BM+BM).
-// The mask is relative to a diagonal offset `off` (0 unless a grouped launch places the
-// C origin above the diagonal): lower keeps i >= j + off, upper keeps i <= j + off.
-//   lower: rows ti >= first_lower(tj);  upper: ti < count_upper(tj).
-__host__ __device__ __forceinline__ int first_lower(int tj, int64_t off = 0) {
-  const int64_t r = ((int64_t)tj * g64::BN + off) / g64::BM;
-  return r > 0 ? (int)r : 0;
-}
-__host__ __device__ __forceinline__ int count_upper(int tj, int TM, int64_t off = 0) {
-  const int64_t c = ((int64_t)tj * g64::BN + g64::BN - 1 + off) / g64::BM + 1;
-  return c < TM ? (int)c : TM;
-}
-// sum_{i=0}^{n-1} floor((a*i + b) / m) for a, b >= 0, m > 0 (Euclid-like reduction, O(log m)).
-__host__ __device__ __forceinline__ int64_t floor_sum(int64_t n, int64_t m, int64_t a, int64_t b) {
-  int64_t ans = 0;
-  while (n > 0) {
-    if (a >= m) { ans += (n - 1) * n / 2 * (a / m); a %= m; }
-    if (b >= m) { ans += n * (b / m); b %= m; }
-    const int64_t y = a * n + b;
-    if (y < m) break;
-    n = y / m; b = y % m;
-    const int64_t t = m; m = a; a = t;
-  }
-  return ans;
-}
-// Number of masked tiles in tile columns [0, j) — O(log), so a CTA finds its tile by a
-// binary search instead of a scan over all tile columns (m = 65536 has 1024 of them).
-// Requires off >= 0 (every caller's diagonal is on or below the C origin row).
-__host__ __device__ __forceinline__ int64_t mask_prefix(int mask, int64_t j, int TM, int TN, int64_t off) {
-  using namespace g64;
-  if (j > TN) j = TN;
-  if (mask == kMaskNone) return j * TM;
-  if (mask == kMaskLower) {
-    // columns t with first_lower(t) < TM: t < (TM*BM - off)/BN
-    int64_t J = ((int64_t)TM * BM - off + BN - 1) / BN;
-    if (J < 0) J = 0;
-    if (J > TN) J = TN;
-    if (j > J) j = J;
-    return j * TM - floor_sum(j, BM, BN, off);
-  }
-  // upper: count_upper(t) = min(TM, h(t)), h(t) = floor((t*BN + BN-1 + off)/BM) + 1
-  int64_t t1 = ((int64_t)(TM - 1) * BM - BN + 1 - off + BN - 1) / BN;
-  if ((int64_t)(TM - 1) * BM - BN + 1 - off <= 0) t1 = 0;
-  if (t1 > TN) t1 = TN;
-  if (j <= t1) return floor_sum(j, BM, BN, BN - 1 + off) + j;
-  return floor_sum(t1, BM, BN, BN - 1 + off) + t1 + (j - t1) * TM;
-}
+using T64 = Tiles<g64::BM, g64::BN>;
+__host__ __device__ __forceinline__ int first_lower(int tj, int64_t off = 0) { return T64::first_lower(tj, off); }
 __host__ __device__ __forceinline__ int masked_tiles(int mask, int TM, int TN, int64_t off) {
-  return (int)mask_prefix(mask, TN, TM, TN, off);
-}
-template <int MASK>
-__device__ __forceinline__ void tile_of(int bid, int TM, int TN, int64_t off, int& ti, int& tj) {
-  if (MASK == kMaskNone) { ti = bid % TM; tj = bid / TM; return; }
-  int lo = 0, hi = TN;   // largest j with prefix(j) <= bid
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (mask_prefix(MASK, mid, TM, TN, off) <= bid) lo = mid; else hi = mid;
-  }
-  tj = lo;
-  const int r = bid - (int)mask_prefix(MASK, lo, TM, TN, off);
-  ti = (MASK == kMaskLower) ? first_lower(lo, off) + r : r;
+  return T64::count(mask, TM, TN, off);
 }
 
 template <bool AK, bool BKC, bool V16, int MASK>
@@ -171,7 +113,7 @@ __device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vec
   const int wm = warp & 1, wn = warp >> 1;
   const int TM = (int)((p.M + BM - 1) / BM), TN = (int)((p.N + BN - 1) / BN);
   int ti, tj;
-  tile_of<MASK>(bid, TM, TN, p.off, ti, tj);
+  T64::tile_of(MASK, bid, TM, TN, p.off, ti, tj);
   const int64_t i0 = (int64_t)ti * BM, j0 = (int64_t)tj * BN;
 
   // K range of this split

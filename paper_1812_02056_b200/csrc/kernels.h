@@ -4,12 +4,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "tiles.cuh"
+
 namespace sf {
 
 // process-wide count of kernel launches enqueued by the library (sf_launch_counter)
 void count_launch(int n = 1);
 
-enum { kMaskNone = 0, kMaskLower = 1, kMaskUpper = 2 };
 
 // C(MxN) = (beta ? Cin : 0) + alpha * op(A)(MxK) * op(B)(KxN)
 //   op(A)(i,k) = a_kcontig ? A[k + i*lda] : A[i + k*lda]
@@ -43,6 +44,24 @@ constexpr int kMaxGroups = 16;
 struct GemmGroups { int count; GemmGroup g[kMaxGroups]; };
 cudaError_t gemm_f64_grouped(GemmF64 p, const GemmGroup* groups, int count, int a_kcontig, int b_kcontig, int mask,
                              cudaStream_t st);
+
+// ---------------------------------------------------------------- fp32: 3xTF32 on tcgen05
+// C(M x N) = Cin - A B^T with A, B given by their 3xTF32 split (x_hi, x_lo) in K-major
+// layout (row i of A: K contiguous floats at Ah + i*ldk_a).  mask / off as for GemmF64.
+// Bases 16-byte aligned, ldk multiples of 4 (TMA).
+struct Tf32Gemm {
+  int64_t M, N, K;
+  const float* Ah; const float* Al; int64_t ldk_a;
+  const float* Bh; const float* Bl; int64_t ldk_b;
+  const float* Cin; int64_t ldcin;
+  float* C; int64_t ldc;
+  int mask; int64_t off;
+  const long long* fail;
+};
+cudaError_t gemm_tf32x3(const Tf32Gemm& g, cudaStream_t st);
+// column-major X (m x k, ld) -> K-major hi/lo split (row i at H + i*ldk)
+cudaError_t split_tf32(int64_t m, int64_t k, const float* X, int64_t ld, float* H, float* L, int64_t ldk,
+                       cudaStream_t st);
 
 // ---------------------------------------------------------------- panels (templated T)
 // Cholesky leaf (Alg. 1 inner loops) on columns [0,w) of the m x w block
