@@ -39,9 +39,12 @@ WORKLOADS = {
     "lu_f64_n4096_s64": ("lu", 4096, 64, "diag_dominant", "f64", "configs[1]"),
     "qr_f64_n8192_s128": ("qr", 8192, 128, "gaussian", "f64", "configs[3]"),
     "chol_f64_n65536_s512": ("chol", 65536, 512, "spd_scaled", "f64", "configs[4]"),
+    "chol_f32_n65536_s512": ("chol", 65536, 512, "spd_scaled", "f32", "configs[4]"),
+    "chol_f32_n16384_s512": ("chol", 16384, 512, "spd_scaled", "f32", "configs[2] in fp32"),
 }
 DEFAULT = "chol_f64_n65536_s512"
 CALIB = os.path.join(ROOT, "calib", "peaks_fp64_tf32.json")
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
 def classical_flops(kind, n):
@@ -151,8 +154,8 @@ def host_inputs(kind, gen, n, seed, K, dev_A=None):
     import numpy as np
     if dev_A is not None:
         if kind == "chol":   # symmetric: device buffer column-major == logical A; first K columns
-            return np.asfortranarray(dev_A[:K, :].cpu().numpy().T), None
-        full = dev_A.cpu().numpy().T.copy()   # buffer -> logical matrix
+            return np.asfortranarray(dev_A[:K, :].double().cpu().numpy().T), None
+        full = dev_A.double().cpu().numpy().T.copy()   # buffer -> logical matrix
         return None, full
     import synth
     A = synth.gen_numpy(gen, n, seed)
@@ -195,7 +198,7 @@ def run_reference(args):
         return 0
     kind, n, s, gen, dtype, cfgname = WORKLOADS[args.workload]
     s = args.s or s
-    K = max(1, sample_cols(kind, n) // 2)
+    K = max(1, oracle_k(kind, n, s, target_flops=2e10))
     dev_A = None
     try:
         import torch
@@ -204,6 +207,8 @@ def run_reference(args):
             dev_A = synth.gen_torch(gen, n, args.seed) if n > 4096 else None
             if dev_A is not None and kind != "chol":
                 dev_A = dev_A.mT.contiguous()
+            if dev_A is not None and dtype == "f32":
+                dev_A = dev_A.float()      # the fp32 workload's input, rounded (P9)
     except Exception:
         dev_A = None
     Acols, Afull = host_inputs(kind, gen, n, args.seed, K, dev_A)
@@ -286,6 +291,9 @@ def main():
     # ---- inputs (synthetic, seeded, same recipe on every rank; A stays pristine: out of place)
     seed = args.seed
     A = make_inputs(torch, sf, synth, kind, gen, n, s, seed, ws, rank, use_dist)
+    if dtype == "f32":      # fp32 path: the fp64-generated matrix rounded to fp32 (P9)
+        A = A.float()
+    dcode = sf.SF_F32 if dtype == "f32" else sf.SF_F64
     ld = n
     info = torch.zeros(1, dtype=torch.int64, device="cuda")
     out1 = torch.zeros_like(A)
@@ -295,13 +303,13 @@ def main():
     def step():
         if use_dist:
             if kind == "chol":
-                sf.chol_dist(comm, n, s, [A], [out1], ld, [info], stream=stream)
+                sf.chol_dist(comm, n, s, [A], [out1], ld, [info], dtype=dcode, stream=stream)
             elif kind == "lu":
                 sf.lu_dist(comm, n, s, [A], [out1], ld, [info], stream=stream)
             else:
                 sf.qr_dist(comm, n, s, [A], [out1], [out2], ld, [info], stream=stream)
         elif kind == "chol":
-            sf.chol_colmajor(n, s, A, n, out1, n, info, stream=stream)
+            sf.chol_colmajor(n, s, A, n, out1, n, info, dtype=dcode, stream=stream)
         elif kind == "lu":
             sf.lu_colmajor(n, s, A, n, out1, n, info, stream=stream)
         else:
@@ -348,7 +356,6 @@ def main():
 
     # ---- roofline of the dominant kernel (the trailing-update GEMM/SYRK launches)
     peaks = json.load(open(CALIB)) if os.path.exists(CALIB) else {}
-    peak = peaks.get("fp64_dmma_tflops")
     upd_ms, upd_n, upd_fl = prof["update"]
     pan_ms, pan_n, _ = prof["panel"]
     qr_ms, qr_n, qr_fl = prof["qr_r"]
@@ -357,16 +364,31 @@ def main():
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):
         traffic = json.load(open(tr_path)).get(args.workload)
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
-                "kernel": "gemm_f64_kernel (flush update, DMMA.8x8x4)" + (", rank 0" if ws > 1 else ""),
-                "peak_source": "measured: calib/peaks_fp64_tf32.json fp64_dmma_tflops (DMMA microbenchmark, "
-                               "this pool's B200); MEASURED_PEAKS.json has no fp64 entry",
-                "launches_per_step": upd_n / args.steps if args.steps else None,
-                "avg_launch_ms": upd_ms / upd_n if upd_n else None,
-                "flops_per_launch": upd_fl / upd_n if upd_n else None,
-                "update_share_of_step": upd_ms / ms if ms else None,
-                "panel_ms_per_step": pan_ms / args.steps, "qr_r_ms_per_step": qr_ms / args.steps}
+    if dtype == "f32":
+        # TF32 dense peak = measured bf16 (sustained: the kernel runs inside a long step) x
+        # the nominal tf32/bf16 ratio 1.1/2.25 (B200_PROFILING.md)
+        mp = json.load(open(MEASURED)) if os.path.exists(MEASURED) else {}
+        bf16 = mp.get("bf16_tflops_sustained") or 1400.0
+        peak = bf16 * 1.1 / 2.25
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
+                    "kernel": "gemm_tf32x3_kernel (flush update, tcgen05.mma kind::tf32, 3xTF32: K' = 3s)",
+                    "flops_counted": "tensor flops executed = 3 x useful (hi.hi + hi.lo + lo.hi)",
+                    "useful_achieved": achieved / 3.0 if achieved else None,
+                    "peak_source": ("measured: MEASURED_PEAKS.json bf16_tflops_sustained x 1.1/2.25 (nominal "
+                                    "tf32/bf16 ratio)" if mp else "fallback 1400 x 1.1/2.25")}
+    else:
+        peak = peaks.get("fp64_dmma_tflops")
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
+                    "kernel": "gemm_f64_kernel (flush update, DMMA.8x8x4)" + (", rank 0" if ws > 1 else ""),
+                    "peak_source": "measured: calib/peaks_fp64_tf32.json fp64_dmma_tflops (DMMA microbenchmark, "
+                                   "this pool's B200); MEASURED_PEAKS.json has no fp64 entry"}
+    roofline.update({"launches_per_step": upd_n / args.steps if args.steps else None,
+                     "avg_launch_ms": upd_ms / upd_n if upd_n else None,
+                     "flops_per_launch": upd_fl / upd_n if upd_n else None,
+                     "update_share_of_step": upd_ms / ms if ms else None,
+                     "panel_ms_per_step": pan_ms / args.steps, "qr_r_ms_per_step": qr_ms / args.steps})
 
     # ---- end to end through the public API with HOST buffers (copies inside the timed region)
     e2e = None
@@ -383,7 +405,7 @@ def main():
                 dA.copy_(hA, non_blocking=True)
                 step_out = (out1, out2)
                 if kind == "chol":
-                    sf.chol_dist(comm, n, s, [dA], [out1], ld, [info], stream=stream)
+                    sf.chol_dist(comm, n, s, [dA], [out1], ld, [info], dtype=dcode, stream=stream)
                 elif kind == "lu":
                     sf.lu_dist(comm, n, s, [dA], [out1], ld, [info], stream=stream)
                 else:
@@ -397,7 +419,7 @@ def main():
         else:
             def hstep():
                 if kind == "chol":
-                    _, inf = sf.chol_host(hA, s, h1)
+                    _, inf = sf.chol_host(hA, s, h1, dtype=dcode)
                 elif kind == "lu":
                     _, inf = sf.lu_host(hA, s, h1)
                 else:
@@ -442,7 +464,9 @@ def main():
                            "generator": gen, "seed": args.seed, "parallelism": par,
                            "l2": f"inputs larger than L2 ({A.numel() * A.element_size() / 1e9:.2f} GB per rank "
                                  "> 126 MB); out-of-place factorization, A re-read from HBM every step"},
-                "pct_fp64_peak": (value / ws / 1e3 / peak) if peak else None,
+                "pct_tensor_peak": (value / ws / 1e3 / peak) if peak else None,
+                "pct_peak_kind": ("classical useful GFLOP/s per GPU / TF32 dense peak" if dtype == "f32"
+                                  else "classical GFLOP/s per GPU / FP64 tensor (DMMA) peak"),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(l1 - l0), "clocks": ck}
         print(json.dumps(line), flush=True)

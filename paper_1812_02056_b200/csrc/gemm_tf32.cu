@@ -12,15 +12,17 @@
 // x_lo have zero low mantissa bits, so the hardware's TF32 operand truncation is exact and
 // the products accumulate in fp32 in TMEM.
 //
-// Kernel (persistent, one CTA per SM, 6 warps):
-//   warp 0     TMA producer (one lane): per k-block a 128 x 32 A tile and a 256 x 32 B tile
-//              (128-byte rows, 128B swizzle) into a 4-stage ring, mbarrier complete_tx
-//   warp 1     MMA issuer (one lane): 4 x tcgen05.mma 128x256x8 per k-block into one of two
-//              TMEM accumulators (2 x 256 of the 512 columns), tcgen05.commit releases the
-//              smem stage / publishes the accumulator
+// Kernel (one 128 x BN tile per CTA, BN = 256 for the flush, 64/128 for the narrow in-panel
+// corrections; two CTAs per SM, 6 warps):
+//   warp 0     TMA producer (one lane): per BK = 16 slice the four operand tiles A_hi, A_lo
+//              (128 x 16), B_hi, B_lo (BN x 16) — 64-byte rows, 64B swizzle — into a ring of
+//              96 KB, mbarrier complete_tx; lanes 1-31 first warm L2 with the C tile
+//   warp 1     MMA issuer (one lane): per 8-wide k-step hi.hi, hi.lo, lo.hi tcgen05.mma
+//              (M = 128, N = BN) into one TMEM accumulator; tcgen05.commit frees the stage
 //   warps 2-5  epilogue: tcgen05.ld 32 lanes x 32 columns at a time, C = Cin - acc, masked
-//              store (column-major C: a warp's 32 rows of one column are one 128-byte line);
-//              the next tile's MMAs run meanwhile in the other accumulator
+//              store (column-major C: a warp's 32 rows of one column are one 128-byte line)
+// Non-persistent on purpose: the lookahead stream's panel kernels get SMs between CTAs, and
+// the second CTA on the SM overlaps this one's epilogue (DESIGN.md §5 K5).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <math.h>
@@ -31,16 +33,18 @@
 namespace sf {
 
 namespace t32 {
-constexpr int BM = 128, BN = 256, BK = 32;      // BK fp32 = 128 bytes = one swizzle row
-constexpr int STAGES = 4;
-constexpr int UMMA_K = 8;                       // kind::tf32: K = 8 per instruction (32 bytes)
-constexpr int A_BYTES = BM * BK * 4;            // 16 KB
-constexpr int B_BYTES = BN * BK * 4;            // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int BM = 128, BK = 16;                 // BK fp32 = 64 bytes = one 64B-swizzle row
+constexpr int UMMA_K = 8;                        // kind::tf32: K = 8 per instruction (32 bytes)
 constexpr int THREADS = 192;
-constexpr int TMEM_COLS = 512;
-constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-using TT = Tiles<BM, BN>;
+template <int BN> struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 4;                 // one of A_hi / A_lo: 8 KB
+  static constexpr int B_BYTES = BN * BK * 4;                 // one of B_hi / B_lo
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES = (96 * 1024) / STAGE_BYTES;    // 96 KB of stages: two CTAs per SM
+  static constexpr int TMEM_COLS = BN;                        // one fp32 accumulator
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  using TT = Tiles<BM, BN>;
+};
 }  // namespace t32
 
 // ------------------------------------------------------------------ PTX helpers
@@ -79,14 +83,14 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
-// K-major, 128B-swizzled operand tile: rows of 128 bytes, 8-row atoms 1024 bytes apart.
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+// K-major, 64B-swizzled operand tile: rows of 64 bytes (16 fp32), 8-row atoms 512 bytes apart.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
-  d |= (uint64_t)1 << 16;                           // leading byte offset (unused for SW128 K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;                 // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 16;                           // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;                  // stride byte offset: 8 rows x 64 B
   d |= (uint64_t)1 << 46;                           // descriptor version (tcgen05)
-  d |= (uint64_t)2 << 61;                           // layout: SWIZZLE_128B
+  d |= (uint64_t)4 << 61;                           // layout: SWIZZLE_64B
   return d;
 }
 // Instruction descriptor, kind::tf32: D fp32, A/B tf32, both K-major, M = 128, N = BN.
@@ -129,40 +133,59 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 // ------------------------------------------------------------------ the kernel
 struct Tf32Params {
   int64_t M, N, K;          // C is M x N, products over K (the split operands have K columns)
-  int64_t a_row0, b_row0;   // first row of A / B in their tensor maps
   const float* Cin; int64_t ldcin;
   float* C; int64_t ldc;
   int64_t off;              // mask diagonal offset
   int mask;
-  int ntiles;
   const long long* fail;
 };
 
-__global__ void __launch_bounds__(t32::THREADS, 1)
+// One 128 x BN tile per CTA, two CTAs per SM (96 KB of stages each): one CTA's epilogue
+// overlaps the other's MMAs, and between CTAs the lookahead stream's panel kernels get SMs.
+// Each stage holds one BK = 16 slice of all four operands (A_hi, A_lo, B_hi, B_lo), so the
+// three products of a slice are issued back to back and every operand byte fetched from L2
+// feeds 1.5 MMAs on average (3 products from 4 tiles).
+template <int BN>
+__global__ void __launch_bounds__(t32::THREADS, 2)
 gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                    const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, Tf32Params p) {
   using namespace t32;
+  using C_ = Cfg<BN>;
+  constexpr int STAGES = C_::STAGES, A_BYTES = C_::A_BYTES, B_BYTES = C_::B_BYTES;
   if (p.fail && failed(p.fail)) return;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);   // SW128 atoms: 1 KB aligned
-  uint8_t* sA = smem;                                   // [STAGES][A_BYTES]
-  uint8_t* sB = smem + STAGES * A_BYTES;                // [STAGES][B_BYTES]
-  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);   // swizzle atoms aligned
+  uint64_t* full = (uint64_t*)(smem + STAGES * C_::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;                     // [2]
-  uint64_t* tempty = tfull + 2;                         // [2]
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* tfull = empty + STAGES;
+  uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
+  auto sAh = [&](int s) { return smem + s * C_::STAGE_BYTES; };
+  auto sAl = [&](int s) { return smem + s * C_::STAGE_BYTES + A_BYTES; };
+  auto sBh = [&](int s) { return smem + s * C_::STAGE_BYTES + 2 * A_BYTES; };
+  auto sBl = [&](int s) { return smem + s * C_::STAGE_BYTES + 2 * A_BYTES + B_BYTES; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int TM = (int)((p.M + BM - 1) / BM), TN = (int)((p.N + BN - 1) / BN);
+  int ti, tj;
+  C_::TT::tile_of(p.mask, blockIdx.x, TM, TN, p.off, ti, tj);
+  const int64_t i0 = (int64_t)ti * BM, j0 = (int64_t)tj * BN;
+  const int nkb = (int)((p.K + BK - 1) / BK);
+
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    mbar_init(tfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     tma_prefetch_desc(&mAh); tma_prefetch_desc(&mAl); tma_prefetch_desc(&mBh); tma_prefetch_desc(&mBl);
+  } else if (warp == 0) {
+    // warm L2 with this tile's C columns for the epilogue's read-modify-write
+    for (int u = lane - 1; u < BN * 4; u += 31) {
+      const int64_t j = j0 + (u >> 2), i = i0 + (u & 3) * 32;
+      if (j < p.N && i < p.M) prefetch_l2(p.Cin + i + j * p.ldcin);
+    }
   }
-  if (warp == 0) {
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
+                 "r"(C_::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   tc_fence_before();
@@ -170,100 +193,73 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constan
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int TM = (int)((p.M + BM - 1) / BM), TN = (int)((p.N + BN - 1) / BN);
-  const int nkb = (int)((p.K + BK - 1) / BK);          // k-blocks per product
-  const int nkb3 = 3 * nkb;
-
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer
-      int stage = 0; uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        int ti, tj;
-        TT::tile_of(p.mask, t, TM, TN, p.off, ti, tj);
-        const int ya = (int)(p.a_row0 + (int64_t)ti * BM), yb = (int)(p.b_row0 + (int64_t)tj * BN);
-        for (int kb = 0; kb < nkb3; ++kb) {
-          const int prod = kb / nkb, kx = (kb - prod * nkb) * BK;
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
-          // products: hi*hi, hi*lo, lo*hi
-          tma_load_2d(sA + stage * A_BYTES, prod < 2 ? &mAh : &mAl, &full[stage], kx, ya);
-          tma_load_2d(sB + stage * B_BYTES, prod == 1 ? &mBl : &mBh, &full[stage], kx, yb);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
+      // ---------------- TMA producer: one BK slice of A_hi, A_lo, B_hi, B_lo per stage
+      const int ya = (int)i0, yb = (int)j0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+        mbar_expect_tx(&full[s], C_::STAGE_BYTES);
+        tma_load_2d(sAh(s), &mAh, &full[s], kb * BK, ya);
+        tma_load_2d(sAl(s), &mAl, &full[s], kb * BK, ya);
+        tma_load_2d(sBh(s), &mBh, &full[s], kb * BK, yb);
+        tma_load_2d(sBl(s), &mBl, &full[s], kb * BK, yb);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer
+      // ---------------- MMA issuer: per k-step hi.hi, hi.lo, lo.hi into one accumulator
       constexpr uint32_t idesc = idesc_tf32(BM, BN);
-      int stage = 0; uint32_t phase = 0;
-      int local = 0;
-      for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++local) {
-        const int acc = local & 1;
-        const uint32_t use = (uint32_t)(local >> 1) & 1;
-        mbar_wait(&tempty[acc], use ^ 1);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&full[s], (kb / STAGES) & 1);
         tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < nkb3; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * A_BYTES), b0 = smem_u32(sB + stage * B_BYTES);
+        const uint32_t ah = smem_u32(sAh(s)), al = smem_u32(sAl(s)), bh = smem_u32(sBh(s)), bl = smem_u32(sBl(s));
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            // advance along K inside the 128-byte swizzle row: 32 bytes per instruction
-            umma_tf32(d, umma_desc_sw128(a0 + k * UMMA_K * 4), umma_desc_sw128(b0 + k * UMMA_K * 4), idesc,
-                      (kb | k) != 0);
-          }
-          umma_commit(&empty[stage]);          // frees the smem stage when these MMAs retire
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        for (int k = 0; k < BK / UMMA_K; ++k) {
+          const uint32_t o = k * UMMA_K * 4;   // 32 bytes along K inside the swizzled row
+          umma_tf32(tmem, umma_desc_sw64(ah + o), umma_desc_sw64(bh + o), idesc, (kb | k) != 0);
+          umma_tf32(tmem, umma_desc_sw64(ah + o), umma_desc_sw64(bl + o), idesc, 1);
+          umma_tf32(tmem, umma_desc_sw64(al + o), umma_desc_sw64(bh + o), idesc, 1);
         }
-        umma_commit(&tfull[acc]);              // accumulator complete
+        umma_commit(&empty[s]);                // frees the stage when these MMAs retire
       }
+      umma_commit(tfull);                      // accumulator complete
     }
   } else {
     // ---------------- epilogue: warps 2..5 -> TMEM lanes 32*(warp%4) .. +31
     const int q = warp & 3;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    int local = 0;
-    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++local) {
-      int ti, tj;
-      TT::tile_of(p.mask, t, TM, TN, p.off, ti, tj);
-      const int acc = local & 1;
-      const uint32_t use = (uint32_t)(local >> 1) & 1;
-      mbar_wait(&tfull[acc], use);
-      tc_fence_after();
-      const int64_t i = (int64_t)ti * BM + q * 32 + lane;
-      const int64_t j0 = (int64_t)tj * BN;
-      for (int c = 0; c < BN; c += 32) {
-        if (j0 + c >= p.N) break;
-        float v[32];
-        tmem_ld32(tmem + lane_base + (uint32_t)(acc * BN + c), v);
-        if (i < p.M) {
-          float cin[32];
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const int64_t i = i0 + q * 32 + lane;
+    for (int c = 0; c < BN; c += 32) {
+      if (j0 + c >= p.N) break;
+      float v[32];
+      tmem_ld32(tmem + lane_base + (uint32_t)c, v);
+      if (i < p.M) {
+        float cin[32];
 #pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            const int64_t j = j0 + c + u;
-            const bool in = j < p.N && (p.mask == kMaskNone || (p.mask == kMaskLower ? i >= j + p.off : i <= j + p.off));
-            cin[u] = in ? __ldcg(p.Cin + i + j * p.ldcin) : 0.f;
-          }
+        for (int u = 0; u < 32; ++u) {
+          const int64_t j = j0 + c + u;
+          const bool in = j < p.N && (p.mask == kMaskNone || (p.mask == kMaskLower ? i >= j + p.off : i <= j + p.off));
+          cin[u] = in ? __ldcg(p.Cin + i + j * p.ldcin) : 0.f;
+        }
 #pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            const int64_t j = j0 + c + u;
-            const bool in = j < p.N && (p.mask == kMaskNone || (p.mask == kMaskLower ? i >= j + p.off : i <= j + p.off));
-            if (in) __stcg(p.C + i + j * p.ldc, cin[u] - v[u]);
-          }
+        for (int u = 0; u < 32; ++u) {
+          const int64_t j = j0 + c + u;
+          const bool in = j < p.N && (p.mask == kMaskNone || (p.mask == kMaskLower ? i >= j + p.off : i <= j + p.off));
+          if (in) __stcg(p.C + i + j * p.ldc, cin[u] - v[u]);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
+    tc_fence_before();
   }
   __syncthreads();
-  if (warp == 0) {
+  if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(C_::TMEM_COLS));
   }
 }
 
@@ -320,7 +316,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D map over a K-major fp32 operand: `rows` rows of `k` valid columns, row stride ldk;
-// box = BK columns x box_rows rows, 128-byte swizzle; out-of-range elements read as zero.
+// box = BK columns x box_rows rows, 64-byte swizzle; out-of-range elements read as zero.
 static cudaError_t make_map(CUtensorMap* map, const float* base, int64_t k, int64_t rows, int64_t ldk, int box_rows) {
   auto fn = encode_fn();
   if (!fn) return cudaErrorNotSupported;
@@ -329,42 +325,47 @@ static cudaError_t make_map(CUtensorMap* map, const float* base, int64_t k, int6
   cuuint32_t box[2] = {(cuuint32_t)t32::BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-cudaError_t gemm_tf32x3(const Tf32Gemm& g, cudaStream_t st) {
+template <int BN>
+static cudaError_t launch_bn(const Tf32Gemm& g, cudaStream_t st) {
   using namespace t32;
-  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaSuccess;
-  if ((g.ldk_a % 4) || (g.ldk_b % 4) || ((uintptr_t)g.Ah % 16) || ((uintptr_t)g.Al % 16) || ((uintptr_t)g.Bh % 16) ||
-      ((uintptr_t)g.Bl % 16))
-    return cudaErrorInvalidValue;   // TMA: 16-byte aligned bases and row strides
+  using C_ = Cfg<BN>;
   const int TM = (int)((g.M + BM - 1) / BM), TN = (int)((g.N + BN - 1) / BN);
-  const int ntiles = TT::count(g.mask, TM, TN, g.off);
+  const int ntiles = C_::TT::count(g.mask, TM, TN, g.off);
   if (ntiles == 0) return cudaSuccess;
   CUtensorMap mAh, mAl, mBh, mBl;
   cudaError_t e;
-  // the maps start at the operands' first rows; TMA rows beyond M / N read zeros
+  // the maps start at the operands' first rows; TMA rows beyond M / N and columns beyond K
+  // read zeros
   if ((e = make_map(&mAh, g.Ah, g.K, g.M, g.ldk_a, BM)) != cudaSuccess) return e;
   if ((e = make_map(&mAl, g.Al, g.K, g.M, g.ldk_a, BM)) != cudaSuccess) return e;
   if ((e = make_map(&mBh, g.Bh, g.K, g.N, g.ldk_b, BN)) != cudaSuccess) return e;
   if ((e = make_map(&mBl, g.Bl, g.K, g.N, g.ldk_b, BN)) != cudaSuccess) return e;
-  static int sms = 0;
   static bool attr = false;
   if (!attr) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    e = cudaFuncSetAttribute(gemm_tf32x3_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  Tf32Params p{g.M, g.N, g.K, 0, 0, g.Cin, g.ldcin, g.C, g.ldc, g.off, g.mask, ntiles, g.fail};
-  const int grid = ntiles < sms ? ntiles : sms;
-  gemm_tf32x3_kernel<<<grid, THREADS, SMEM, st>>>(mAh, mAl, mBh, mBl, p);
+  Tf32Params p{g.M, g.N, g.K, g.Cin, g.ldcin, g.C, g.ldc, g.off, g.mask, g.fail};
+  gemm_tf32x3_kernel<BN><<<ntiles, THREADS, C_::SMEM, st>>>(mAh, mAl, mBh, mBl, p);
   count_launch();
   return cudaGetLastError();
+}
+
+cudaError_t gemm_tf32x3(const Tf32Gemm& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaSuccess;
+  if ((g.ldk_a % 4) || (g.ldk_b % 4) || ((uintptr_t)g.Ah % 16) || ((uintptr_t)g.Al % 16) || ((uintptr_t)g.Bh % 16) ||
+      ((uintptr_t)g.Bl % 16))
+    return cudaErrorInvalidValue;   // TMA: 16-byte aligned bases and row strides
+  // narrow updates (the panel recursion's corrections) take a narrower tile
+  if (g.N <= 64) return launch_bn<64>(g, st);
+  if (g.N <= 128) return launch_bn<128>(g, st);
+  return launch_bn<256>(g, st);
 }
 
 }  // namespace sf
