@@ -31,6 +31,7 @@
 
 #include <cstring>
 #include <map>
+#include <type_traits>
 
 #include "common.cuh"
 #include "drv.cuh"
@@ -115,6 +116,7 @@ struct Rank {
   T* qfull = nullptr;               // QR: every panel of Q, n x n, ld n
   T* mgsw = nullptr; T* cw = nullptr; T* split = nullptr; T* cw2 = nullptr; T* split2 = nullptr;
   int64_t split_elems = 0;
+  SplitBuf sb_upd{}, sb_pan{};      // fp32 Cholesky: 3xTF32 split of the received / own panel
   Events recv, ready, done, la;
 };
 
@@ -307,12 +309,11 @@ static int join_rank(Rank<T>& x) {
 // Flush of panel p into rank x's local panels in slots [j_begin, j_end): for each, rows
 // [qs, n) of its columns -= Lp[qs-ps : n-ps] Lp[qs-ps : qs-ps+wq]^T, lower part;
 // one grouped launch.  Adds the algorithmic flops to *flops.
-template <typename T>
-static cudaError_t chol_update_slots(const Cyclic& cy, Rank<T>& x, int64_t p, int64_t j_begin, int64_t j_end,
-                                     const T* Lp, int64_t ldp, int64_t ld, double* flops, cudaStream_t st) {
+static cudaError_t chol_update_slots(const Cyclic& cy, Rank<double>& x, int64_t p, int64_t j_begin, int64_t j_end,
+                                     const double* Lp, int64_t ldp, int64_t ld, double* flops, cudaStream_t st) {
   std::vector<GemmGroup> gs;
   const int64_t ps = p * cy.s, wp = cy.width(p);
-  const T* src = (p == 0) ? x.A : x.X;   // out of place: the first flush reads A
+  const double* src = (p == 0) ? x.A : x.X;   // out of place: the first flush reads A
   for (int64_t j = j_begin; j < j_end; ++j) {
     const int64_t q = cy.panel_of(j, x.r), qs = q * cy.s, wq = cy.width(q);
     GemmGroup g{};
@@ -325,6 +326,39 @@ static cudaError_t chol_update_slots(const Cyclic& cy, Rank<T>& x, int64_t p, in
   if (gs.empty()) return cudaSuccess;
   GemmF64 p64{0, 0, wp, nullptr, ldp, nullptr, ldp, nullptr, ld, nullptr, ld, -1.0, 1, 1, nullptr, x.fail};
   return gemm_f64_grouped(p64, gs.data(), (int)gs.size(), 0, 0, kMaskLower, st);
+}
+
+// fp32: the received panel's rows [c, n) were split once into x.sb_upd (chol_split_panel);
+// one 3xTF32 tcgen05 launch per local panel.
+static cudaError_t chol_update_slots(const Cyclic& cy, Rank<float>& x, int64_t p, int64_t j_begin, int64_t j_end,
+                                     const float*, int64_t, int64_t ld, double* flops, cudaStream_t st) {
+  const int64_t c = p * cy.s + cy.width(p), wp = cy.width(p);
+  const float* src = (p == 0) ? x.A : x.X;
+  for (int64_t j = j_begin; j < j_end; ++j) {
+    const int64_t q = cy.panel_of(j, x.r), qs = q * cy.s, wq = cy.width(q), M = cy.n - qs;
+    const SplitBuf R = x.sb_upd.at(qs - c, 0);
+    cudaError_t e = syrk_tf32(M, wq, wp, R, R, src + qs + j * cy.s * ld, ld, x.X + qs + j * cy.s * ld, ld, x.fail, st);
+    if (e != cudaSuccess) return e;
+    *flops += 3.0 * 2.0 * wp * ((double)wq * (double)M - 0.5 * (double)wq * (double)(wq - 1));
+  }
+  return cudaSuccess;
+}
+static cudaError_t chol_split_panel(const Cyclic&, Rank<double>&, int64_t, const double*, int64_t, cudaStream_t) {
+  return cudaSuccess;
+}
+static cudaError_t chol_split_panel(const Cyclic& cy, Rank<float>& x, int64_t p, const float* Lp, int64_t ld,
+                                    cudaStream_t st) {
+  const int64_t wp = cy.width(p), c = p * cy.s + wp;
+  if (c >= cy.n) return cudaSuccess;
+  return split_tf32(cy.n - c, wp, Lp + wp, ld, x.sb_upd.h, x.sb_upd.l, x.sb_upd.ldk, st);
+}
+static cudaError_t chol_panel_any(Rank<double>& x, int64_t m, int64_t w, const double* src, int64_t lds, double* dst,
+                                  int64_t ldd, int64_t col0, cudaStream_t st) {
+  return chol_panel_rec<double>(m, w, src, lds, dst, ldd, col0, x.fail, st);
+}
+static cudaError_t chol_panel_any(Rank<float>& x, int64_t m, int64_t w, const float* src, int64_t lds, float* dst,
+                                  int64_t ldd, int64_t col0, cudaStream_t st) {
+  return chol_panel_rec_f32(m, w, src, lds, dst, ldd, col0, x.sb_pan, x.fail, st);
 }
 
 // Panel p as broadcast: the contiguous span of the owner's local storage from (ps, first
@@ -344,14 +378,24 @@ static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, 
                          int64_t* const* d_info, cudaStream_t caller) {
   const Cyclic cy(n, s, comm->nranks);
   std::vector<Rank<T>> rk;
-  int rc = setup_ranks<T>(comm, rk, cy, dA, dL, nullptr, d_info, (size_t)s * ld, 0, 0, caller);
+  const int64_t ldk = (s + 3) / 4 * 4;
+  const size_t split_elems = std::is_same<T, float>::value ? 4 * (size_t)n * ldk + 1024 : 0;
+  int rc = setup_ranks<T>(comm, rk, cy, dA, dL, nullptr, d_info, (size_t)s * ld, 0, split_elems, caller);
   if (rc) return rc;
+  if (std::is_same<T, float>::value) {
+    for (auto& x : rk) {
+      x.sb_upd = SplitBuf{(float*)x.ws.template take<T>((size_t)n * ldk), nullptr, ldk};
+      x.sb_upd.l = (float*)x.ws.template take<T>((size_t)n * ldk);
+      x.sb_pan = SplitBuf{(float*)x.ws.template take<T>((size_t)n * ldk), nullptr, ldk};
+      x.sb_pan.l = (float*)x.ws.template take<T>((size_t)n * ldk);
+    }
+  }
   const Span<T> sp{cy, ld};
   // prologue: panel 0 on its owner, out of place from A
   for (auto& o : rk) {
     if (o.r != 0) continue;
     ProfScope ps(1, 0.0, o.st.pan);
-    SF_CUDA(chol_panel_rec<T>(n, cy.width(0), o.A, ld, o.X, ld, 0, o.fail, o.st.pan));
+    SF_CUDA(chol_panel_any(o, n, cy.width(0), o.A, ld, o.X, ld, 0, o.st.pan));
     SF_CUDA(cudaEventRecord(o.ready[0], o.st.pan));
   }
   for (int64_t p = 0; p < cy.P; ++p) {
@@ -363,6 +407,7 @@ static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, 
       SF_CUDA(wait_on(x.st.mn, x.recv[p]));
       const T* Lp = sp.at(x, p);
       const int64_t nslots = (cy.local_cols(x.r) + s - 1) / s;
+      SF_CUDA(chol_split_panel(cy, x, p, Lp, ld, x.st.mn));
       int64_t j0 = cy.first_slot_after(p, x.r);
       if (cy.owner(p + 1) == x.r) {
         // lookahead: flush into panel p+1 first, factor it while the rest of the flush runs
@@ -370,7 +415,7 @@ static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, 
         {
           double fl = 0.0;
           ProfScope pf(0, 0.0, x.st.mn);
-          SF_CUDA(chol_update_slots<T>(cy, x, p, j, j + 1, Lp, ld, ld, &fl, x.st.mn));
+          SF_CUDA(chol_update_slots(cy, x, p, j, j + 1, Lp, ld, ld, &fl, x.st.mn));
           pf.r.flops = fl;
         }
         j0 = j + 1;
@@ -379,14 +424,14 @@ static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, 
         {
           ProfScope pp(1, 0.0, x.st.pan);
           T* P0 = x.X + qs + j * s * ld;
-          SF_CUDA(chol_panel_rec<T>(n - qs, wq, P0, ld, P0, ld, qs, x.fail, x.st.pan));
+          SF_CUDA(chol_panel_any(x, n - qs, wq, P0, ld, P0, ld, qs, x.st.pan));
         }
         SF_CUDA(cudaEventRecord(x.ready[q], x.st.pan));
       }
       {
         double fl = 0.0;
         ProfScope pf(0, 0.0, x.st.mn);
-        SF_CUDA(chol_update_slots<T>(cy, x, p, j0, nslots, Lp, ld, ld, &fl, x.st.mn));
+        SF_CUDA(chol_update_slots(cy, x, p, j0, nslots, Lp, ld, ld, &fl, x.st.mn));
         pf.r.flops = fl;
       }
       SF_CUDA(cudaEventRecord(x.done[p], x.st.mn));
@@ -671,7 +716,7 @@ int chol_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* cons
                      int64_t ld_local, int64_t* const* d_info, void* stream) {
   int rc = check_dist(comm, n, s, dtype, dA_local, dL_local, ld_local, d_info);
   if (rc) return rc;
-  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp32 distributed Cholesky not built yet");
+  if (dtype == SF_F32) return chol_dist_run<float>(comm, n, s, dA_local, dL_local, ld_local, d_info, (cudaStream_t)stream);
   return chol_dist_run<double>(comm, n, s, dA_local, dL_local, ld_local, d_info, (cudaStream_t)stream);
 }
 

@@ -23,9 +23,11 @@ import paper_1812_02056_b200 as sf  # noqa: E402
 from tests.test_parity_gpu import EPS, TOL64, check_qr, dev, host, run_chol  # noqa: E402
 
 
-def run_dist(kind, A, s, G, comm=None, inplace=False):
+def run_dist(kind, A, s, G, comm=None, inplace=False, dtype=None):
     n = A.shape[0]
     B = dev(A)                                   # column-major buffer
+    if dtype == sf.SF_F32:
+        B = B.float()
     own = comm is None
     comm = comm or sf.Comm.loopback(G)
     try:
@@ -43,7 +45,8 @@ def run_dist(kind, A, s, G, comm=None, inplace=False):
             outs = (Q, R)
         else:
             X = Aloc if inplace else [torch.full_like(a, 7.0) for a in Aloc]
-            (sf.chol_dist if kind == "chol" else sf.lu_dist)(comm, n, s, Aloc, X, n, info)
+            (sf.chol_dist if kind == "chol" else sf.lu_dist)(comm, n, s, Aloc, X, n, info,
+                                                             dtype=sf.SF_F64 if dtype is None else dtype)
             torch.cuda.synchronize()
             if not inplace:
                 for a, b in zip(Aloc, Aref):
@@ -55,7 +58,7 @@ def run_dist(kind, A, s, G, comm=None, inplace=False):
         for X in outs:
             Y = torch.zeros_like(B)
             sf.gather_cyclic(X, n, s, G, Y)
-            full.append(host(Y))
+            full.append(host(Y.double()))
         return full, infos[0]
     finally:
         if own:
@@ -167,3 +170,30 @@ def test_chol_dist_cfg5_shape_sampled():
     assert np.array_equal(np.tril(Lg), np.tril(L1))
     Lo, io = oracle.chol(np.asfortranarray(An[:, :K]), s, kcols=K)
     assert io == 0 and synth.r2_error(np.tril(Lg)[:, :K], Lo[:, :K]) <= TOL64
+
+
+@pytest.mark.parametrize("n,s,G", [(64, 16, 2), (300, 64, 4), (1000, 168, 3), (2048, 512, 2), (4096, 512, 8)])
+def test_chol_dist_fp32_loopback(n, s, G):
+    """fp32 (3xTF32) distributed Cholesky: against the fp64 oracle on the fp32-rounded input
+    (reading P9, R2 <= 2e-4) and equal to the single-GPU fp32 factor."""
+    A = synth.gen_numpy("spd_scaled", n, seed=n + G).astype(np.float32).astype(np.float64)
+    (Lg,), info = run_dist("chol", A, s, G, dtype=sf.SF_F32)
+    assert info == 0
+    Lo, io = oracle.chol(A, s)
+    Lg = np.tril(Lg)
+    assert synth.r2_error(Lg, Lo) <= 2e-4
+    assert synth.rel_residual(A, Lg, Lg.T) <= 1e-5 * n
+    B32 = torch.from_numpy(np.ascontiguousarray(A.T)).float().cuda()
+    L1 = torch.full_like(B32, 7.0)
+    info1 = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sf.chol_colmajor(n, s, B32, n, L1, n, info1, dtype=sf.SF_F32)
+    torch.cuda.synchronize()
+    L1 = np.tril(L1.double().cpu().numpy().T)
+    assert np.array_equal(Lg, L1)
+
+
+def test_chol_dist_fp32_planted():
+    n, s = 1024, 128
+    Lx = synth.planted_chol(n, seed=5)
+    (Lg,), info = run_dist("chol", Lx @ Lx.T, s, 3, dtype=sf.SF_F32)
+    assert info == 0 and np.array_equal(np.tril(Lg), Lx)
