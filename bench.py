@@ -182,6 +182,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--dist", action="store_true", help="use the distributed (block-cyclic) driver even at N=1")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--loopback", type=int, default=0,
+                    help="test mode: run the distributed driver with G ranks emulated on this one GPU")
     return ap.parse_args()
 
 
@@ -277,37 +279,48 @@ def main():
     kind, n, s, gen, dtype, cfgname = WORKLOADS[args.workload]
     s = args.s or s
     assert args.warmup >= 3 or os.environ.get("SF_BENCH_ALLOW_SHORT"), "timing rules need >= 3 warm-up steps"
-    use_dist = ws > 1 or args.dist
+    use_dist = ws > 1 or args.dist or args.loopback > 0
     stream = torch.cuda.current_stream()
 
-    # ---- communicator (multi-GPU: block-cyclic panels, NCCL broadcast)
+    # ---- communicator (multi-GPU: block-cyclic panels, NCCL broadcast).
+    # --loopback G (test mode): one process drives G emulated ranks on this GPU.
     comm = None
-    if use_dist:
+    G = ws
+    if args.loopback > 0:
+        assert ws == 1, "--loopback is a single-process test mode"
+        G = args.loopback
+        comm = sf.Comm.loopback(G)
+    elif use_dist:
         uid = [sf.unique_id() if rank == 0 else None]
         if ws > 1:
             dist.broadcast_object_list(uid, src=0)
         comm = sf.Comm.nccl(ws, rank, uid[0])
+    my_ranks = comm.local_ranks if comm is not None else [rank]
 
     # ---- inputs (synthetic, seeded, same recipe on every rank; A stays pristine: out of place)
     seed = args.seed
-    A = make_inputs(torch, sf, synth, kind, gen, n, s, seed, ws, rank, use_dist)
+    As = [make_inputs(torch, sf, synth, kind, gen, n, s, seed, G, r, use_dist) for r in my_ranks]
     if dtype == "f32":      # fp32 path: the fp64-generated matrix rounded to fp32 (P9)
-        A = A.float()
+        As = [a.float() for a in As]
+    A = As[0]
     dcode = sf.SF_F32 if dtype == "f32" else sf.SF_F64
     ld = n
-    info = torch.zeros(1, dtype=torch.int64, device="cuda")
-    out1 = torch.zeros_like(A)
-    out2 = torch.zeros_like(A) if kind == "qr" else None
+    infos = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in my_ranks]
+    info = infos[0]
+    outs1 = [torch.zeros_like(a) for a in As]
+    outs2 = [torch.zeros_like(a) for a in As] if kind == "qr" else None
+    out1 = outs1[0]
+    out2 = outs2[0] if outs2 else None
     torch.cuda.synchronize()
 
     def step():
         if use_dist:
             if kind == "chol":
-                sf.chol_dist(comm, n, s, [A], [out1], ld, [info], dtype=dcode, stream=stream)
+                sf.chol_dist(comm, n, s, As, outs1, ld, infos, dtype=dcode, stream=stream)
             elif kind == "lu":
-                sf.lu_dist(comm, n, s, [A], [out1], ld, [info], stream=stream)
+                sf.lu_dist(comm, n, s, As, outs1, ld, infos, stream=stream)
             else:
-                sf.qr_dist(comm, n, s, [A], [out1], [out2], ld, [info], stream=stream)
+                sf.qr_dist(comm, n, s, As, outs1, outs2, ld, infos, stream=stream)
         elif kind == "chol":
             sf.chol_colmajor(n, s, A, n, out1, n, info, dtype=dcode, stream=stream)
         elif kind == "lu":
@@ -392,7 +405,7 @@ def main():
 
     # ---- end to end through the public API with HOST buffers (copies inside the timed region)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.loopback:
         ke = max(1, min(args.steps, args.e2e_steps))
         nbytes = A.numel() * A.element_size()
         hA = A.cpu().pin_memory()
@@ -456,6 +469,9 @@ def main():
 
     if rank == 0:
         par = f"block-cyclic s-column panels over {ws} GPU(s), NCCL panel broadcast" if use_dist else "single GPU"
+        if args.loopback:
+            par = (f"LOOPBACK TEST MODE: {G} ranks of the block-cyclic schedule emulated on 1 GPU "
+                   "(device-copy broadcast; not a scaling measurement)")
         line = {"metric": "factorization GFLOP/s (classical count) and % of FP64 tensor peak",
                 "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "strong",

@@ -97,6 +97,8 @@ __device__ __forceinline__ double frag(const double* Xs, int base, int kk, int l
 }
 
 using T64 = Tiles<g64::BM, g64::BN>;
+// rasterization: tile columns in groups of 32 (2048 C columns); see Tiles::tile_of_grouped
+constexpr int kGroupCols = 32;
 __host__ __device__ __forceinline__ int first_lower(int tj, int64_t off = 0) { return T64::first_lower(tj, off); }
 __host__ __device__ __forceinline__ int masked_tiles(int mask, int TM, int TN, int64_t off) {
   return T64::count(mask, TM, TN, off);
@@ -113,7 +115,8 @@ __device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vec
   const int wm = warp & 1, wn = warp >> 1;
   const int TM = (int)((p.M + BM - 1) / BM), TN = (int)((p.N + BN - 1) / BN);
   int ti, tj;
-  T64::tile_of(MASK, bid, TM, TN, p.off, ti, tj);
+  if (p.rs.ngroups > 0) T64::tile_of_raster(MASK, bid, TM, p.off, p.rs, ti, tj);
+  else T64::tile_of(MASK, bid, TM, TN, p.off, ti, tj);
   const int64_t i0 = (int64_t)ti * BM, j0 = (int64_t)tj * BN;
 
   // K range of this split
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(g64::THREADS, 2) gemm_f64_grouped_kernel(GemmF
   if (p.fail && failed(p.fail)) return;
   int g = 0;
   while (g + 1 < gs.count && (int)blockIdx.x >= gs.g[g + 1].tile0) ++g;
-  p.M = gs.g[g].M; p.N = gs.g[g].N; p.off = gs.g[g].off;
+  p.M = gs.g[g].M; p.N = gs.g[g].N; p.off = gs.g[g].off; p.rs.ngroups = 0;
   p.A = gs.g[g].A; p.B = gs.g[g].B; p.Cin = gs.g[g].Cin; p.C = gs.g[g].C;
   gemm_f64_body<AK, BKC, V16, MASK>(p, (int)blockIdx.x - gs.g[g].tile0, vecC);
 }
@@ -350,6 +353,7 @@ cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStre
   const int TM = (int)((p.M + g64::BM - 1) / g64::BM), TN = (int)((p.N + g64::BN - 1) / g64::BN);
   const int ntiles = masked_tiles(mask, TM, TN, p.off);
   if (ntiles == 0) return cudaSuccess;
+  T64::make_raster(mask, TM, TN, p.off, kGroupCols, p.rs);
   const bool v16 = aligned16(p.A, p.lda) && aligned16(p.B, p.ldb);
   const int vecC = aligned16(p.C, p.ldc) && (!p.beta || aligned16(p.Cin, p.ldcin));
   cudaError_t e = launch_key(p, nullptr, a_kcontig, b_kcontig, v16, mask, ntiles, vecC, st);
@@ -366,6 +370,7 @@ cudaError_t gemm_f64_grouped(GemmF64 p, const GemmGroup* groups, int count, int 
                              cudaStream_t st) {
   // groups with an empty block are dropped; one launch per kMaxGroups groups
   if (p.K <= 0) return cudaErrorInvalidValue;
+  p.rs.ngroups = 0;
   bool v16 = (p.lda % 2) == 0 && (p.ldb % 2) == 0;
   int vecC = (p.ldc % 2) == 0 && (!p.beta || (p.ldcin % 2) == 0);
   p.splits = 1;

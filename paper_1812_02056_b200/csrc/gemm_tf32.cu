@@ -167,6 +167,8 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constan
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int TM = (int)((p.M + BM - 1) / BM), TN = (int)((p.N + BN - 1) / BN);
   int ti, tj;
+  // column order (not the DMMA kernel's rasterized order): the CTAs running at once then
+  // read the same B slices (2/3 of the operand bytes), which L2 serves as one request
   C_::TT::tile_of(p.mask, blockIdx.x, TM, TN, p.off, ti, tj);
   const int64_t i0 = (int64_t)ti * BM, j0 = (int64_t)tj * BN;
   const int nkb = (int)((p.K + BK - 1) / BK);

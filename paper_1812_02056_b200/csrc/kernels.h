@@ -29,6 +29,7 @@ struct GemmF64 {
   double* work;
   const long long* fail;   // device "first failed column" word; kernels exit early if set
   int64_t off = 0;         // mask diagonal offset: lower keeps i >= j + off, upper i <= j + off
+  Raster rs;               // tile rasterization (filled by the launcher)
 };
 cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStream_t st);
 

@@ -3,7 +3,7 @@ import sys
 import torch
 sys.path.insert(0, '.')
 import paper_1812_02056_b200 as sf
-m, k = 8192, 512
+m, k = (int(sys.argv[1]) if len(sys.argv) > 1 else 8192), 512
 R = torch.randn(k, m, device='cuda', dtype=torch.float64)   # column-major m x k
 C = torch.randn(m, m, device='cuda', dtype=torch.float64)
 for _ in range(2):
