@@ -336,6 +336,78 @@ static int check_common(int64_t n, int64_t s, int dtype, const void* a, int64_t 
   return SF_OK;
 }
 
+// ------------------------------------------------------------------ CUDA graphs
+// A factorization is a fixed sequence of ~3 launches per panel for given (n, s, pointers),
+// so repeated calls replay one captured CUDA graph instead of re-launching every kernel —
+// the small configs (n = 256 .. 4096) are launch-bound.  The first call with a key runs
+// eagerly (it also performs one-time setup: function attributes, streams, module loading),
+// the second captures and instantiates, later ones replay.  Off when profiling is enabled,
+// on the legacy default stream, inside a caller's own capture, or with SF_GRAPH=0.
+struct GraphKey {
+  int kind, dtype;
+  int64_t n, s, lda, ld1, ld2;
+  const void *a, *o1, *o2;
+  int64_t* info;
+  cudaStream_t st;
+  bool operator==(const GraphKey& o) const {
+    return kind == o.kind && dtype == o.dtype && n == o.n && s == o.s && lda == o.lda && ld1 == o.ld1 &&
+           ld2 == o.ld2 && a == o.a && o1 == o.o1 && o2 == o.o2 && info == o.info && st == o.st;
+  }
+};
+struct GraphEntry { GraphKey key; cudaGraphExec_t exec = nullptr; long long launches = 0; uint64_t used = 0; };
+static std::vector<GraphEntry> g_graphs;
+static uint64_t g_graph_clock = 0;
+static bool graphs_on() {
+  static int on = [] { const char* e = getenv("SF_GRAPH"); return e ? atoi(e) : 1; }();
+  return on != 0;
+}
+
+template <typename F>
+static int run_graph(const GraphKey& key, cudaStream_t st, F&& body) {
+  if (!graphs_on() || g_prof || st == nullptr) return body();
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return body();
+  GraphEntry* e = nullptr;
+  for (auto& g : g_graphs)
+    if (g.key == key) e = &g;
+  if (!e) {   // first sighting: eager run, remember the key
+    if (g_graphs.size() >= 8) {   // evict the least recently used
+      size_t lru = 0;
+      for (size_t i = 1; i < g_graphs.size(); ++i)
+        if (g_graphs[i].used < g_graphs[lru].used) lru = i;
+      if (g_graphs[lru].exec) cudaGraphExecDestroy(g_graphs[lru].exec);
+      g_graphs.erase(g_graphs.begin() + lru);
+    }
+    GraphEntry ne;
+    ne.key = key;
+    ne.used = ++g_graph_clock;
+    g_graphs.push_back(ne);
+    return body();
+  }
+  e->used = ++g_graph_clock;
+  if (!e->exec) {
+    const long long l0 = g_launches.load();
+    SF_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    const int rc = body();
+    cudaGraph_t g = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(st, &g);
+    const long long nl = g_launches.load() - l0;
+    g_launches.fetch_sub(nl);   // captured, not launched
+    if (rc != SF_OK || ec != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      if (rc != SF_OK) return rc;
+      return fail_with(SF_ECUDA, "graph capture: %s", cudaGetErrorString(ec));
+    }
+    const cudaError_t ei = cudaGraphInstantiateWithFlags(&e->exec, g, cudaGraphInstantiateFlagUseNodePriority);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) { e->exec = nullptr; return fail_with(SF_ECUDA, "graph instantiate: %s", cudaGetErrorString(ei)); }
+    e->launches = nl;
+  }
+  SF_CUDA(cudaGraphLaunch(e->exec, st));
+  count_launch((int)e->launches);
+  return SF_OK;
+}
+
 }  // namespace sf
 
 using namespace sf;
@@ -348,8 +420,11 @@ int chol_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, vo
   if (rc) return rc;
   if (!d_info) return fail_with(SF_EINVAL, "null d_info");
   cudaStream_t st = (cudaStream_t)stream;
-  if (dtype == SF_F64) return chol_run<double>(n, s, (const double*)dA, lda, (double*)dL, ldl, d_info, st);
-  return chol_run_f32(n, s, (const float*)dA, lda, (float*)dL, ldl, d_info, st);
+  const GraphKey key{0, dtype, n, s, lda, ldl, 0, dA, dL, nullptr, d_info, st};
+  return run_graph(key, st, [&]() {
+    if (dtype == SF_F64) return chol_run<double>(n, s, (const double*)dA, lda, (double*)dL, ldl, d_info, st);
+    return chol_run_f32(n, s, (const float*)dA, lda, (float*)dL, ldl, d_info, st);
+  });
 }
 
 int lu_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dLU, int64_t ldlu, int64_t* d_info,
@@ -358,7 +433,9 @@ int lu_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void
   if (rc) return rc;
   if (!d_info) return fail_with(SF_EINVAL, "null d_info");
   if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp32 LU not implemented (SURVEY.md §8 f4)");
-  return lu_run<double>(n, s, (const double*)dA, lda, (double*)dLU, ldlu, d_info, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  const GraphKey key{1, dtype, n, s, lda, ldlu, 0, dA, dLU, nullptr, d_info, st};
+  return run_graph(key, st, [&]() { return lu_run<double>(n, s, (const double*)dA, lda, (double*)dLU, ldlu, d_info, st); });
 }
 
 int qr_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dQ, int64_t ldq, void* dR,
@@ -370,8 +447,11 @@ int qr_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void
   if (dA == dQ || dA == dR || dQ == dR) return fail_with(SF_EINVAL, "qr_factor outputs must not alias");
   if (!d_info) return fail_with(SF_EINVAL, "null d_info");
   if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp32 QR not implemented (SURVEY.md §8 f4)");
-  return qr_run<double>(n, s, (const double*)dA, lda, (double*)dQ, ldq, (double*)dR, ldr, d_info,
-                        (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  const GraphKey key{2, dtype, n, s, lda, ldq, ldr, dA, dQ, dR, d_info, st};
+  return run_graph(key, st, [&]() {
+    return qr_run<double>(n, s, (const double*)dA, lda, (double*)dQ, ldq, (double*)dR, ldr, d_info, st);
+  });
 }
 
 // ------------------------------------------------------------------ host-buffer variants
@@ -381,8 +461,11 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
   if (lda < n || ld1 < n || (kind == 2 && ld2 < n)) return fail_with(SF_EINVAL, "leading dimension < n");
   const size_t elt = dtype == SF_F64 ? 8 : 4;
   const size_t bytes = elt * (size_t)n * (size_t)n;
-  cudaStream_t st;
-  SF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  static cudaStream_t streams[16] = {};
+  int devh = 0;
+  SF_CUDA(cudaGetDevice(&devh));
+  if (!streams[devh & 15]) SF_CUDA(cudaStreamCreateWithFlags(&streams[devh & 15], cudaStreamNonBlocking));
+  cudaStream_t st = streams[devh & 15];
   {
     // keep freed device blocks in the stream-ordered pool so repeated calls do not pay
     // for fresh allocations
@@ -396,7 +479,7 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
   char* d = nullptr;
   const int nbuf = kind == 2 ? 3 : 1;
   cudaError_t e = cudaMallocAsync((void**)&d, nbuf * bytes + 256, st);
-  if (e != cudaSuccess) { cudaStreamDestroy(st); return fail_with(SF_ENOMEM, "device allocation failed"); }
+  if (e != cudaSuccess) return fail_with(SF_ENOMEM, "device allocation failed");
   int64_t* dinfo = (int64_t*)(d + nbuf * bytes);
   int rc = SF_OK;
   e = cudaMemcpy2DAsync(d, n * elt, hA, lda * elt, n * elt, n, cudaMemcpyHostToDevice, st);
@@ -418,7 +501,6 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
   }
   cudaFreeAsync(d, st);
   cudaError_t e2 = cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
   if (rc) return rc;
   if (e != cudaSuccess) return fail_with(SF_ECUDA, "host copy: %s", cudaGetErrorString(e));
   if (e2 != cudaSuccess) return fail_with(SF_ECUDA, "stream sync: %s", cudaGetErrorString(e2));

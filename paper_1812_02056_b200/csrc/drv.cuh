@@ -70,7 +70,21 @@ struct Workspace {
   cudaError_t init(size_t bytes, cudaStream_t s) {
     st = s;
     cap = bytes;
+    keep_pool();
     return cudaMallocAsync((void**)&base, bytes, s);
+  }
+  // keep freed workspace in the device's stream-ordered pool (the default release
+  // threshold of 0 would unmap it at every synchronization and remap it next call)
+  static void keep_pool() {
+    static bool done[16] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || done[dev & 15]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev & 15] = true;
   }
   template <typename U>
   U* take(size_t n) {

@@ -305,3 +305,55 @@ def test_lookahead_repeatable(s):
     for _ in range(3):
         Lg, Ug, info = run_lu(B, s)
         assert info == 0 and synth.r2_error(Lg, Lo) <= TOL64 and synth.r2_error(Ug, Uo) <= TOL64
+
+
+@pytest.mark.parametrize("kind", ["chol", "lu", "qr", "chol32"])
+def test_graph_replay(kind):
+    """Repeated calls with the same arguments replay a captured CUDA graph (driver.cu
+    run_graph: eager, capture, replay): every call must produce the oracle's factor, and
+    the library's launch counter must keep counting the replayed kernels."""
+    n, s = 600, 96
+    if kind.startswith("chol"):
+        A = synth.gen_numpy("spd_scaled", n, seed=3)
+        if kind == "chol32":
+            A = A.astype(np.float32).astype(np.float64)
+        Lo, _ = oracle.chol(A, s)
+    elif kind == "lu":
+        A = synth.gen_numpy("diag_dominant", n, seed=3)
+        Lo, Uo, _ = oracle.lu(A, s)
+    else:
+        A = synth.gen_numpy("gaussian", n, seed=3)
+        Qo, Ro, _, _ = oracle.qr(A, s)
+    dA = dev(A)
+    if kind == "chol32":
+        dA = dA.float()
+    o1 = torch.empty_like(dA); o2 = torch.empty_like(dA)
+    info = torch.zeros(1, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.Stream()
+    counts = []
+    for it in range(4):
+        o1.fill_(0.0); o2.fill_(0.0); info.fill_(-1)
+        torch.cuda.synchronize()
+        l0 = sf.launch_counter()
+        with torch.cuda.stream(stream):
+            if kind == "chol":
+                sf.chol_colmajor(n, s, dA, n, o1, n, info, stream=stream)
+            elif kind == "chol32":
+                sf.chol_colmajor(n, s, dA, n, o1, n, info, dtype=sf.SF_F32, stream=stream)
+            elif kind == "lu":
+                sf.lu_colmajor(n, s, dA, n, o1, n, info, stream=stream)
+            else:
+                sf.qr_colmajor(n, s, dA, n, o1, n, o2, n, info, stream=stream)
+        stream.synchronize()
+        counts.append(sf.launch_counter() - l0)
+        assert int(info.item()) == 0, it
+        F = host(o1.double())
+        if kind == "chol":
+            assert synth.r2_error(np.tril(F), Lo) <= TOL64, it
+        elif kind == "chol32":
+            assert synth.r2_error(np.tril(F), Lo) <= 2e-4, it
+        elif kind == "lu":
+            assert synth.r2_error(np.tril(F), Lo) <= TOL64 and synth.r2_error(np.triu(F, 1) + np.eye(n), Uo) <= TOL64
+        else:
+            check_qr(A, s, F, host(o2), Qo, Ro)
+    assert counts[0] > 10 and counts[1:] == [counts[0]] * 3, counts
