@@ -265,6 +265,242 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constan
   }
 }
 
+// ------------------------------------------------------------------ CTA-pair variant
+// cta_group::2: a cluster of two CTAs on one TPC computes a 256 x 256 tile with M = 256
+// MMAs issued by the leader (rank 0).  Each CTA stages only ITS half of the operands — A rows
+// [rank*128, +128) and B rows [rank*128, +128) — so an SM receives 2 x 32 KB per BK slice
+// instead of 48 KB for the same MMA work (the single-CTA kernel is bound by that operand
+// traffic).  Protocol (the leader's barriers coordinate both CTAs):
+//   full[s]   (leader)   1 arrival (leader's expect_tx of both CTAs' bytes) + the tx of both
+//                        CTAs' TMA (cta_group::2 form, barrier address with the peer bit
+//                        cleared -> the leader's barrier)
+//   empty[s]  (each CTA) the leader's tcgen05.commit multicast to both CTAs
+//   tfull     (each CTA) likewise, after the last MMA; each CTA then drains its own TMEM
+//                        (its 128 rows of D)
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;   // shared::cluster address of the rank-0 CTA
+
+namespace t32p {
+constexpr int BM = 256, BN = 256, HALF = 128, BK = 16;
+constexpr int TILE = HALF * BK * 4;                 // one operand tile per CTA: 8 KB
+constexpr int STAGE_BYTES = 4 * TILE;               // A_hi, A_lo, B_hi, B_lo halves: 32 KB
+constexpr int STAGES = 3;                           // 96 KB: two CTAs (of different pairs) per SM
+constexpr int TMEM_COLS = BN;
+constexpr int ECOLS = 64;                           // epilogue C chunk: 128 rows x 64 columns = 32 KB
+constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+static_assert(3 * HALF * ECOLS * 4 <= STAGES * STAGE_BYTES, "epilogue ring fits in the stage buffers");
+using TT = Tiles<BM, BN>;
+}  // namespace t32p
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];\n" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(leader_bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void umma_tf32_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
+// One 256 x 256 tile per pair, two CTAs per SM.  Epilogue: when the CTA's 128 x 256 block of
+// C lies inside the mask with whole 16-byte columns, C is fetched with bulk async copies
+// (cp.async.bulk, 512 B per column) through a 3-deep ring of 64-column chunks in the idle
+// stage buffers — the epilogue is latency-bound otherwise (32 scalar loads in flight per
+// thread) — and results are stored straight from registers.  Other blocks (the diagonal,
+// ragged edges, unaligned C) take the per-element path.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(t32::THREADS, 2)
+gemm_tf32x3_pair_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+                        const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, Tf32Params p,
+                        int vecC) {
+  using namespace t32p;
+  // no early exit on p.fail here: both CTAs of the pair must reach every cluster barrier
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* cbar = tfull + 1;           // [3] epilogue chunk ring
+  uint32_t* tmem_slot = (uint32_t*)(cbar + 3);
+  auto sAh = [&](int s) { return smem + s * STAGE_BYTES; };
+  auto sAl = [&](int s) { return smem + s * STAGE_BYTES + TILE; };
+  auto sBh = [&](int s) { return smem + s * STAGE_BYTES + 2 * TILE; };
+  auto sBl = [&](int s) { return smem + s * STAGE_BYTES + 3 * TILE; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int TM = (int)((p.M + BM - 1) / BM), TN = (int)((p.N + BN - 1) / BN);
+  int ti, tj;
+  TT::tile_of(p.mask, blockIdx.x >> 1, TM, TN, p.off, ti, tj);
+  const int64_t i0 = (int64_t)ti * BM, j0 = (int64_t)tj * BN;
+  const int64_t r0 = i0 + rank * HALF;    // this CTA's first C row
+  const int nkb = (int)((p.K + BK - 1) / BK);
+  const bool skip = p.fail && failed(p.fail);
+  // bulk epilogue: the whole 128 x 256 block is inside M, N and the mask
+  const int64_t jl = j0 + BN - 1;
+  const bool inside = (r0 + HALF <= p.M) && (j0 + BN <= p.N) &&
+                      (p.mask == kMaskNone || (p.mask == kMaskLower ? r0 >= jl + p.off : r0 + HALF - 1 <= j0 + p.off));
+  const bool bulk = vecC && inside && !skip;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    for (int c = 0; c < 3; ++c) mbar_init(&cbar[c], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tma_prefetch_desc(&mAh); tma_prefetch_desc(&mAl); tma_prefetch_desc(&mBh); tma_prefetch_desc(&mBl);
+  } else if (warp == 0) {
+    for (int u = lane - 1; u < BN * 4; u += 31) {   // warm L2 with this CTA's C rows
+      const int64_t j = j0 + (u >> 2), i = r0 + (u & 3) * 32;
+      if (j < p.N && i < p.M) prefetch_l2(p.Cin + i + j * p.ldcin);
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync_all();   // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int ya = (int)r0, yb = (int)(j0 + rank * HALF);
+      const uint32_t lbar0 = smem_u32(&full[0]) & kPeerMask;
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+        if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+        const uint32_t lbar = lbar0 + s * 8;
+        tma_load_2d_pair(sAh(s), &mAh, lbar, kb * BK, ya);
+        tma_load_2d_pair(sAl(s), &mAl, lbar, kb * BK, ya);
+        tma_load_2d_pair(sBh(s), &mBh, lbar, kb * BK, yb);
+        tma_load_2d_pair(sBl(s), &mBl, lbar, kb * BK, yb);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_tf32(BM, BN);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&full[s], (kb / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t ah = smem_u32(sAh(s)), al = smem_u32(sAl(s)), bh = smem_u32(sBh(s)), bl = smem_u32(sBl(s));
+#pragma unroll
+        for (int k = 0; k < BK / t32::UMMA_K; ++k) {
+          const uint32_t o = k * t32::UMMA_K * 4;
+          umma_tf32_pair(tmem, umma_desc_sw64(ah + o), umma_desc_sw64(bh + o), idesc, (kb | k) != 0);
+          umma_tf32_pair(tmem, umma_desc_sw64(ah + o), umma_desc_sw64(bl + o), idesc, 1);
+          umma_tf32_pair(tmem, umma_desc_sw64(al + o), umma_desc_sw64(bh + o), idesc, 1);
+        }
+        umma_commit_pair(&empty[s]);
+      }
+      umma_commit_pair(tfull);
+    }
+  } else {
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const int row = q * 32 + lane;          // this thread's row inside the CTA's 128 rows
+    const int64_t i = r0 + row;
+    mbar_wait(tfull, 0);                    // all MMAs done: the stage buffers are free
+    tc_fence_after();
+    if (bulk) {
+      float* ring = (float*)smem;           // [3][ECOLS][HALF], column-major chunks
+      constexpr int NCH = BN / ECOLS;
+      auto issue = [&](int ch) {            // warp 2 fetches chunk ch into ring slot ch % 3
+        float* dst = ring + (ch % 3) * ECOLS * HALF;
+        if (lane == 0) mbar_expect_tx(&cbar[ch % 3], ECOLS * HALF * 4);
+        __syncwarp();
+        for (int u = lane; u < ECOLS; u += 32)
+          bulk_g2s(dst + u * HALF, p.Cin + r0 + (j0 + ch * ECOLS + u) * p.ldcin, HALF * 4, &cbar[ch % 3]);
+      };
+      if (warp == 2)
+        for (int ch = 0; ch < 3 && ch < NCH; ++ch) issue(ch);
+      for (int ch = 0; ch < NCH; ++ch) {
+        mbar_wait(&cbar[ch % 3], (ch / 3) & 1);
+        const float* src = ring + (ch % 3) * ECOLS * HALF;
+#pragma unroll
+        for (int c = 0; c < ECOLS; c += 32) {
+          float v[32];
+          tmem_ld32(tmem + lane_base + (uint32_t)(ch * ECOLS + c), v);
+#pragma unroll
+          for (int u = 0; u < 32; ++u) {
+            const int64_t j = j0 + ch * ECOLS + c + u;
+            __stcg(p.C + i + j * p.ldc, src[(c + u) * HALF + row] - v[u]);
+          }
+        }
+        epi_bar_sync();                     // all four epilogue warps are done with slot ch % 3
+        if (warp == 2 && ch + 3 < NCH) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic reads before async writes
+          issue(ch + 3);
+        }
+      }
+    } else {
+      for (int c = 0; c < BN; c += 32) {
+        if (j0 + c >= p.N) break;
+        float v[32];
+        tmem_ld32(tmem + lane_base + (uint32_t)c, v);
+        if (i < p.M && !skip) {
+          float cin[32];
+#pragma unroll
+          for (int u = 0; u < 32; ++u) {
+            const int64_t j = j0 + c + u;
+            const bool in = j < p.N && (p.mask == kMaskNone || (p.mask == kMaskLower ? i >= j + p.off : i <= j + p.off));
+            cin[u] = in ? __ldcg(p.Cin + i + j * p.ldcin) : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 32; ++u) {
+            const int64_t j = j0 + c + u;
+            const bool in = j < p.N && (p.mask == kMaskNone || (p.mask == kMaskLower ? i >= j + p.off : i <= j + p.off));
+            if (in) __stcg(p.C + i + j * p.ldc, cin[u] - v[u]);
+          }
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  cluster_sync_all();   // the peer's TMEM / smem stay live until the leader's MMAs are done
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 // ------------------------------------------------------------------ split kernel
 // x -> (rna_tf32(x), rna_tf32(x - hi)), transposed from column-major (m x k, ld) to K-major
 // (row i: k contiguous values at H + i*ldk).  32 x 32 tiles through shared memory.
@@ -359,6 +595,37 @@ static cudaError_t launch_bn(const Tf32Gemm& g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+static cudaError_t launch_pair(const Tf32Gemm& g, cudaStream_t st) {
+  using namespace t32p;
+  const int TM = (int)((g.M + BM - 1) / BM), TN = (int)((g.N + BN - 1) / BN);
+  const int ntiles = TT::count(g.mask, TM, TN, g.off);
+  if (ntiles == 0) return cudaSuccess;
+  CUtensorMap mAh, mAl, mBh, mBl;
+  cudaError_t e;
+  if ((e = make_map(&mAh, g.Ah, g.K, g.M, g.ldk_a, HALF)) != cudaSuccess) return e;
+  if ((e = make_map(&mAl, g.Al, g.K, g.M, g.ldk_a, HALF)) != cudaSuccess) return e;
+  if ((e = make_map(&mBh, g.Bh, g.K, g.N, g.ldk_b, HALF)) != cudaSuccess) return e;
+  if ((e = make_map(&mBl, g.Bl, g.K, g.N, g.ldk_b, HALF)) != cudaSuccess) return e;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(gemm_tf32x3_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  Tf32Params p{g.M, g.N, g.K, g.Cin, g.ldcin, g.C, g.ldc, g.off, g.mask, g.fail};
+  static int bulk_on = [] { const char* e = getenv("SF_TF32_BULKEPI"); return e ? atoi(e) : 1; }();
+  const int vecC = bulk_on && (g.ldc % 4) == 0 && (g.ldcin % 4) == 0 && ((uintptr_t)g.Cin % 16) == 0 &&
+                   ((uintptr_t)g.C % 16) == 0;
+  gemm_tf32x3_pair_kernel<<<2 * ntiles, t32::THREADS, SMEM, st>>>(mAh, mAl, mBh, mBl, p, vecC);
+  count_launch();
+  return cudaGetLastError();
+}
+
+static bool pair_on() {
+  static int on = [] { const char* e = getenv("SF_TF32_PAIR"); return e ? atoi(e) : 1; }();
+  return on != 0;
+}
+
 cudaError_t gemm_tf32x3(const Tf32Gemm& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaSuccess;
   if ((g.ldk_a % 4) || (g.ldk_b % 4) || ((uintptr_t)g.Ah % 16) || ((uintptr_t)g.Al % 16) || ((uintptr_t)g.Bh % 16) ||
@@ -367,6 +634,7 @@ cudaError_t gemm_tf32x3(const Tf32Gemm& g, cudaStream_t st) {
   // narrow updates (the panel recursion's corrections) take a narrower tile
   if (g.N <= 64) return launch_bn<64>(g, st);
   if (g.N <= 128) return launch_bn<128>(g, st);
+  if (pair_on()) return launch_pair(g, st);   // wide flushes: CTA pairs (cta_group::2)
   return launch_bn<256>(g, st);
 }
 
