@@ -452,6 +452,9 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dist.all_reduce(bb, op=dist.ReduceOp.SUM)
         dt = float(tt.item()); tot_bytes = int(bb.item())
+        if kind == "chol" and not use_dist:
+            # chol_factor_host moves the lower triangle panel by panel, both directions
+            tot_bytes = sum((n - z) * min(s, n - z) for z in range(0, n, s)) * A.element_size()
         e2e = {"value": ke * flops / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": tot_bytes,
                "d2h_bytes_per_step": tot_bytes * (2 if kind == "qr" else 1), "steps": ke, "api": api}
         del hA, h1, h2

@@ -81,8 +81,12 @@ int qr_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void
 
 /* Host-buffer variants (the end-to-end path): same arguments with HOST matrices (pinned
  * memory recommended) and a host info word.  The library copies A to the device, runs
- * the device entry point on an internal stream, copies the outputs back and
- * synchronizes before returning.  Outputs may alias the input exactly (in place). */
+ * the factorization on an internal stream, copies the outputs back and synchronizes
+ * before returning.  Outputs may alias the input exactly (in place).
+ * chol_factor_host moves only the lower triangle (incl. diagonal), panel by panel, and
+ * copies each panel of L back as soon as it is final, overlapped with the remaining
+ * flushes.  The strict upper triangle of hL is unspecified out of place (entries inside the
+ * s x s diagonal blocks receive A's values); in place (hL == hA) it keeps A's values. */
 int chol_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hL, int64_t ldl,
                      int64_t* info);
 int lu_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hLU, int64_t ldlu,

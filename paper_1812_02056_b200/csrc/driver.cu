@@ -54,7 +54,7 @@ int fail_with(int code, const char* fmt, ...) {
 
 template <typename T>
 static int chol_run(int64_t n, int64_t s, const T* A, int64_t lda, T* L, int64_t ldl, int64_t* d_info,
-                    cudaStream_t st) {
+                    cudaStream_t st, PanelHook* hook = nullptr) {
   Workspace ws;
   SF_CUDA(ws.init(4096, st));
   long long* fail = ws.take<long long>(2);   // [0] first failed column, [1] leaf counter
@@ -66,6 +66,7 @@ static int chol_run(int64_t n, int64_t s, const T* A, int64_t lda, T* L, int64_t
     ProfScope ps(1, 0.0, st);
     const int64_t w0 = s < n ? s : n;
     SF_CUDA(chol_panel_rec<T>(n, w0, A, lda, L, ldl, 0, fail, st));
+    if (hook) SF_CUDA(hook->done(0, w0, st));
   }
   for (int64_t z = 0; z < n; z += s) {
     const int64_t w = (s < n - z) ? s : n - z, c = z + w;
@@ -84,6 +85,7 @@ static int chol_run(int64_t n, int64_t s, const T* A, int64_t lda, T* L, int64_t
       {
         ProfScope ps(1, 0.0, sd->st);
         SF_CUDA(chol_panel_rec<T>(m, w2, L + c + c * ldl, ldl, L + c + c * ldl, ldl, c, fail, sd->st));
+        if (hook) SF_CUDA(hook->done(c, w2, sd->st));
       }
       if (m > w2) {  // flush, part 2: the rest of the trailing matrix, concurrently with the panel
         const int64_t c2 = c + w2;
@@ -100,6 +102,7 @@ static int chol_run(int64_t n, int64_t s, const T* A, int64_t lda, T* L, int64_t
       }
       ProfScope ps(1, 0.0, st);
       SF_CUDA(chol_panel_rec<T>(m, w2, L + c + c * ldl, ldl, L + c + c * ldl, ldl, c, fail, st));
+      if (hook) SF_CUDA(hook->done(c, w2, st));
     }
   }
   SF_CUDA(finish_info(fail, d_info, st));
@@ -111,7 +114,7 @@ static int chol_run(int64_t n, int64_t s, const T* A, int64_t lda, T* L, int64_t
 // schedule and lookahead as chol_run; each panel's split (hi/lo) lives in one of two
 // buffers so the side stream can split panel p+1 while the flush of panel p reads panel p's.
 static int chol_run_f32(int64_t n, int64_t s, const float* A, int64_t lda, float* L, int64_t ldl, int64_t* d_info,
-                        cudaStream_t st) {
+                        cudaStream_t st, PanelHook* hook = nullptr) {
   const int64_t ldk = (s + 3) / 4 * 4;
   Workspace ws;
   SF_CUDA(ws.init(4096 + 4 * sizeof(float) * (size_t)n * ldk + 4 * 256, st));
@@ -130,6 +133,7 @@ static int chol_run_f32(int64_t n, int64_t s, const float* A, int64_t lda, float
     ProfScope ps(1, 0.0, st);
     const int64_t w0 = s < n ? s : n;
     SF_CUDA(chol_panel_rec_f32(n, w0, A, lda, L, ldl, 0, sb[0], fail, st));
+    if (hook) SF_CUDA(hook->done(0, w0, st));
     if (w0 < n) SF_CUDA(split_tf32(n - w0, w0, L + w0, ldl, sb[0].at(w0, 0).h, sb[0].at(w0, 0).l, ldk, st));
   }
   int64_t p = 0;
@@ -153,6 +157,7 @@ static int chol_run_f32(int64_t n, int64_t s, const float* A, int64_t lda, float
     {
       ProfScope ps(1, 0.0, pst);
       SF_CUDA(chol_panel_rec_f32(m, w2, L + c + c * ldl, ldl, L + c + c * ldl, ldl, c, nxt, fail, pst));
+      if (hook) SF_CUDA(hook->done(c, w2, pst));
       if (w2 < m) SF_CUDA(split_tf32(m - w2, w2, L + c + w2 + c * ldl, ldl, nxt.at(w2, 0).h, nxt.at(w2, 0).l, ldk, pst));
     }
     if (la) {
@@ -459,6 +464,9 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
                      void* hO2, int64_t ld2, int64_t* info) {
   if (n < 1 || !hA || !hO1 || !info || (kind == 2 && !hO2)) return fail_with(SF_EINVAL, "bad host arguments");
   if (lda < n || ld1 < n || (kind == 2 && ld2 < n)) return fail_with(SF_EINVAL, "leading dimension < n");
+  if (s < 1 || s > n) return fail_with(SF_EINVAL, "step s=%lld outside [1, n=%lld]", (long long)s, (long long)n);
+  if (dtype != SF_F64 && dtype != SF_F32) return fail_with(SF_EINVAL, "unknown dtype %d", dtype);
+  if (kind != 0 && dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp32 LU/QR not implemented (SURVEY.md §8 f4)");
   const size_t elt = dtype == SF_F64 ? 8 : 4;
   const size_t bytes = elt * (size_t)n * (size_t)n;
   static cudaStream_t streams[16] = {};
@@ -482,13 +490,50 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
   if (e != cudaSuccess) return fail_with(SF_ENOMEM, "device allocation failed");
   int64_t* dinfo = (int64_t*)(d + nbuf * bytes);
   int rc = SF_OK;
+  if (kind == 0) {
+    // Cholesky reads and writes only the lower triangle: copy it panel by panel (half the
+    // bytes), and return each panel of L as soon as it is final, on a copy stream, while the
+    // later flushes run (the device->host copy hides behind the factorization).
+    static cudaStream_t cstreams[16] = {};
+    static cudaEvent_t cevents[16] = {};
+    if (!cstreams[devh & 15]) {
+      SF_CUDA(cudaStreamCreateWithFlags(&cstreams[devh & 15], cudaStreamNonBlocking));
+      SF_CUDA(cudaEventCreateWithFlags(&cevents[devh & 15], cudaEventDisableTiming));
+    }
+    cudaStream_t cs = cstreams[devh & 15];
+    cudaEvent_t ev = cevents[devh & 15];
+    for (int64_t z = 0; z < n && e == cudaSuccess; z += s) {
+      const int64_t w = (s < n - z) ? s : n - z;
+      e = cudaMemcpy2DAsync(d + elt * (z + z * n), n * elt, (const char*)hA + elt * (z + z * lda), lda * elt,
+                            (n - z) * elt, w, cudaMemcpyHostToDevice, st);
+    }
+    struct D2H : PanelHook {
+      int64_t n, ldh; size_t elt; const char* dev; char* host; cudaStream_t cs; cudaEvent_t ev;
+      cudaError_t done(int64_t z, int64_t w, cudaStream_t pst) override {
+        cudaError_t r = cudaEventRecord(ev, pst);
+        if (r == cudaSuccess) r = cudaStreamWaitEvent(cs, ev, 0);
+        if (r == cudaSuccess)
+          r = cudaMemcpy2DAsync(host + elt * (z + z * ldh), ldh * elt, dev + elt * (z + z * n), n * elt,
+                                (n - z) * elt, w, cudaMemcpyDeviceToHost, cs);
+        return r;
+      }
+    } hook;
+    hook.n = n; hook.ldh = ld1; hook.elt = elt; hook.dev = d; hook.host = (char*)hO1; hook.cs = cs; hook.ev = ev;
+    if (e == cudaSuccess) {
+      SF_CUDA(cudaEventRecord(ev, st));      // the copy stream must not run ahead of the previous call
+      SF_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+      rc = dtype == SF_F64 ? chol_run<double>(n, s, (const double*)d, n, (double*)d, n, dinfo, st, &hook)
+                           : chol_run_f32(n, s, (const float*)d, n, (float*)d, n, dinfo, st, &hook);
+      if (!rc) {
+        e = cudaEventRecord(ev, cs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev, 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(info, dinfo, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+      }
+    }
+  } else {
   e = cudaMemcpy2DAsync(d, n * elt, hA, lda * elt, n * elt, n, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) {
-    if (kind == 0) {
-      // upper triangle of the device copy is A's own (in-place factorization)
-      rc = chol_factor(n, s, dtype, d, n, d, n, dinfo, st);
-      if (!rc) e = cudaMemcpy2DAsync(hO1, ld1 * elt, d, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);
-    } else if (kind == 1) {
+    if (kind == 1) {
       rc = lu_factor(n, s, dtype, d, n, d, n, dinfo, st);
       if (!rc) e = cudaMemcpy2DAsync(hO1, ld1 * elt, d, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);
     } else {
@@ -498,6 +543,7 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
         e = cudaMemcpy2DAsync(hO2, ld2 * elt, d + 2 * bytes, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);
     }
     if (!rc && e == cudaSuccess) e = cudaMemcpyAsync(info, dinfo, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  }
   }
   cudaFreeAsync(d, st);
   cudaError_t e2 = cudaStreamSynchronize(st);

@@ -98,6 +98,15 @@ struct Workspace {
   }
 };
 
+// ------------------------------------------------------------------ panel completion hook
+// Called (on the host, while enqueueing) after the work that finishes panel [z, z+w) has
+// been enqueued on stream `st`: the end-to-end host path uses it to start the device->host
+// copy of each finished panel while the later flushes run.
+struct PanelHook {
+  virtual ~PanelHook() {}
+  virtual cudaError_t done(int64_t z, int64_t w, cudaStream_t st) = 0;
+};
+
 // ------------------------------------------------------------------ lookahead streams
 // Panel p+1 is factored on a high-priority side stream while the rest of flush p runs on
 // the caller's stream (classic lookahead): the caller's stream first updates only the

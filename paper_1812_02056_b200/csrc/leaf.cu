@@ -128,12 +128,103 @@ __global__ void __launch_bounds__(kLeafT) chol_leaf_kernel(int64_t m, int w, con
     if (k < w) dst[r + (int64_t)k * ldd] = x[k];
 }
 
+// Variant: ONE warp factors the diagonal block (warp-synchronous Crout in shared memory,
+// lane i = row i, no block-wide barrier per column) while the other warps already load
+// their rows below from HBM; one __syncthreads, then the substitutions.  Same arithmetic per
+// element as chol_leaf_kernel (k-sums in four interleaved partial sums, then one
+// subtraction, sqrt, division by L_cc in the block, multiplication by 1/L_cc below).
+template <typename T, int W>
+__global__ void __launch_bounds__(kLeafT) chol_leaf_warp_kernel(int64_t m, int w, const T* __restrict__ src,
+                                                                int64_t lds, T* __restrict__ dst, int64_t ldd,
+                                                                int64_t col0, long long* fail) {
+  if (failed(fail)) return;
+  __shared__ T Ls[W][W + 1];
+  __shared__ T inv[W];
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r = w + (int64_t)blockIdx.x * kLeafT + tid;
+  T x[W];
+  if (warp == 0) {
+    if (lane < W)
+      for (int k = 0; k < W; ++k) Ls[lane][k] = (lane < w && k <= lane && k < w) ? __ldcg(src + lane + (int64_t)k * lds) : T(0);
+    __syncwarp();
+    int okc = 1;
+    for (int c = 0; c < w; ++c) {
+      T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+      const int i = lane;
+      if (i >= c && i < w) {
+        int k = 0;
+        for (; k + 3 < c; k += 4) {
+          a0 = fma(Ls[i][k], Ls[c][k], a0);
+          a1 = fma(Ls[i][k + 1], Ls[c][k + 1], a1);
+          a2 = fma(Ls[i][k + 2], Ls[c][k + 2], a2);
+          a3 = fma(Ls[i][k + 3], Ls[c][k + 3], a3);
+        }
+        for (; k < c; ++k) a0 = fma(Ls[i][k], Ls[c][k], a0);
+      }
+      const T t = (i < w) ? Ls[i][c] - ((a0 + a1) + (a2 + a3)) : T(0);
+      const T d = __shfl_sync(kFull, t, c);
+      if (!(d > T(0))) {
+        okc = 0;
+        if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
+        break;
+      }
+      const T Lcc = leaf_sqrt(d);
+      if (i == c) { Ls[c][c] = Lcc; inv[c] = T(1) / Lcc; }
+      else if (i > c && i < w) Ls[i][c] = t / Lcc;
+      __syncwarp();
+    }
+    if (lane == 0) bad = !okc;
+  }
+  // rows below (all warps; warp 0 after the block): loads in flight during the Crout
+  if (r < m) {
+#pragma unroll
+    for (int k = 0; k < W; ++k) x[k] = (k < w) ? __ldcg(src + r + (int64_t)k * lds) : T(0);
+  }
+  __syncthreads();
+  if (bad) return;
+  if (last_reader(fail + 1)) {
+    for (int idx = tid; idx < w * w; idx += kLeafT) {
+      const int i = idx % w, k = idx / w;
+      if (k <= i) dst[i + (int64_t)k * ldd] = Ls[i][k];
+    }
+  }
+  if (r >= m) return;
+#pragma unroll
+  for (int c = 0; c < W; ++c) {
+    T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
+#pragma unroll
+    for (int k = 0; k < c; ++k) {
+      if ((k & 3) == 0) a0 = fma(-x[k], Ls[c][k], a0);
+      else if ((k & 3) == 1) a1 = fma(-x[k], Ls[c][k], a1);
+      else if ((k & 3) == 2) a2 = fma(-x[k], Ls[c][k], a2);
+      else a3 = fma(-x[k], Ls[c][k], a3);
+    }
+    x[c] = ((a0 + a1) + (a2 + a3)) * inv[c];
+  }
+#pragma unroll
+  for (int k = 0; k < W; ++k)
+    if (k < w) dst[r + (int64_t)k * ldd] = x[k];
+}
+
+static bool leaf_warp_on() {
+  static int on = [] { const char* e = getenv("SF_LEAF_WARP"); return e ? atoi(e) : 1; }();
+  return on != 0;
+}
+
 template <typename T>
 cudaError_t chol_leaf(int64_t m, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
                       long long* fail, cudaStream_t st) {
   if (w <= 0 || m <= 0) return cudaSuccess;
   const int64_t below = m - w;
   const int grid = below > 0 ? (int)((below + kLeafT - 1) / kLeafT) : 1;
+  if (leaf_warp_on()) {
+    if (w <= 16) chol_leaf_warp_kernel<T, 16><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+    else if (w <= 32) chol_leaf_warp_kernel<T, 32><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+    else return cudaErrorInvalidValue;
+    count_launch();
+    return cudaGetLastError();
+  }
   if (w <= 16) chol_leaf_kernel<T, 16><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
   else if (w <= 32) chol_leaf_kernel<T, 32><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
   else return cudaErrorInvalidValue;

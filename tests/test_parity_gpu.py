@@ -357,3 +357,27 @@ def test_graph_replay(kind):
         else:
             check_qr(A, s, F, host(o2), Qo, Ro)
     assert counts[0] > 10 and counts[1:] == [counts[0]] * 3, counts
+
+
+@pytest.mark.parametrize("n,s,dtype", [(1, 1, 0), (300, 64, 0), (257, 100, 0), (1000, 128, 1), (513, 512, 0)])
+def test_chol_host_lower_panels(n, s, dtype):
+    """chol_factor_host: lower triangle copied panel by panel, each panel of L returned as
+    soon as it is final (overlapped D2H); out of place the strict upper is unspecified
+    except outside the diagonal blocks (untouched); in place it keeps A's values."""
+    A = synth.gen_numpy("spd_scaled", n, seed=n)
+    if dtype == 1:
+        A = A.astype(np.float32).astype(np.float64)
+    npdt = np.float64 if dtype == 0 else np.float32
+    hA = np.asfortranarray(A.astype(npdt))
+    hL = np.asfortranarray(np.full((n, n), 7.0, dtype=npdt))
+    out, info = sf.chol_host(hA, s, hL, dtype=dtype)
+    assert info == 0
+    Lo, _ = oracle.chol(A, s)
+    assert synth.r2_error(np.tril(out).astype(np.float64), Lo) <= (TOL64 if dtype == 0 else 2e-4)
+    far = np.triu(np.ones((n, n), bool), 1) & ((np.arange(n)[:, None] // s) != (np.arange(n)[None, :] // s))
+    assert np.all(out[far] == 7.0), "entries above the diagonal blocks must be untouched"
+    assert np.array_equal(hA, A.astype(npdt)), "input modified"
+    # in place: upper triangle keeps A's values
+    hB = np.asfortranarray(A.astype(npdt))
+    out2, info2 = sf.chol_host(hB, s, dtype=dtype)
+    assert info2 == 0 and np.array_equal(np.tril(out2), np.tril(out)) and np.array_equal(np.triu(out2, 1), np.triu(A.astype(npdt), 1))
