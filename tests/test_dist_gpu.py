@@ -197,3 +197,33 @@ def test_chol_dist_fp32_planted():
     Lx = synth.planted_chol(n, seed=5)
     (Lg,), info = run_dist("chol", Lx @ Lx.T, s, 3, dtype=sf.SF_F32)
     assert info == 0 and np.array_equal(np.tril(Lg), Lx)
+
+
+def test_qr_dist_cfg4_shape_sampled():
+    """BASELINE configs[3] (QR n=8192, s=128) on G=2 loopback ranks: the first K columns of Q
+    and rows of R against the restricted oracle, orthogonality and residual of the whole."""
+    n, s, G, K = 8192, 128, 2, 256
+    A = synth.gen_numpy("gaussian", n, seed=0)
+    (Qg, Rg), info = run_dist("qr", A, s, G)
+    assert info == 0
+    Qo, Ro, io, _ = oracle.qr(A, s, kcols=K)
+    assert io == 0
+    assert synth.r2_error(Qg[:, :K], Qo[:, :K]) <= TOL64
+    assert synth.r2_error(Rg[:K, :], Ro[:K, :]) <= TOL64
+    Qt = torch.from_numpy(Qg).cuda(); At = torch.from_numpy(A).cuda(); Rt = torch.from_numpy(Rg).cuda()
+    assert float((Qt.mT @ Qt - torch.eye(n, device="cuda", dtype=torch.float64)).norm()) <= 1e-12 * n
+    assert float((At - Qt @ Rt).norm() / At.norm()) <= 1e-13 * n
+    assert np.all(np.tril(Rg, -1) == 0)
+
+
+def test_lu_dist_cfg2_shape():
+    """BASELINE configs[1] (LU n=4096, s=64) on G=2 and G=4 loopback ranks against the
+    oracle."""
+    n, s = 4096, 64
+    A = synth.gen_numpy("diag_dominant", n, seed=0)
+    Lo, Uo, io = oracle.lu(A, s)
+    for G in (2, 4):
+        (F,), info = run_dist("lu", A, s, G)
+        assert info == 0
+        Lg, Ug = np.tril(F), np.triu(F, 1) + np.eye(n)
+        assert synth.r2_error(Lg, Lo) <= TOL64 and synth.r2_error(Ug, Uo) <= TOL64
