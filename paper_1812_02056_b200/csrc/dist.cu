@@ -529,7 +529,7 @@ static int qr_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, vo
   const Cyclic cy(n, s, comm->nranks);
   const int64_t wmax = qr_mgs_max_width(n, (int)sizeof(T));
   const int64_t wcap = s < wmax ? s : wmax;
-  const size_t mgs_elems = qr_mgs_work_elems(n, (int)wcap) + 64;
+  const size_t mgs_elems = qr_mgs_work_elems(n, (int)wcap, (int)sizeof(T)) + 64;
   const int64_t cw_elems = s * n;
   int64_t split_elems = 1;
   for (int64_t p = 0; p + 1 < cy.P; ++p) {
@@ -632,8 +632,18 @@ static int qr_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, vo
       fl += 2.0 * n * ((double)wq * qs + 0.5 * (double)wq * (wq + 1));
     }
     ProfScope pr(2, fl, x.st.mn);
-    GemmF64 p64{0, n, n, nullptr, n, nullptr, ld, nullptr, 0, nullptr, ld, 1.0, 0, 1, nullptr, x.fail};
-    SF_CUDA(gemm_f64_grouped(p64, gs.data(), (int)gs.size(), 1, 1, kMaskUpper, x.st.mn));
+    if (std::is_same<T, double>::value) {
+      GemmF64 p64{0, n, n, nullptr, n, nullptr, ld, nullptr, 0, nullptr, ld, 1.0, 0, 1, nullptr, x.fail};
+      SF_CUDA(gemm_f64_grouped(p64, gs.data(), (int)gs.size(), 1, 1, kMaskUpper, x.st.mn));
+    } else {
+      for (int64_t j = 0; j * s < nloc; ++j) {   // fp32: one 3xTF32 launch per local panel
+        const int64_t q = cy.panel_of(j, x.r), qs = q * s, wq = cy.width(q);
+        Gemm<T> g{qs + wq, wq, n, x.qfull, n, 1, x.A + j * s * ld, ld, 1, nullptr, 0, x.R + j * s * ld, ld,
+                  1.0, 0, kMaskUpper, 1, nullptr, x.fail};
+        g.off = qs;
+        SF_CUDA(run_gemm(g, x.st.mn));
+      }
+    }
   }
   return finish_dist<T>(comm, rk, caller);
 }
@@ -724,7 +734,7 @@ int lu_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* const*
                    int64_t ld_local, int64_t* const* d_info, void* stream) {
   int rc = check_dist(comm, n, s, dtype, dA_local, dLU_local, ld_local, d_info);
   if (rc) return rc;
-  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp32 LU not implemented (SURVEY.md §8 f4)");
+  if (dtype == SF_F32) return lu_dist_run<float>(comm, n, s, dA_local, dLU_local, ld_local, d_info, (cudaStream_t)stream);
   return lu_dist_run<double>(comm, n, s, dA_local, dLU_local, ld_local, d_info, (cudaStream_t)stream);
 }
 
@@ -737,7 +747,8 @@ int qr_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* const*
     if (sf_local_cols(n, s, comm->nranks, comm->local_rank(i)) > 0 &&
         (!dR_local[i] || dR_local[i] == dQ_local[i] || dR_local[i] == dA_local[i] || dQ_local[i] == dA_local[i]))
       return fail_with(SF_EINVAL, "qr_factor_dist outputs must not alias");
-  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp32 QR not implemented (SURVEY.md §8 f4)");
+  if (dtype == SF_F32)
+    return qr_dist_run<float>(comm, n, s, dA_local, dQ_local, dR_local, ld_local, d_info, (cudaStream_t)stream);
   return qr_dist_run<double>(comm, n, s, dA_local, dQ_local, dR_local, ld_local, d_info, (cudaStream_t)stream);
 }
 

@@ -241,7 +241,7 @@ static int qr_run(int64_t n, int64_t s, const T* A, int64_t lda, T* Q, int64_t l
                   cudaStream_t st) {
   const int64_t wmax = qr_mgs_max_width(n, (int)sizeof(T));
   const int64_t wcap = s < wmax ? s : wmax;
-  const size_t mgs_elems = qr_mgs_work_elems(n, (int)wcap) + 64;
+  const size_t mgs_elems = qr_mgs_work_elems(n, (int)wcap, (int)sizeof(T)) + 64;
   const int64_t cw_elems = s * n;
   int64_t split_elems = 0;
   for (int64_t z = 0; z < n; z += s) {
@@ -437,10 +437,12 @@ int lu_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void
   int rc = check_common(n, s, dtype, dA, lda, dLU, ldlu);
   if (rc) return rc;
   if (!d_info) return fail_with(SF_EINVAL, "null d_info");
-  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp32 LU not implemented (SURVEY.md §8 f4)");
   cudaStream_t st = (cudaStream_t)stream;
   const GraphKey key{1, dtype, n, s, lda, ldlu, 0, dA, dLU, nullptr, d_info, st};
-  return run_graph(key, st, [&]() { return lu_run<double>(n, s, (const double*)dA, lda, (double*)dLU, ldlu, d_info, st); });
+  return run_graph(key, st, [&]() {
+    if (dtype == SF_F32) return lu_run<float>(n, s, (const float*)dA, lda, (float*)dLU, ldlu, d_info, st);
+    return lu_run<double>(n, s, (const double*)dA, lda, (double*)dLU, ldlu, d_info, st);
+  });
 }
 
 int qr_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dQ, int64_t ldq, void* dR,
@@ -451,10 +453,10 @@ int qr_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void
   if (rc) return rc;
   if (dA == dQ || dA == dR || dQ == dR) return fail_with(SF_EINVAL, "qr_factor outputs must not alias");
   if (!d_info) return fail_with(SF_EINVAL, "null d_info");
-  if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp32 QR not implemented (SURVEY.md §8 f4)");
   cudaStream_t st = (cudaStream_t)stream;
   const GraphKey key{2, dtype, n, s, lda, ldq, ldr, dA, dQ, dR, d_info, st};
   return run_graph(key, st, [&]() {
+    if (dtype == SF_F32) return qr_run<float>(n, s, (const float*)dA, lda, (float*)dQ, ldq, (float*)dR, ldr, d_info, st);
     return qr_run<double>(n, s, (const double*)dA, lda, (double*)dQ, ldq, (double*)dR, ldr, d_info, st);
   });
 }
@@ -466,7 +468,6 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
   if (lda < n || ld1 < n || (kind == 2 && ld2 < n)) return fail_with(SF_EINVAL, "leading dimension < n");
   if (s < 1 || s > n) return fail_with(SF_EINVAL, "step s=%lld outside [1, n=%lld]", (long long)s, (long long)n);
   if (dtype != SF_F64 && dtype != SF_F32) return fail_with(SF_EINVAL, "unknown dtype %d", dtype);
-  if (kind != 0 && dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp32 LU/QR not implemented (SURVEY.md §8 f4)");
   const size_t elt = dtype == SF_F64 ? 8 : 4;
   const size_t bytes = elt * (size_t)n * (size_t)n;
   static cudaStream_t streams[16] = {};
@@ -643,7 +644,7 @@ int sf_qr_panel(int64_t n, int64_t w, int dtype, void* dV, int64_t ld, int64_t c
   const int64_t wcap = w < wmax ? w : wmax;
   const int sp = splitk_for(w, wcap, n);
   const int64_t split_elems = (int64_t)sp * w * wcap;
-  const size_t mgs = qr_mgs_work_elems(n, (int)wcap) + 64;
+  const size_t mgs = qr_mgs_work_elems(n, (int)wcap, 8) + 64;
   Workspace ws;
   SF_CUDA(ws.init(8 * (mgs + w * wcap + split_elems) + 4096, st));
   long long* fail = ws.take<long long>(2);   // [0] first failed column, [1] leaf counter

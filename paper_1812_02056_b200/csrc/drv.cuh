@@ -158,14 +158,44 @@ struct Gemm {
   double alpha; int beta; int mask;
   int splits; T* work;
   const long long* fail;
+  int64_t off = 0;   // mask diagonal offset (lower: i >= j + off, upper: i <= j + off)
 };
 
 inline cudaError_t run_gemm(const Gemm<double>& g, cudaStream_t st) {
   GemmF64 p{g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, g.Cin, g.ldcin, g.C, g.ldc,
             g.alpha, g.beta, g.splits, g.work, g.fail};
+  p.off = g.off;
   return gemm_f64(p, g.ak, g.bk, g.mask, st);
 }
-inline cudaError_t run_gemm(const Gemm<float>&, cudaStream_t) { return cudaErrorNotSupported; }
+// fp32: split op(A) and op(B) once into K-major hi/lo copies (stream-ordered scratch), then
+// ONE 3xTF32 tcgen05 GEMM (gemm_tf32.cu); split-K requests are served unsplit.
+inline cudaError_t run_gemm(const Gemm<float>& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+  if (g.K <= 0) {
+    if (g.beta && g.Cin == g.C && g.ldcin == g.ldc) return cudaSuccess;
+    return cudaErrorNotSupported;
+  }
+  const int64_t ldk = (g.K + 3) / 4 * 4;
+  float* buf = nullptr;
+  const size_t elems = 2 * (size_t)(g.M + g.N) * ldk;
+  cudaError_t e = cudaMallocAsync((void**)&buf, elems * sizeof(float) + 64, st);
+  if (e != cudaSuccess) return e;
+  float* Ah = buf; float* Al = Ah + (size_t)g.M * ldk;
+  float* Bh = Al + (size_t)g.M * ldk; float* Bl = Bh + (size_t)g.N * ldk;
+  // op(A)(i,k): ak ? A[k + i*lda] (K-major) : A[i + k*lda] (column-major)
+  e = g.ak ? split_tf32_kmajor(g.M, g.K, g.A, g.lda, Ah, Al, ldk, st) : split_tf32(g.M, g.K, g.A, g.lda, Ah, Al, ldk, st);
+  // op(B)(k,j): bk ? B[k + j*ldb] (row j of B^T is K-major) : B[j + k*ldb]
+  if (e == cudaSuccess)
+    e = g.bk ? split_tf32_kmajor(g.N, g.K, g.B, g.ldb, Bh, Bl, ldk, st) : split_tf32(g.N, g.K, g.B, g.ldb, Bh, Bl, ldk, st);
+  if (e == cudaSuccess) {
+    Tf32Gemm t{g.M, g.N, g.K, Ah, Al, ldk, Bh, Bl, ldk, g.Cin, g.ldcin, g.C, g.ldc, g.mask, g.off, g.fail};
+    t.alpha = (float)g.alpha;
+    t.beta = g.beta;
+    e = gemm_tf32x3(t, st);
+  }
+  cudaError_t e2 = cudaFreeAsync(buf, st);
+  return e != cudaSuccess ? e : e2;
+}
 
 // C -= op(A) op(B) with C read from Cin (may differ) : common "subtract" form
 template <typename T>

@@ -138,6 +138,8 @@ struct Tf32Params {
   int64_t off;              // mask diagonal offset
   int mask;
   const long long* fail;
+  float alpha;              // C = (beta ? Cin : 0) + alpha * acc
+  int beta;
 };
 
 // One 128 x BN tile per CTA, two CTAs per SM (96 KB of stages each): one CTA's epilogue
@@ -182,7 +184,7 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constan
     // warm L2 with this tile's C columns for the epilogue's read-modify-write
     for (int u = lane - 1; u < BN * 4; u += 31) {
       const int64_t j = j0 + (u >> 2), i = i0 + (u & 3) * 32;
-      if (j < p.N && i < p.M) prefetch_l2(p.Cin + i + j * p.ldcin);
+      if (p.beta && j < p.N && i < p.M) prefetch_l2(p.Cin + i + j * p.ldcin);
     }
   }
   if (warp == 1) {
@@ -246,13 +248,13 @@ gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constan
         for (int u = 0; u < 32; ++u) {
           const int64_t j = j0 + c + u;
           const bool in = j < p.N && (p.mask == kMaskNone || (p.mask == kMaskLower ? i >= j + p.off : i <= j + p.off));
-          cin[u] = in ? __ldcg(p.Cin + i + j * p.ldcin) : 0.f;
+          cin[u] = (in && p.beta) ? __ldcg(p.Cin + i + j * p.ldcin) : 0.f;
         }
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
           const int64_t j = j0 + c + u;
           const bool in = j < p.N && (p.mask == kMaskNone || (p.mask == kMaskLower ? i >= j + p.off : i <= j + p.off));
-          if (in) __stcg(p.C + i + j * p.ldc, cin[u] - v[u]);
+          if (in) __stcg(p.C + i + j * p.ldc, fmaf(p.alpha, v[u], cin[u]));
         }
       }
     }
@@ -373,7 +375,7 @@ gemm_tf32x3_pair_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_co
   const int64_t jl = j0 + BN - 1;
   const bool inside = (r0 + HALF <= p.M) && (j0 + BN <= p.N) &&
                       (p.mask == kMaskNone || (p.mask == kMaskLower ? r0 >= jl + p.off : r0 + HALF - 1 <= j0 + p.off));
-  const bool bulk = vecC && inside && !skip;
+  const bool bulk = vecC && inside && !skip && p.beta;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -384,7 +386,7 @@ gemm_tf32x3_pair_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_co
   } else if (warp == 0) {
     for (int u = lane - 1; u < BN * 4; u += 31) {   // warm L2 with this CTA's C rows
       const int64_t j = j0 + (u >> 2), i = r0 + (u & 3) * 32;
-      if (j < p.N && i < p.M) prefetch_l2(p.Cin + i + j * p.ldcin);
+      if (p.beta && j < p.N && i < p.M) prefetch_l2(p.Cin + i + j * p.ldcin);
     }
   }
   if (warp == 1) {
@@ -460,7 +462,7 @@ gemm_tf32x3_pair_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_co
 #pragma unroll
           for (int u = 0; u < 32; ++u) {
             const int64_t j = j0 + ch * ECOLS + c + u;
-            __stcg(p.C + i + j * p.ldc, src[(c + u) * HALF + row] - v[u]);
+            __stcg(p.C + i + j * p.ldc, fmaf(p.alpha, v[u], src[(c + u) * HALF + row]));
           }
         }
         epi_bar_sync();                     // all four epilogue warps are done with slot ch % 3
@@ -480,13 +482,13 @@ gemm_tf32x3_pair_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_co
           for (int u = 0; u < 32; ++u) {
             const int64_t j = j0 + c + u;
             const bool in = j < p.N && (p.mask == kMaskNone || (p.mask == kMaskLower ? i >= j + p.off : i <= j + p.off));
-            cin[u] = in ? __ldcg(p.Cin + i + j * p.ldcin) : 0.f;
+            cin[u] = (in && p.beta) ? __ldcg(p.Cin + i + j * p.ldcin) : 0.f;
           }
 #pragma unroll
           for (int u = 0; u < 32; ++u) {
             const int64_t j = j0 + c + u;
             const bool in = j < p.N && (p.mask == kMaskNone || (p.mask == kMaskLower ? i >= j + p.off : i <= j + p.off));
-            if (in) __stcg(p.C + i + j * p.ldc, cin[u] - v[u]);
+            if (in) __stcg(p.C + i + j * p.ldc, fmaf(p.alpha, v[u], cin[u]));
           }
         }
       }
@@ -540,6 +542,28 @@ cudaError_t split_tf32(int64_t m, int64_t k, const float* X, int64_t ld, float* 
   return cudaGetLastError();
 }
 
+__global__ void split_tf32_kmajor_kernel(int64_t m, int64_t k, const float* __restrict__ X, int64_t ld,
+                                         float* __restrict__ H, float* __restrict__ L, int64_t ldk) {
+  const int64_t total = m * k;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / k, kk = t % k;
+    const float x = __ldcg(X + i * ld + kk);
+    const float hi = rna_tf32(x);
+    H[i * ldk + kk] = hi;
+    L[i * ldk + kk] = rna_tf32(x - hi);
+  }
+}
+
+cudaError_t split_tf32_kmajor(int64_t m, int64_t k, const float* X, int64_t ld, float* H, float* L, int64_t ldk,
+                              cudaStream_t st) {
+  if (m <= 0 || k <= 0) return cudaSuccess;
+  int64_t blocks = (m * k + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  split_tf32_kmajor_kernel<<<(unsigned)blocks, 256, 0, st>>>(m, k, X, ld, H, L, ldk);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
@@ -589,7 +613,7 @@ static cudaError_t launch_bn(const Tf32Gemm& g, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  Tf32Params p{g.M, g.N, g.K, g.Cin, g.ldcin, g.C, g.ldc, g.off, g.mask, g.fail};
+  Tf32Params p{g.M, g.N, g.K, g.Cin, g.ldcin, g.C, g.ldc, g.off, g.mask, g.fail, g.alpha, g.beta};
   gemm_tf32x3_kernel<BN><<<ntiles, THREADS, C_::SMEM, st>>>(mAh, mAl, mBh, mBl, p);
   count_launch();
   return cudaGetLastError();
@@ -612,9 +636,9 @@ static cudaError_t launch_pair(const Tf32Gemm& g, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  Tf32Params p{g.M, g.N, g.K, g.Cin, g.ldcin, g.C, g.ldc, g.off, g.mask, g.fail};
+  Tf32Params p{g.M, g.N, g.K, g.Cin, g.ldcin, g.C, g.ldc, g.off, g.mask, g.fail, g.alpha, g.beta};
   static int bulk_on = [] { const char* e = getenv("SF_TF32_BULKEPI"); return e ? atoi(e) : 1; }();
-  const int vecC = bulk_on && (g.ldc % 4) == 0 && (g.ldcin % 4) == 0 && ((uintptr_t)g.Cin % 16) == 0 &&
+  const int vecC = bulk_on && g.beta && (g.ldc % 4) == 0 && (g.ldcin % 4) == 0 && ((uintptr_t)g.Cin % 16) == 0 &&
                    ((uintptr_t)g.C % 16) == 0;
   gemm_tf32x3_pair_kernel<<<2 * ntiles, t32::THREADS, SMEM, st>>>(mAh, mAl, mBh, mBl, p, vecC);
   count_launch();

@@ -58,11 +58,16 @@ struct Tf32Gemm {
   float* C; int64_t ldc;
   int mask; int64_t off;
   const long long* fail;
+  float alpha = -1.f;   // C = (beta ? Cin : 0) + alpha * A B^T
+  int beta = 1;
 };
 cudaError_t gemm_tf32x3(const Tf32Gemm& g, cudaStream_t st);
 // column-major X (m x k, ld) -> K-major hi/lo split (row i at H + i*ldk)
 cudaError_t split_tf32(int64_t m, int64_t k, const float* X, int64_t ld, float* H, float* L, int64_t ldk,
                        cudaStream_t st);
+// K-major X (row i: k contiguous at X + i*ld) -> K-major hi/lo split (no transpose)
+cudaError_t split_tf32_kmajor(int64_t m, int64_t k, const float* X, int64_t ld, float* H, float* L, int64_t ldk,
+                              cudaStream_t st);
 
 // ---------------------------------------------------------------- panels (templated T)
 // Cholesky leaf (Alg. 1 inner loops) on columns [0,w) of the m x w block
@@ -87,7 +92,7 @@ cudaError_t lu_usolve_leaf(int64_t ncols, int w, const T* l11, int64_t ldl, cons
 template <typename T>
 cudaError_t qr_mgs_panel(int64_t n, int w, const T* src, int64_t lds, T* dst, int64_t ldd,
                          int64_t col0, const T* tol, T* work, long long* fail, cudaStream_t st);
-size_t qr_mgs_work_elems(int64_t n, int w);
+size_t qr_mgs_work_elems(int64_t n, int w, int elt);   // in units of the element type
 int qr_mgs_max_width(int64_t n, int elt);   // widest panel the smem-resident MGS kernel takes
 
 // utilities

@@ -55,9 +55,10 @@ static MgsGeom mgs_geom(int64_t n, int w, int elt) {
   return g;
 }
 
-size_t qr_mgs_work_elems(int64_t n, int w) {
-  MgsGeom g = mgs_geom(n, w, 8);
-  return (size_t)g.G + 2 * (size_t)g.G * (size_t)w + 2;   // flags[2][G] + partials[2][w][G]
+size_t qr_mgs_work_elems(int64_t n, int w, int elt) {
+  MgsGeom g = mgs_geom(n, w, elt);
+  // flags[2][G] (int) + partials[2][w][G] (T), in units of T
+  return (2 * (size_t)g.G * sizeof(int) + elt - 1) / elt + 2 * (size_t)g.G * (size_t)w + 2;
 }
 
 // Inter-CTA exchange for a cooperative (co-resident) grid, without atomics: CTA g publishes

@@ -38,7 +38,7 @@ def run_dist(kind, A, s, G, comm=None, inplace=False, dtype=None):
         if kind == "qr":
             Q = [torch.full_like(a, 5.0) for a in Aloc]
             R = [torch.full_like(a, 3.0) for a in Aloc]
-            sf.qr_dist(comm, n, s, Aloc, Q, R, n, info)
+            sf.qr_dist(comm, n, s, Aloc, Q, R, n, info, dtype=sf.SF_F64 if dtype is None else dtype)
             torch.cuda.synchronize()
             for a, b in zip(Aloc, Aref):
                 assert torch.equal(a, b), "QR input modified"
@@ -227,3 +227,20 @@ def test_lu_dist_cfg2_shape():
         assert info == 0
         Lg, Ug = np.tril(F), np.triu(F, 1) + np.eye(n)
         assert synth.r2_error(Lg, Lo) <= TOL64 and synth.r2_error(Ug, Uo) <= TOL64
+
+
+@pytest.mark.parametrize("G", [1, 2, 3])
+def test_lu_qr_dist_fp32(G):
+    """fp32 (3xTF32) distributed LU and QR: planted integer factors come out exactly, and a
+    random LU matches the fp64 oracle on the fp32-rounded input (R2 <= 2e-4)."""
+    n, s = 512, 64
+    Lx, Ux = synth.planted_lu(n, seed=11)
+    (F,), info = run_dist("lu", Lx @ Ux, s, G, dtype=sf.SF_F32)
+    assert info == 0 and np.array_equal(np.tril(F), Lx) and np.array_equal(np.triu(F, 1) + np.eye(n), Ux)
+    A = synth.gen_numpy("diag_dominant", 300, seed=G).astype(np.float32).astype(np.float64)
+    (F,), info = run_dist("lu", A, 64, G, dtype=sf.SF_F32)
+    Lo, Uo, _ = oracle.lu(A, 64)
+    assert info == 0 and synth.r2_error(np.tril(F), Lo) <= 2e-4 and synth.r2_error(np.triu(F, 1) + np.eye(300), Uo) <= 2e-4
+    Qx, Rx = synth.planted_qr(256, seed=5)
+    (Qg, Rg), info = run_dist("qr", Qx @ Rx, 64, G, dtype=sf.SF_F32)
+    assert info == 0 and np.array_equal(Qg, Qx) and np.array_equal(Rg, Rx)

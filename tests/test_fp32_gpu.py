@@ -115,3 +115,85 @@ def test_chol32_cfg5_shape_sampled():
     x = torch.randn(n, 4, device="cuda", dtype=torch.float64, generator=g)
     r = (Ar @ x - Ll @ (Ll.mT @ x)).norm() / (Ar @ x).norm()
     assert float(r) <= 1e-5 * n
+
+
+# ------------------------------------------------------------------ fp32 LU / QR
+
+def run_lu32(A, s):
+    n = A.shape[0]
+    dA = torch.from_numpy(np.ascontiguousarray(np.asarray(A, np.float32).T)).cuda()
+    out = torch.full_like(dA, 7.0)
+    info = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sf.lu_colmajor(n, s, dA, n, out, n, info, dtype=sf.SF_F32)
+    torch.cuda.synchronize()
+    F = host(out)
+    return np.tril(F), np.triu(F, 1) + np.eye(n), int(info.item())
+
+
+def run_qr32(A, s):
+    n = A.shape[0]
+    dA = torch.from_numpy(np.ascontiguousarray(np.asarray(A, np.float32).T)).cuda()
+    Q = torch.empty_like(dA); R = torch.full_like(dA, 3.0)
+    info = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sf.qr_colmajor(n, s, dA, n, Q, n, R, n, info, dtype=sf.SF_F32)
+    torch.cuda.synchronize()
+    return host(Q), host(R), int(info.item())
+
+
+@pytest.mark.parametrize("n,s", [(1, 1), (33, 16), (130, 32), (300, 64), (1000, 168), (2048, 512), (4096, 64)])
+def test_lu32_vs_oracle(n, s):
+    A = synth.gen_numpy("diag_dominant", n, seed=n + s).astype(np.float32).astype(np.float64)
+    Lg, Ug, info = run_lu32(A, s)
+    assert info == 0
+    Lo, Uo, io = oracle.lu(A, s)
+    assert io == 0
+    assert synth.r2_error(Lg, Lo) <= TOL32 and synth.r2_error(Ug, Uo) <= TOL32
+    assert synth.rel_residual(A, Lg, Ug) <= 1e-5 * n
+
+
+@pytest.mark.parametrize("n,s", [(700, 64), (1024, 128)])
+def test_lu32_planted_exact(n, s):
+    Lx, Ux = synth.planted_lu(n, seed=n + s)
+    Lg, Ug, info = run_lu32(Lx @ Ux, s)
+    assert info == 0 and np.array_equal(Lg, Lx) and np.array_equal(Ug, Ux)
+
+
+@pytest.mark.parametrize("n,s", [(4, 2), (130, 32), (300, 64), (1024, 128)])
+def test_qr32_vs_oracle(n, s):
+    """fp32 QR against the fp64 oracle on the fp32-rounded input (reading P10):
+    forward errors within the classical bounds — per column of Q
+    ||dq_j|| <= (100 kappa_j + 3n + 2) u32 (kappa_j: of the head block for columns [0, n-2s),
+    of A for the tail; 3n + 2: the worst-case fp32 dot product over the 3xTF32 K' = 3n,
+    since the tensor core's fp32 accumulation is not round-to-nearest), per row of R the
+    same times ||A||_2 sqrt(n); residual <= 1e-5 n (the north star's fp32 residual bar);
+    orthogonality <= max(1e-5 n, 100 u32 kappa(A)) (MGS loses orthogonality ~ u kappa).  The floored elementwise R2 is dominated by Q's tiny entries (a plain
+    fp32 MGS of the n = 130 case already has head R2 = 1.0e-4), so it is not used here."""
+    A = synth.gen_numpy("gaussian", n, seed=n + s).astype(np.float32).astype(np.float64)
+    Qg, Rg, info = run_qr32(A, s)
+    assert info == 0
+    Qo, Ro, io, _ = oracle.qr(A, s)
+    assert io == 0
+    u32 = 2.0 ** -24
+    head = max(0, n - 2 * s)
+    k_all = np.linalg.cond(A)
+    k_head = np.linalg.cond(A[:, :head]) if head else k_all
+    dq = np.linalg.norm(Qg - Qo, axis=0)
+    dr = np.linalg.norm(Rg - Ro, axis=1)
+    nA = np.linalg.norm(A, 2) * np.sqrt(n)
+    g = (3 * n + 2) * u32
+    if head:
+        assert np.max(dq[:head]) <= 100 * u32 * k_head + g, (np.max(dq[:head]), k_head)
+        assert np.max(dr[:head]) <= (100 * u32 * k_head + g) * nA, (np.max(dr[:head]), k_head)
+    assert np.max(dq) <= 100 * u32 * k_all + g
+    assert np.max(dr) <= (100 * u32 * k_all + g) * nA
+    assert np.all(np.tril(Rg, -1) == 0)
+    # MGS loses orthogonality like c u kappa(A) (Bjorck), fp32: u = 2^-24
+    assert synth.orthogonality(Qg) <= max(1e-5 * n, 100 * u32 * k_all)
+    assert synth.rel_residual(A, Qg, Rg) <= 1e-5 * n
+
+
+def test_qr32_planted_exact():
+    n, s = 1024, 128
+    Qx, Rx = synth.planted_qr(n, seed=3)
+    Qg, Rg, info = run_qr32(Qx @ Rx, s)
+    assert info == 0 and np.array_equal(Qg, Qx) and np.array_equal(Rg, Rx)
