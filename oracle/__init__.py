@@ -46,6 +46,13 @@ def _load():
         lib.orc_lu.argtypes = [i64, i64, i64, p, i64, p, i64, p, i64, dbl]
         lib.orc_qr.restype = i64
         lib.orc_qr.argtypes = [i64, i64, i64, p, i64, p, i64, p, i64, dbl, ctypes.POINTER(dbl)]
+        pi = ctypes.POINTER(ctypes.c_int64)
+        lib.orc_chol_steps.restype = i64
+        lib.orc_chol_steps.argtypes = [i64, i64, pi, i64, p, i64, p, i64]
+        lib.orc_lu_steps.restype = i64
+        lib.orc_lu_steps.argtypes = [i64, i64, pi, i64, p, i64, p, i64, p, i64, dbl]
+        lib.orc_qr_steps.restype = i64
+        lib.orc_qr_steps.argtypes = [i64, i64, pi, i64, p, i64, p, i64, p, i64, dbl, ctypes.POINTER(dbl)]
         lib.orc_flush_count.restype = i64
         lib.orc_flush_count.argtypes = [i64, i64]
         lib.orc_frobenius.restype = dbl
@@ -63,8 +70,20 @@ def _colmajor(A):
 
 
 def _check_s(n, s):
+    if isinstance(s, (list, tuple, np.ndarray)):
+        if len(s) == 0 or min(int(x) for x in s) < 1:
+            raise ValueError("step sequence must be non-empty with steps >= 1")
+        return
     if not (1 <= s <= n):
         raise ValueError(f"step s={s} outside [1, n={n}]")
+
+
+def _steps(s):
+    """A step sequence (reading R11) as a ctypes int64 array, or None."""
+    if not isinstance(s, (list, tuple, np.ndarray)):
+        return None
+    arr = (ctypes.c_int64 * len(s))(*[int(x) for x in s])
+    return arr
 
 
 def set_threads(n):
@@ -83,12 +102,18 @@ def flush_count(n, s):
 def chol(A, s, kcols=None):
     """Algorithm 1. Returns (L, info); info 0 or 1-based failing column.
 
+    s: the step (int), or a sequence of steps s_0, s_1, ... (reading R11).
+
     With kcols=K < n, A may be the n x K block of its first K columns; L is then n x K."""
     A = np.asfortranarray(np.asarray(A, dtype=np.float64)); n = A.shape[0]; _check_s(n, s)
     K = n if kcols is None else min(int(kcols), n)
     assert A.shape[1] >= K and (kcols is not None or A.shape[1] == n), "square matrix expected"
     L = np.zeros((n, K), order="F")
-    info = _load().orc_chol(n, s, K, A.ctypes.data, n, L.ctypes.data, n)
+    st = _steps(s)
+    if st is None:
+        info = _load().orc_chol(n, s, K, A.ctypes.data, n, L.ctypes.data, n)
+    else:
+        info = _load().orc_chol_steps(n, len(st), st, K, A.ctypes.data, n, L.ctypes.data, n)
     if K < n and A.shape[1] == n:
         L = np.concatenate([L, np.zeros((n, n - K))], axis=1)
     return L, int(info)
@@ -98,8 +123,13 @@ def lu(A, s, kcols=None, tol=0.0):
     """Algorithm 2, Crout form (U unit upper). Returns (L, U, info)."""
     A = _colmajor(A); n = A.shape[0]; _check_s(n, s)
     L = np.zeros((n, n), order="F"); U = np.zeros((n, n), order="F")
-    info = _load().orc_lu(n, s, n if kcols is None else kcols, A.ctypes.data, n,
-                          L.ctypes.data, n, U.ctypes.data, n, float(tol))
+    st = _steps(s)
+    K = n if kcols is None else kcols
+    if st is None:
+        info = _load().orc_lu(n, s, K, A.ctypes.data, n, L.ctypes.data, n, U.ctypes.data, n, float(tol))
+    else:
+        info = _load().orc_lu_steps(n, len(st), st, K, A.ctypes.data, n, L.ctypes.data, n, U.ctypes.data, n,
+                                    float(tol))
     return L, U, int(info)
 
 
@@ -108,8 +138,14 @@ def qr(A, s, kcols=None, tol=0.0):
     A = _colmajor(A); n = A.shape[0]; _check_s(n, s)
     Q = np.zeros((n, n), order="F"); R = np.zeros((n, n), order="F")
     mass = ctypes.c_double(0.0)
-    info = _load().orc_qr(n, s, n if kcols is None else kcols, A.ctypes.data, n,
-                          Q.ctypes.data, n, R.ctypes.data, n, float(tol), ctypes.byref(mass))
+    st = _steps(s)
+    K = n if kcols is None else kcols
+    if st is None:
+        info = _load().orc_qr(n, s, K, A.ctypes.data, n, Q.ctypes.data, n, R.ctypes.data, n, float(tol),
+                              ctypes.byref(mass))
+    else:
+        info = _load().orc_qr_steps(n, len(st), st, K, A.ctypes.data, n, Q.ctypes.data, n, R.ctypes.data, n,
+                                    float(tol), ctypes.byref(mass))
     return Q, R, int(info), float(mass.value)
 
 

@@ -29,6 +29,9 @@
  *   R4  v/||v|| is an elementwise division; ||v|| = sqrt(sum v_i^2) unscaled.
  *   R5  R := Q^T A is formed in full, the mass of its strict lower part is
  *       reported, then the strict lower part is set to 0.
+ *   R11 variable step ("the s parameter could be varied during the
+ *       execution"): with a step sequence s_0, s_1, ..., panel p flushes when c = z + s_p;
+ *       the *_steps entry points.  A constant sequence is bitwise the fixed-s algorithm.
  *
  * Restricted variants: every routine takes `kcols` (K).  With K = n it is the verbatim
  * algorithm.  With K < n it produces only the first K columns of L (Cholesky), the first
@@ -73,6 +76,23 @@ double orc_frobenius(int64_t n, const double* A, int64_t lda) {
   return sqrt(acc);
 }
 
+/* Step sequence.  The paper fixes one s and notes that "the s parameter could
+ * be varied during the execution": with a sequence s_0, s_1, ... the flush
+ * condition of the current panel is c = z + s_p and p advances at each flush (reading R11).
+ * steps == NULL means the constant s. */
+typedef struct { const int64_t* steps; int64_t nsteps, s, p; } Steps;
+static int64_t step_now(const Steps* st) {
+  if (!st->steps) return st->s;
+  return st->p < st->nsteps ? st->steps[st->p] : st->steps[st->nsteps - 1];
+}
+static void step_next(Steps* st) { st->p++; }
+static int64_t step_max(const Steps* st) {
+  if (!st->steps) return st->s;
+  int64_t m = 1;
+  for (int64_t i = 0; i < st->nsteps; ++i) if (st->steps[i] > m) m = st->steps[i];
+  return m;
+}
+
 /* Number of flushes the schedule of Algorithms 1-3 performs (R1). */
 int64_t orc_flush_count(int64_t n, int64_t s) {
   int64_t z = 0, flushes = 0;
@@ -89,8 +109,8 @@ int64_t orc_flush_count(int64_t n, int64_t s) {
  *   With K < n only the first K columns of A are read and of L written (n x K blocks).
  * Returns info (0 or 1-based failing column).
  */
-int64_t orc_chol(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t lda,
-                 double* L, int64_t ldl) {
+static int64_t chol_core(int64_t n, Steps sp, int64_t kcols, const double* A, int64_t lda,
+                         double* L, int64_t ldl) {
   const int64_t K = min64(kcols, n);
   /* the paper's A (mutated by the flushes); a restricted run only ever touches columns < K,
      so only those are copied (A and L may then be n x K blocks) */
@@ -102,7 +122,7 @@ int64_t orc_chol(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t l
   int64_t info = 0;
   int64_t z = 0;                                             /* z := 1            (:37) */
   for (int64_t c = 0; c < K; ++c) {                          /* for c from 1 to n (:39) */
-    if (c == z + s) {                                        /* if c = z+s        (:41) */
+    if (c == z + step_now(&sp)) {                            /* if c = z+s        (:41) */
       /* R := L[c..n, z..c-1] (:42); S := R R^T (:43); A_ij := A_ij - S (:44-50).
          Columns j >= K of W are never read again in a restricted run. */
 #pragma omp parallel for schedule(dynamic, 16)
@@ -114,6 +134,7 @@ int64_t orc_chol(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t l
         }
       }
       z = c;                                                 /* z := c            (:51) */
+      step_next(&sp);
     }
     double d = AT(W, n, c, c);                               /* L_cc := A_cc      (:53) */
     for (int64_t k = z; k < c; ++k)                          /* (:54-57) */
@@ -132,14 +153,24 @@ int64_t orc_chol(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t l
   return info;
 }
 
+int64_t orc_chol(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t lda, double* L, int64_t ldl) {
+  Steps sp = {NULL, 0, s, 0};
+  return chol_core(n, sp, kcols, A, lda, L, ldl);
+}
+int64_t orc_chol_steps(int64_t n, int64_t nsteps, const int64_t* steps, int64_t kcols, const double* A, int64_t lda,
+                       double* L, int64_t ldl) {
+  Steps sp = {steps, nsteps, steps[0], 0};
+  return chol_core(n, sp, kcols, A, lda, L, ldl);
+}
+
 /*
  * Algorithm 2, "A fast LU decomposition algorithm".  Crout form:
  * L lower with its own diagonal, U unit upper.
  *   L, U: n x n outputs; entries never written stay 0.
  *   tol: R3 threshold 1e-12*||A||_F/n (pass <= 0 to compute it here).
  */
-int64_t orc_lu(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t lda,
-               double* L, int64_t ldl, double* U, int64_t ldu, double tol) {
+static int64_t lu_core(int64_t n, Steps sp, int64_t kcols, const double* A, int64_t lda,
+                       double* L, int64_t ldl, double* U, int64_t ldu, double tol) {
   const int64_t K = min64(kcols, n);
   if (tol <= 0.0) tol = 1e-12 * orc_frobenius(n, A, lda) / (double)n;
   double* W = (double*)malloc(sizeof(double) * (size_t)n * (size_t)n);
@@ -152,7 +183,7 @@ int64_t orc_lu(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t lda
   int64_t info = 0;
   int64_t z = 0;
   for (int64_t c = 0; c < K; ++c) {
-    if (c == z + s) {                                        /* (:91) */
+    if (c == z + step_now(&sp)) {                            /* (:91) */
       /* R_L := L[c..n, z..c-1], R_U := U[z..c-1, c..n], S := R_L R_U, A -= S (:92-103).
          A restricted run only ever reads W[i][j] with j < K (L columns) or i < K (U rows). */
 #pragma omp parallel for schedule(dynamic, 16)
@@ -165,6 +196,7 @@ int64_t orc_lu(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t lda
         }
       }
       z = c;
+      step_next(&sp);
     }
 #pragma omp parallel for schedule(static)
     for (int64_t i = c; i < n; ++i) {                        /* L column (:105-112) */
@@ -185,14 +217,26 @@ int64_t orc_lu(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t lda
   return info;
 }
 
+int64_t orc_lu(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t lda, double* L, int64_t ldl, double* U,
+               int64_t ldu, double tol) {
+  Steps sp = {NULL, 0, s, 0};
+  return lu_core(n, sp, kcols, A, lda, L, ldl, U, ldu, tol);
+}
+int64_t orc_lu_steps(int64_t n, int64_t nsteps, const int64_t* steps, int64_t kcols, const double* A, int64_t lda,
+                     double* L, int64_t ldl, double* U, int64_t ldu, double tol) {
+  Steps sp = {steps, nsteps, steps[0], 0};
+  return lu_core(n, sp, kcols, A, lda, L, ldl, U, ldu, tol);
+}
+
 /*
  * Algorithm 3, "A fast QR decomposition algorithm".
  *   Q: n x n output (orthonormal columns);  R: n x n output (upper; strict lower zeroed, R5)
  *   *lower_mass: ||tril(Q^T A, -1)||_F before zeroing (rows < K only in a restricted run)
  *   tol: R3 threshold (<= 0: computed here).
  */
-int64_t orc_qr(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t lda,
-               double* Q, int64_t ldq, double* R, int64_t ldr, double tol, double* lower_mass) {
+static int64_t qr_core(int64_t n, Steps sp, int64_t kcols, const double* A, int64_t lda,
+                       double* Q, int64_t ldq, double* R, int64_t ldr, double tol, double* lower_mass) {
+  const int64_t s = step_max(&sp);
   const int64_t K = min64(kcols, n);
   if (tol <= 0.0) tol = 1e-12 * orc_frobenius(n, A, lda) / (double)n;
   double* M = (double*)malloc(sizeof(double) * (size_t)n * (size_t)n);  /* M := copy of A */
@@ -207,7 +251,7 @@ int64_t orc_qr(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t lda
   int64_t info = 0;
   int64_t z = 0;
   for (int64_t c = 0; c < K; ++c) {
-    if (c == z + s) {                                        /* (:143) */
+    if (c == z + step_now(&sp)) {                            /* (:143) */
       const int64_t w = c - z;
       const int64_t jend = K;  /* a restricted run never reads M columns >= K */
       /* B_Q := Q[1..n, z..c-1], B_M := M[1..n, c..n] (:145-146); C := B_Q^T B_M (:147) */
@@ -227,6 +271,7 @@ int64_t orc_qr(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t lda
           AT(M, n, i, j) = AT(M, n, i, j) - S;
         }
       z = c;                                                 /* (:156) */
+      step_next(&sp);
     }
     for (int64_t i = 0; i < n; ++i) v[i] = AT(M, n, i, c);   /* v := column c of M (:158) */
     for (int64_t j = z; j < c; ++j) {                        /* (:159-163) */
@@ -256,4 +301,15 @@ int64_t orc_qr(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t lda
   }
   free(M); free(C); free(v);
   return info;
+}
+
+int64_t orc_qr(int64_t n, int64_t s, int64_t kcols, const double* A, int64_t lda, double* Q, int64_t ldq, double* R,
+               int64_t ldr, double tol, double* lower_mass) {
+  Steps sp = {NULL, 0, s, 0};
+  return qr_core(n, sp, kcols, A, lda, Q, ldq, R, ldr, tol, lower_mass);
+}
+int64_t orc_qr_steps(int64_t n, int64_t nsteps, const int64_t* steps, int64_t kcols, const double* A, int64_t lda,
+                     double* Q, int64_t ldq, double* R, int64_t ldr, double tol, double* lower_mass) {
+  Steps sp = {steps, nsteps, steps[0], 0};
+  return qr_core(n, sp, kcols, A, lda, Q, ldq, R, ldr, tol, lower_mass);
 }

@@ -225,3 +225,40 @@ def test_thread_count_does_not_change_bits():
     oracle.set_threads(4); L4, _ = oracle.chol(A, 20)
     oracle.set_threads(0)
     assert np.array_equal(L1, L4)
+
+
+# ------------------------------------------------------------------ variable step (R11)
+
+def test_variable_steps_pins():
+    """PAPER.md:194 ("the s parameter could be varied during the execution"), reading R11:
+    a constant sequence is bitwise the fixed-s algorithm; all-ones is the s = 1 schedule and
+    [n] the s = n one (the textbook pins); the hand-worked 4x4 examples come out exactly for
+    every sequence."""
+    import itertools
+    n = 37
+    A = synth.gen_numpy("paper_spd", n, seed=4)
+    B = synth.gen_numpy("diag_dominant", n, seed=4)
+    C = synth.gen_numpy("gaussian", n, seed=4)
+    for s in (1, 5, 16, n):
+        seq = [s] * (-(-n // s))
+        assert np.array_equal(oracle.chol(A, seq)[0], oracle.chol(A, s)[0])
+        assert all(np.array_equal(x, y) for x, y in zip(oracle.lu(B, seq)[:2], oracle.lu(B, s)[:2]))
+        assert all(np.array_equal(x, y) for x, y in zip(oracle.qr(C, seq)[:2], oracle.qr(C, s)[:2]))
+    seq = [9, 3, 1, 12, 5, 7]
+    L, info = oracle.chol(A, seq)
+    assert info == 0 and np.abs(L @ L.T - A).max() <= 1e-12 * np.abs(A).max() * n
+    L2, U2, info = oracle.lu(B, seq)
+    assert info == 0 and np.abs(L2 @ U2 - B).max() <= 1e-12 * np.abs(B).max() * n
+    Q, R, info, _ = oracle.qr(C, seq)
+    assert info == 0 and np.abs(Q @ R - C).max() <= 1e-11 * np.abs(C).max() * n
+    for seq in itertools.product((1, 2, 3), repeat=3):
+        for ex in GOLD["cholesky"]:
+            Lc, info = oracle.chol(np.array(ex["A"], float), list(seq))
+            assert info == 0 and np.array_equal(Lc, np.array(ex["L"], float)), (seq, ex["cite"])
+        for ex in GOLD["lu"]:
+            Ll, Ul, info = oracle.lu(np.array(ex["A"], float), list(seq))
+            assert info == 0 and np.array_equal(Ll, np.array(ex["L"], float)) and np.array_equal(Ul, np.array(ex["U"], float))
+        for ex in GOLD["qr"]:
+            Qq, Rq, info, _ = oracle.qr(np.array(ex["A"], float), list(seq))
+            Q1, R1, _, _ = oracle.qr(np.array(ex["A"], float), 1)
+            assert info == 0 and np.array_equal(Qq, Q1) and np.array_equal(Rq, R1), (seq, ex["cite"])
