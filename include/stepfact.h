@@ -79,6 +79,19 @@ int lu_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void
 int qr_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dQ, int64_t ldq,
               void* dR, int64_t ldr, int64_t* d_info, void* stream);
 
+/* Variable step: PAPER.md:194 notes that "the s parameter could be varied
+ * during the execution".  steps[0..nsteps) is a HOST array of panel widths s_0, s_1, ...
+ * (each >= 1; the last repeats if the sequence ends before column n; the final panel is
+ * clipped at n): panel p covers [z_p, z_p + s_p) and is flushed (one rectangular product)
+ * before panel p+1 — Algorithms 1-3 with the flush condition c = z + s_p (R11).
+ * A constant sequence is the fixed-s call.  Everything else as for the fixed-s entry points. */
+int chol_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype, const void* dA, int64_t lda, void* dL,
+                      int64_t ldl, int64_t* d_info, void* stream);
+int lu_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype, const void* dA, int64_t lda, void* dLU,
+                    int64_t ldlu, int64_t* d_info, void* stream);
+int qr_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype, const void* dA, int64_t lda, void* dQ,
+                    int64_t ldq, void* dR, int64_t ldr, int64_t* d_info, void* stream);
+
 /* Host-buffer variants (the end-to-end path): same arguments with HOST matrices (pinned
  * memory recommended) and a host info word.  The library copies A to the device, runs
  * the factorization on an internal stream, copies the outputs back and synchronizes

@@ -58,6 +58,13 @@ def lib():
         f = getattr(L, name)
         f.argtypes = args
         f.restype = i32
+    pi = ctypes.POINTER(ctypes.c_int64)
+    for name, args in {"chol_factor_steps": [i64, i64, pi, i32, p, i64, p, i64, p, p],
+                       "lu_factor_steps": [i64, i64, pi, i32, p, i64, p, i64, p, p],
+                       "qr_factor_steps": [i64, i64, pi, i32, p, i64, p, i64, p, i64, p, p]}.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = i32
     pp = ctypes.POINTER(ctypes.c_void_p)
     dist_sig = {
         "chol_factor_dist": [p, i64, i64, i32, pp, pp, i64, pp, p],
@@ -98,7 +105,7 @@ EXPORTS = ("chol_factor", "lu_factor", "qr_factor", "chol_factor_host", "lu_fact
            "sf_launch_counter", "sf_strerror", "sf_last_error", "sf_version", "sf_profile_enable",
            "sf_profile_collect", "sf_get_unique_id", "sf_comm_init", "sf_comm_init_loopback", "sf_comm_destroy",
            "sf_comm_size", "sf_comm_local_ranks", "sf_local_cols", "chol_factor_dist", "lu_factor_dist",
-           "qr_factor_dist")
+           "qr_factor_dist", "chol_factor_steps", "lu_factor_steps", "qr_factor_steps")
 
 
 def _check(rc):
@@ -162,6 +169,29 @@ def lu_colmajor(n, s, dA, lda, dLU, ldlu, d_info, dtype=SF_F64, stream=None):
 def qr_colmajor(n, s, dA, lda, dQ, ldq, dR, ldr, d_info, dtype=SF_F64, stream=None):
     ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
     _check(lib().qr_factor(n, s, dtype, ptr(dA), lda, ptr(dQ), ldq, ptr(dR), ldr, ptr(d_info), _stream(stream)))
+
+
+def _steps_arr(steps):
+    return (ctypes.c_int64 * len(steps))(*[int(x) for x in steps])
+
+
+def chol_steps_colmajor(n, steps, dA, lda, dL, ldl, d_info, dtype=SF_F64, stream=None):
+    """chol_factor_steps: variable step sequence."""
+    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
+    _check(lib().chol_factor_steps(n, len(steps), _steps_arr(steps), dtype, ptr(dA), lda, ptr(dL), ldl, ptr(d_info),
+                                   _stream(stream)))
+
+
+def lu_steps_colmajor(n, steps, dA, lda, dLU, ldlu, d_info, dtype=SF_F64, stream=None):
+    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
+    _check(lib().lu_factor_steps(n, len(steps), _steps_arr(steps), dtype, ptr(dA), lda, ptr(dLU), ldlu, ptr(d_info),
+                                 _stream(stream)))
+
+
+def qr_steps_colmajor(n, steps, dA, lda, dQ, ldq, dR, ldr, d_info, dtype=SF_F64, stream=None):
+    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
+    _check(lib().qr_factor_steps(n, len(steps), _steps_arr(steps), dtype, ptr(dA), lda, ptr(dQ), ldq, ptr(dR), ldr,
+                                 ptr(d_info), _stream(stream)))
 
 
 # ----------------------------------------------------------------------- torch convenience API

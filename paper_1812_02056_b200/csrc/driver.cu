@@ -53,25 +53,24 @@ int fail_with(int code, const char* fmt, ...) {
 
 
 template <typename T>
-static int chol_run(int64_t n, int64_t s, const T* A, int64_t lda, T* L, int64_t ldl, int64_t* d_info,
+static int chol_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* L, int64_t ldl, int64_t* d_info,
                     cudaStream_t st, PanelHook* hook = nullptr) {
   Workspace ws;
   SF_CUDA(ws.init(4096, st));
   long long* fail = ws.take<long long>(2);   // [0] first failed column, [1] leaf counter
   SF_CUDA(init_fail(fail, st));
   Side* sd = nullptr;
-  const bool la = lookahead_on() && s < n;
+  const bool la = lookahead_on() && S.P() > 1;
   if (la) SF_CUDA(side_stream(sd));
   {
     ProfScope ps(1, 0.0, st);
-    const int64_t w0 = s < n ? s : n;
+    const int64_t w0 = S.w(0);
     SF_CUDA(chol_panel_rec<T>(n, w0, A, lda, L, ldl, 0, fail, st));
     if (hook) SF_CUDA(hook->done(0, w0, st));
   }
-  for (int64_t z = 0; z < n; z += s) {
-    const int64_t w = (s < n - z) ? s : n - z, c = z + w;
-    if (c >= n) break;
-    const int64_t w2 = (s < n - c) ? s : n - c, m = n - c;
+  for (int64_t p = 0; p + 1 < S.P(); ++p) {
+    const int64_t z = S.z(p), w = S.w(p), c = z + w;
+    const int64_t w2 = S.w(p + 1), m = n - c;
     const T* src = (z == 0) ? A : L;
     const int64_t lds = (z == 0) ? lda : ldl;
     const T* R = L + c + z * ldl;   // R = L[c:n, z:c)
@@ -113,9 +112,9 @@ static int chol_run(int64_t n, int64_t s, const T* A, int64_t lda, T* L, int64_t
 // fp32 Cholesky: fp32 storage and panel, 3xTF32 tcgen05 flush.  Same
 // schedule and lookahead as chol_run; each panel's split (hi/lo) lives in one of two
 // buffers so the side stream can split panel p+1 while the flush of panel p reads panel p's.
-static int chol_run_f32(int64_t n, int64_t s, const float* A, int64_t lda, float* L, int64_t ldl, int64_t* d_info,
-                        cudaStream_t st, PanelHook* hook = nullptr) {
-  const int64_t ldk = (s + 3) / 4 * 4;
+static int chol_run_f32(int64_t n, const Sched& S, const float* A, int64_t lda, float* L, int64_t ldl,
+                        int64_t* d_info, cudaStream_t st, PanelHook* hook = nullptr) {
+  const int64_t ldk = (S.maxw() + 3) / 4 * 4;
   Workspace ws;
   SF_CUDA(ws.init(4096 + 4 * sizeof(float) * (size_t)n * ldk + 4 * 256, st));
   long long* fail = ws.take<long long>(2);
@@ -127,20 +126,18 @@ static int chol_run_f32(int64_t n, int64_t s, const float* A, int64_t lda, float
   }
   SF_CUDA(init_fail(fail, st));
   Side* sd = nullptr;
-  const bool la = lookahead_on() && s < n;
+  const bool la = lookahead_on() && S.P() > 1;
   if (la) SF_CUDA(side_stream(sd));
   {
     ProfScope ps(1, 0.0, st);
-    const int64_t w0 = s < n ? s : n;
+    const int64_t w0 = S.w(0);
     SF_CUDA(chol_panel_rec_f32(n, w0, A, lda, L, ldl, 0, sb[0], fail, st));
     if (hook) SF_CUDA(hook->done(0, w0, st));
     if (w0 < n) SF_CUDA(split_tf32(n - w0, w0, L + w0, ldl, sb[0].at(w0, 0).h, sb[0].at(w0, 0).l, ldk, st));
   }
-  int64_t p = 0;
-  for (int64_t z = 0; z < n; z += s, ++p) {
-    const int64_t w = (s < n - z) ? s : n - z, c = z + w;
-    if (c >= n) break;
-    const int64_t w2 = (s < n - c) ? s : n - c, m = n - c;
+  for (int64_t p = 0; p + 1 < S.P(); ++p) {
+    const int64_t z = S.z(p), w = S.w(p), c = z + w;
+    const int64_t w2 = S.w(p + 1), m = n - c;
     const float* src = (z == 0) ? A : L;
     const int64_t lds = (z == 0) ? lda : ldl;
     const SplitBuf R = sb[p & 1].at(w, 0);       // R = L[c:n, z:c), split
@@ -175,7 +172,7 @@ static int chol_run_f32(int64_t n, int64_t s, const float* A, int64_t lda, float
 }
 
 template <typename T>
-static int lu_run(int64_t n, int64_t s, const T* A, int64_t lda, T* LU, int64_t ldd, int64_t* d_info,
+static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int64_t ldd, int64_t* d_info,
                   cudaStream_t st) {
   Workspace ws;
   SF_CUDA(ws.init(16384, st));
@@ -185,17 +182,16 @@ static int lu_run(int64_t n, int64_t s, const T* A, int64_t lda, T* LU, int64_t 
   SF_CUDA(init_fail(fail, st));
   SF_CUDA(frob_norm_tol<T>(n, A, lda, tol, part, st));
   Side* sd = nullptr;
-  const bool la = lookahead_on() && s < n;
+  const bool la = lookahead_on() && S.P() > 1;
   if (la) SF_CUDA(side_stream(sd));
   {
     ProfScope ps(1, 0.0, st);
-    const int64_t w0 = s < n ? s : n;
+    const int64_t w0 = S.w(0);
     SF_CUDA(lu_panel_rec<T>(n, w0, n - w0, A, lda, LU, ldd, 0, tol, fail, st));
   }
-  for (int64_t z = 0; z < n; z += s) {
-    const int64_t w = (s < n - z) ? s : n - z, c = z + w;
-    if (c >= n) break;
-    const int64_t w2 = (s < n - c) ? s : n - c, m = n - c;
+  for (int64_t p = 0; p + 1 < S.P(); ++p) {
+    const int64_t z = S.z(p), w = S.w(p), c = z + w;
+    const int64_t w2 = S.w(p + 1), m = n - c;
     const T* src = (z == 0) ? A : LU;
     const int64_t lds = (z == 0) ? lda : ldd;
     const T* RL = LU + c + z * ldd;   // R_L = L[c:n, z:c)
@@ -237,15 +233,16 @@ static int lu_run(int64_t n, int64_t s, const T* A, int64_t lda, T* LU, int64_t 
 
 
 template <typename T>
-static int qr_run(int64_t n, int64_t s, const T* A, int64_t lda, T* Q, int64_t ldq, T* R, int64_t ldr, int64_t* d_info,
-                  cudaStream_t st) {
+static int qr_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* Q, int64_t ldq, T* R, int64_t ldr,
+                  int64_t* d_info, cudaStream_t st) {
+  const int64_t s = S.maxw();
   const int64_t wmax = qr_mgs_max_width(n, (int)sizeof(T));
   const int64_t wcap = s < wmax ? s : wmax;
   const size_t mgs_elems = qr_mgs_work_elems(n, (int)wcap, (int)sizeof(T)) + 64;
   const int64_t cw_elems = s * n;
   int64_t split_elems = 0;
-  for (int64_t z = 0; z < n; z += s) {
-    const int64_t w = (s < n - z) ? s : n - z;
+  for (int64_t p = 0; p < S.P(); ++p) {
+    const int64_t z = S.z(p), w = S.w(p);
     if (z + w < n) {
       const int sp = splitk_for(w, n - z - w, n);
       if ((int64_t)sp * w * (n - z - w) > split_elems) split_elems = (int64_t)sp * w * (n - z - w);
@@ -270,17 +267,16 @@ static int qr_run(int64_t n, int64_t s, const T* A, int64_t lda, T* Q, int64_t l
   SF_CUDA(cudaMemsetAsync(mgsw, 0, sizeof(T) * mgs_elems, st));   // MGS flags (epochs start at 0)
   SF_CUDA(frob_norm_tol<T>(n, A, lda, tol, part, st));
   Side* sd = nullptr;
-  const bool la = lookahead_on() && s < n;
+  const bool la = lookahead_on() && S.P() > 1;
   if (la) SF_CUDA(side_stream(sd));
   {
     ProfScope ps(1, 0.0, st);
-    const int64_t w0 = s < n ? s : n;
+    const int64_t w0 = S.w(0);
     SF_CUDA(qr_panel<T>(n, w0, A, lda, Q, ldq, 0, tol, mgsw, Cw, split, split_elems, fail, st));
   }
-  for (int64_t z = 0; z < n; z += s) {
-    const int64_t w = (s < n - z) ? s : n - z, c = z + w;
-    if (c >= n) break;
-    const int64_t w2 = (s < n - c) ? s : n - c, m = n - c;
+  for (int64_t p = 0; p + 1 < S.P(); ++p) {
+    const int64_t z = S.z(p), w = S.w(p), c = z + w;
+    const int64_t w2 = S.w(p + 1), m = n - c;
     const T* src = (z == 0) ? A : Q;           // M := copy of A lives in Q
     const int64_t lds = (z == 0) ? lda : ldq;
     const T* BQ = Q + z * ldq;                 // B_Q = Q[:, z:c)
@@ -427,8 +423,9 @@ int chol_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, vo
   cudaStream_t st = (cudaStream_t)stream;
   const GraphKey key{0, dtype, n, s, lda, ldl, 0, dA, dL, nullptr, d_info, st};
   return run_graph(key, st, [&]() {
-    if (dtype == SF_F64) return chol_run<double>(n, s, (const double*)dA, lda, (double*)dL, ldl, d_info, st);
-    return chol_run_f32(n, s, (const float*)dA, lda, (float*)dL, ldl, d_info, st);
+    const Sched S(n, s);
+    if (dtype == SF_F64) return chol_run<double>(n, S, (const double*)dA, lda, (double*)dL, ldl, d_info, st);
+    return chol_run_f32(n, S, (const float*)dA, lda, (float*)dL, ldl, d_info, st);
   });
 }
 
@@ -440,8 +437,9 @@ int lu_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void
   cudaStream_t st = (cudaStream_t)stream;
   const GraphKey key{1, dtype, n, s, lda, ldlu, 0, dA, dLU, nullptr, d_info, st};
   return run_graph(key, st, [&]() {
-    if (dtype == SF_F32) return lu_run<float>(n, s, (const float*)dA, lda, (float*)dLU, ldlu, d_info, st);
-    return lu_run<double>(n, s, (const double*)dA, lda, (double*)dLU, ldlu, d_info, st);
+    const Sched S(n, s);
+    if (dtype == SF_F32) return lu_run<float>(n, S, (const float*)dA, lda, (float*)dLU, ldlu, d_info, st);
+    return lu_run<double>(n, S, (const double*)dA, lda, (double*)dLU, ldlu, d_info, st);
   });
 }
 
@@ -456,9 +454,56 @@ int qr_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void
   cudaStream_t st = (cudaStream_t)stream;
   const GraphKey key{2, dtype, n, s, lda, ldq, ldr, dA, dQ, dR, d_info, st};
   return run_graph(key, st, [&]() {
-    if (dtype == SF_F32) return qr_run<float>(n, s, (const float*)dA, lda, (float*)dQ, ldq, (float*)dR, ldr, d_info, st);
-    return qr_run<double>(n, s, (const double*)dA, lda, (double*)dQ, ldq, (double*)dR, ldr, d_info, st);
+    const Sched S(n, s);
+    if (dtype == SF_F32) return qr_run<float>(n, S, (const float*)dA, lda, (float*)dQ, ldq, (float*)dR, ldr, d_info, st);
+    return qr_run<double>(n, S, (const double*)dA, lda, (double*)dQ, ldq, (double*)dR, ldr, d_info, st);
   });
+}
+
+// ------------------------------------------------------------------ variable step (R11)
+static int check_steps(int64_t nsteps, const int64_t* steps) {
+  if (nsteps < 1 || !steps) return fail_with(SF_EINVAL, "empty step sequence");
+  for (int64_t i = 0; i < nsteps; ++i)
+    if (steps[i] < 1) return fail_with(SF_EINVAL, "step %lld of the sequence is < 1", (long long)i);
+  return SF_OK;
+}
+
+int chol_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype, const void* dA, int64_t lda, void* dL,
+                      int64_t ldl, int64_t* d_info, void* stream) {
+  int rc = check_common(n, 1, dtype, dA, lda, dL, ldl);
+  if (!rc) rc = check_steps(nsteps, steps);
+  if (rc) return rc;
+  if (!d_info) return fail_with(SF_EINVAL, "null d_info");
+  cudaStream_t st = (cudaStream_t)stream;
+  const Sched S(n, steps, nsteps);
+  if (dtype == SF_F64) return chol_run<double>(n, S, (const double*)dA, lda, (double*)dL, ldl, d_info, st);
+  return chol_run_f32(n, S, (const float*)dA, lda, (float*)dL, ldl, d_info, st);
+}
+
+int lu_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype, const void* dA, int64_t lda, void* dLU,
+                    int64_t ldlu, int64_t* d_info, void* stream) {
+  int rc = check_common(n, 1, dtype, dA, lda, dLU, ldlu);
+  if (!rc) rc = check_steps(nsteps, steps);
+  if (rc) return rc;
+  if (!d_info) return fail_with(SF_EINVAL, "null d_info");
+  cudaStream_t st = (cudaStream_t)stream;
+  const Sched S(n, steps, nsteps);
+  if (dtype == SF_F32) return lu_run<float>(n, S, (const float*)dA, lda, (float*)dLU, ldlu, d_info, st);
+  return lu_run<double>(n, S, (const double*)dA, lda, (double*)dLU, ldlu, d_info, st);
+}
+
+int qr_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype, const void* dA, int64_t lda, void* dQ,
+                    int64_t ldq, void* dR, int64_t ldr, int64_t* d_info, void* stream) {
+  int rc = check_common(n, 1, dtype, dA, lda, dQ, ldq);
+  if (!rc) rc = check_common(n, 1, dtype, dA, lda, dR, ldr);
+  if (!rc) rc = check_steps(nsteps, steps);
+  if (rc) return rc;
+  if (dA == dQ || dA == dR || dQ == dR) return fail_with(SF_EINVAL, "qr_factor outputs must not alias");
+  if (!d_info) return fail_with(SF_EINVAL, "null d_info");
+  cudaStream_t st = (cudaStream_t)stream;
+  const Sched S(n, steps, nsteps);
+  if (dtype == SF_F32) return qr_run<float>(n, S, (const float*)dA, lda, (float*)dQ, ldq, (float*)dR, ldr, d_info, st);
+  return qr_run<double>(n, S, (const double*)dA, lda, (double*)dQ, ldq, (double*)dR, ldr, d_info, st);
 }
 
 // ------------------------------------------------------------------ host-buffer variants
@@ -523,8 +568,9 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
     if (e == cudaSuccess) {
       SF_CUDA(cudaEventRecord(ev, st));      // the copy stream must not run ahead of the previous call
       SF_CUDA(cudaStreamWaitEvent(cs, ev, 0));
-      rc = dtype == SF_F64 ? chol_run<double>(n, s, (const double*)d, n, (double*)d, n, dinfo, st, &hook)
-                           : chol_run_f32(n, s, (const float*)d, n, (float*)d, n, dinfo, st, &hook);
+      const Sched S(n, s);
+      rc = dtype == SF_F64 ? chol_run<double>(n, S, (const double*)d, n, (double*)d, n, dinfo, st, &hook)
+                           : chol_run_f32(n, S, (const float*)d, n, (float*)d, n, dinfo, st, &hook);
       if (!rc) {
         e = cudaEventRecord(ev, cs);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev, 0);

@@ -98,6 +98,37 @@ struct Workspace {
   }
 };
 
+// ------------------------------------------------------------------ schedule (a1)
+// Panel boundaries of the step-s schedule: panel p = columns
+// [z(p), z(p) + w(p)); a flush follows every panel but the last.  Fixed s, or a step
+// sequence s_0, s_1, ... ("the s parameter could be varied during the execution",
+// PAPER.md:194, reading R11; the last step repeats if the sequence is short).
+struct Sched {
+  int64_t n;
+  std::vector<int64_t> start;   // panel starts, then n
+  Sched(int64_t n_, int64_t s) : n(n_) {
+    for (int64_t z = 0; z < n; z += s) start.push_back(z);
+    start.push_back(n);
+  }
+  Sched(int64_t n_, const int64_t* steps, int64_t nsteps) : n(n_) {
+    int64_t z = 0, p = 0;
+    while (z < n) {
+      start.push_back(z);
+      z += steps[p < nsteps ? p : nsteps - 1];
+      ++p;
+    }
+    start.push_back(n);
+  }
+  int64_t P() const { return (int64_t)start.size() - 1; }
+  int64_t z(int64_t p) const { return start[p]; }
+  int64_t w(int64_t p) const { return start[p + 1] - start[p]; }
+  int64_t maxw() const {
+    int64_t m = 1;
+    for (int64_t p = 0; p < P(); ++p) m = w(p) > m ? w(p) : m;
+    return m;
+  }
+};
+
 // ------------------------------------------------------------------ panel completion hook
 // Called (on the host, while enqueueing) after the work that finishes panel [z, z+w) has
 // been enqueued on stream `st`: the end-to-end host path uses it to start the device->host

@@ -381,3 +381,60 @@ def test_chol_host_lower_panels(n, s, dtype):
     hB = np.asfortranarray(A.astype(npdt))
     out2, info2 = sf.chol_host(hB, s, dtype=dtype)
     assert info2 == 0 and np.array_equal(np.tril(out2), np.tril(out)) and np.array_equal(np.triu(out2, 1), np.triu(A.astype(npdt), 1))
+
+
+# ============================================================ variable step (f2, reading R11)
+
+@pytest.mark.parametrize("steps", [[64], [7, 100, 33, 1, 64], [256, 128, 64, 32, 16], [1000]])
+def test_variable_steps(steps):
+    """chol/lu/qr_factor_steps: against the oracle run with the same step
+    sequence; a tapering sequence (large panels early, small at the tail) included."""
+    n = 700
+    A = synth.gen_numpy("spd_scaled", n, seed=21)
+    dA = dev(A)
+    info = torch.zeros(1, dtype=torch.int64, device="cuda")
+    out = torch.full_like(dA, 7.0)
+    sf.chol_steps_colmajor(n, steps, dA, n, out, n, info)
+    torch.cuda.synchronize()
+    Lo, io = oracle.chol(A, steps)
+    assert int(info.item()) == io == 0
+    assert synth.r2_error(np.tril(host(out)), Lo) <= TOL64
+    B = synth.gen_numpy("diag_dominant", n, seed=22)
+    dB = dev(B)
+    out = torch.empty_like(dB)
+    sf.lu_steps_colmajor(n, steps, dB, n, out, n, info)
+    torch.cuda.synchronize()
+    Lo, Uo, io = oracle.lu(B, steps)
+    F = host(out)
+    assert int(info.item()) == io == 0
+    assert synth.r2_error(np.tril(F), Lo) <= TOL64 and synth.r2_error(np.triu(F, 1) + np.eye(n), Uo) <= TOL64
+    C = synth.gen_numpy("gaussian", n, seed=23)
+    dC = dev(C)
+    Q = torch.empty_like(dC); R = torch.empty_like(dC)
+    sf.qr_steps_colmajor(n, steps, dC, n, Q, n, R, n, info)
+    torch.cuda.synchronize()
+    Qo, Ro, io, _ = oracle.qr(C, steps)
+    assert int(info.item()) == io == 0
+    last = steps[-1] if sum(steps) < n else steps[min(len(steps) - 1, 2)]
+    check_qr(C, max(last, 64), host(Q), host(R), Qo, Ro)
+
+
+def test_variable_steps_constant_is_fixed_s():
+    n, s = 520, 96
+    A = synth.gen_numpy("spd_scaled", n, seed=2)
+    dA = dev(A)
+    info = torch.zeros(1, dtype=torch.int64, device="cuda")
+    o1 = torch.zeros_like(dA); o2 = torch.zeros_like(dA)
+    sf.chol_colmajor(n, s, dA, n, o1, n, info)
+    sf.chol_steps_colmajor(n, [s] * 3, dA, n, o2, n, info)   # the last step repeats
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+
+
+def test_variable_steps_invalid():
+    d = torch.zeros(16, device="cuda", dtype=torch.float64)
+    info = torch.zeros(1, dtype=torch.int64, device="cuda")
+    with pytest.raises(sf.StepfactError):
+        sf.chol_steps_colmajor(4, [2, 0], d, 4, d, 4, info)
+    with pytest.raises(sf.StepfactError):
+        sf.chol_steps_colmajor(4, [], d, 4, d, 4, info)
