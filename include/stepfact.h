@@ -92,6 +92,19 @@ int lu_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype, 
 int qr_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype, const void* dA, int64_t lda, void* dQ,
                     int64_t ldq, void* dR, int64_t ldr, int64_t* d_info, void* stream);
 
+/* Solving with the factors ("used everywhere to solve linear systems",
+ * PAPER.md:16): A X = B for nrhs right-hand sides, B (n x nrhs, column-major, ldb >= n,
+ * device) overwritten by X.  Triangular solves by recursive halving: 32-row substitution
+ * leaves plus tensor-core GEMMs for the couplings.  Stream-ordered; no pivoting, no
+ * singularity checks (the factorization's info covers that).
+ *   chol_solve: dL from chol_factor (lower triangle read): L Y = B, L^T X = Y.
+ *   lu_solve:   dLU from lu_factor: L Y = B (L with its diagonal), U X = Y (U unit upper).
+ *   qr_solve:   dQ, dR from qr_factor: X = R^-1 (Q^T B). */
+int chol_solve(int64_t n, int64_t nrhs, int dtype, const void* dL, int64_t ldl, void* dB, int64_t ldb, void* stream);
+int lu_solve(int64_t n, int64_t nrhs, int dtype, const void* dLU, int64_t ldlu, void* dB, int64_t ldb, void* stream);
+int qr_solve(int64_t n, int64_t nrhs, int dtype, const void* dQ, int64_t ldq, const void* dR, int64_t ldr, void* dB,
+             int64_t ldb, void* stream);
+
 /* Host-buffer variants (the end-to-end path): same arguments with HOST matrices (pinned
  * memory recommended) and a host info word.  The library copies A to the device, runs
  * the factorization on an internal stream, copies the outputs back and synchronizes

@@ -53,6 +53,8 @@ def _load():
         lib.orc_lu_steps.argtypes = [i64, i64, pi, i64, p, i64, p, i64, p, i64, dbl]
         lib.orc_qr_steps.restype = i64
         lib.orc_qr_steps.argtypes = [i64, i64, pi, i64, p, i64, p, i64, p, i64, dbl, ctypes.POINTER(dbl)]
+        lib.orc_solve.restype = None
+        lib.orc_solve.argtypes = [i64, i64, i64, p, i64, p, i64, p, i64]
         lib.orc_flush_count.restype = i64
         lib.orc_flush_count.argtypes = [i64, i64]
         lib.orc_frobenius.restype = dbl
@@ -152,3 +154,15 @@ def qr(A, s, kcols=None, tol=0.0):
 def frobenius(A):
     A = _colmajor(A)
     return float(_load().orc_frobenius(A.shape[0], A.ctypes.data, A.shape[0]))
+
+
+def solve(kind, F1, B, F2=None):
+    """Plain forward/back substitution with the factors (oracle/stepfact_oracle.c orc_solve):
+    kind 'chol' (F1 = L), 'lu' (F1 = L with U packed above), 'qr' (F1 = Q, F2 = R).
+    Returns X for A X = B."""
+    k = {"chol": 0, "lu": 1, "qr": 2}[kind]
+    F1 = _colmajor(F1); n = F1.shape[0]
+    F2c = _colmajor(F2) if F2 is not None else F1
+    X = np.asfortranarray(np.array(B, dtype=np.float64).reshape(n, -1))
+    _load().orc_solve(k, n, X.shape[1], F1.ctypes.data, n, F2c.ctypes.data, n, X.ctypes.data, n)
+    return X

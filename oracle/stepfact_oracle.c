@@ -313,3 +313,44 @@ int64_t orc_qr_steps(int64_t n, int64_t nsteps, const int64_t* steps, int64_t kc
   Steps sp = {steps, nsteps, steps[0], 0};
   return qr_core(n, sp, kcols, A, lda, Q, ldq, R, ldr, tol, lower_mass);
 }
+
+/*
+ * Solving with the factors ("used everywhere to solve linear systems"): plain
+ * forward / back substitution, column by column of B (n x nrhs, in place), fp64.
+ *   kind 0: A = L L^T   (F1 = L, lower):      L y = b (forward, / L_ii), L^T x = y (backward)
+ *   kind 1: A = L U     (F1 = L\U packed):    L y = b (forward, / L_ii), U x = y (unit, backward)
+ *   kind 2: A = Q R     (F1 = Q, F2 = R):     y = Q^T b, R x = y (backward, / R_ii)
+ */
+void orc_solve(int64_t kind, int64_t n, int64_t nrhs, const double* F1, int64_t ld1, const double* F2, int64_t ld2,
+               double* B, int64_t ldb) {
+  double* y = (double*)malloc(sizeof(double) * (size_t)n);
+  if (!y) return;
+  for (int64_t j = 0; j < nrhs; ++j) {
+    double* b = B + (size_t)j * (size_t)ldb;
+    if (kind == 2) {
+      for (int64_t i = 0; i < n; ++i) {                       /* y = Q^T b */
+        double t = 0.0;
+        for (int64_t k = 0; k < n; ++k) t += AT(F1, ld1, k, i) * b[k];
+        y[i] = t;
+      }
+      for (int64_t i = n - 1; i >= 0; --i) {                  /* R x = y */
+        double t = y[i];
+        for (int64_t k = i + 1; k < n; ++k) t = t - AT(F2, ld2, i, k) * b[k];
+        b[i] = t / AT(F2, ld2, i, i);
+      }
+      continue;
+    }
+    for (int64_t i = 0; i < n; ++i) {                         /* L y = b */
+      double t = b[i];
+      for (int64_t k = 0; k < i; ++k) t = t - AT(F1, ld1, i, k) * b[k];
+      b[i] = t / AT(F1, ld1, i, i);
+    }
+    for (int64_t i = n - 1; i >= 0; --i) {                    /* L^T x = y  or  U x = y */
+      double t = b[i];
+      for (int64_t k = i + 1; k < n; ++k)
+        t = t - (kind == 0 ? AT(F1, ld1, k, i) : AT(F1, ld1, i, k)) * b[k];
+      b[i] = kind == 0 ? t / AT(F1, ld1, i, i) : t;
+    }
+  }
+  free(y);
+}

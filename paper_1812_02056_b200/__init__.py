@@ -58,6 +58,12 @@ def lib():
         f = getattr(L, name)
         f.argtypes = args
         f.restype = i32
+    for name, args in {"chol_solve": [i64, i64, i32, p, i64, p, i64, p],
+                       "lu_solve": [i64, i64, i32, p, i64, p, i64, p],
+                       "qr_solve": [i64, i64, i32, p, i64, p, i64, p, i64, p]}.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = i32
     pi = ctypes.POINTER(ctypes.c_int64)
     for name, args in {"chol_factor_steps": [i64, i64, pi, i32, p, i64, p, i64, p, p],
                        "lu_factor_steps": [i64, i64, pi, i32, p, i64, p, i64, p, p],
@@ -105,7 +111,8 @@ EXPORTS = ("chol_factor", "lu_factor", "qr_factor", "chol_factor_host", "lu_fact
            "sf_launch_counter", "sf_strerror", "sf_last_error", "sf_version", "sf_profile_enable",
            "sf_profile_collect", "sf_get_unique_id", "sf_comm_init", "sf_comm_init_loopback", "sf_comm_destroy",
            "sf_comm_size", "sf_comm_local_ranks", "sf_local_cols", "chol_factor_dist", "lu_factor_dist",
-           "qr_factor_dist", "chol_factor_steps", "lu_factor_steps", "qr_factor_steps")
+           "qr_factor_dist", "chol_factor_steps", "lu_factor_steps", "qr_factor_steps", "chol_solve", "lu_solve",
+           "qr_solve")
 
 
 def _check(rc):
@@ -192,6 +199,22 @@ def qr_steps_colmajor(n, steps, dA, lda, dQ, ldq, dR, ldr, d_info, dtype=SF_F64,
     ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
     _check(lib().qr_factor_steps(n, len(steps), _steps_arr(steps), dtype, ptr(dA), lda, ptr(dQ), ldq, ptr(dR), ldr,
                                  ptr(d_info), _stream(stream)))
+
+
+def chol_solve_colmajor(n, nrhs, dL, ldl, dB, ldb, dtype=SF_F64, stream=None):
+    """chol_solve: B := A^-1 B with A = L L^T (column-major device buffers)."""
+    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
+    _check(lib().chol_solve(n, nrhs, dtype, ptr(dL), ldl, ptr(dB), ldb, _stream(stream)))
+
+
+def lu_solve_colmajor(n, nrhs, dLU, ldlu, dB, ldb, dtype=SF_F64, stream=None):
+    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
+    _check(lib().lu_solve(n, nrhs, dtype, ptr(dLU), ldlu, ptr(dB), ldb, _stream(stream)))
+
+
+def qr_solve_colmajor(n, nrhs, dQ, ldq, dR, ldr, dB, ldb, dtype=SF_F64, stream=None):
+    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
+    _check(lib().qr_solve(n, nrhs, dtype, ptr(dQ), ldq, ptr(dR), ldr, ptr(dB), ldb, _stream(stream)))
 
 
 # ----------------------------------------------------------------------- torch convenience API

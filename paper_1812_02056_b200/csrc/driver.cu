@@ -409,6 +409,30 @@ static int run_graph(const GraphKey& key, cudaStream_t st, F&& body) {
   return SF_OK;
 }
 
+template <typename T>
+static int solve_run(int kind, int64_t n, int64_t nrhs, const T* F1, int64_t ld1, const T* F2, int64_t ld2, T* B,
+                     int64_t ldb, cudaStream_t st) {
+  if (nrhs == 0) return SF_OK;
+  Workspace ws;
+  SF_CUDA(ws.init(4096 + (kind == 2 ? sizeof(T) * (size_t)n * (size_t)nrhs + 256 : 0), st));
+  long long* fail = ws.take<long long>(2);
+  SF_CUDA(init_fail(fail, st));
+  if (kind == 0) {          // A = L L^T: L Y = B, then L^T X = Y
+    SF_CUDA(lu_usolve_rec<T>(n, nrhs, F1, ld1, B, ldb, fail, st));
+    SF_CUDA(trsm_upper_rec<T>(n, nrhs, F1, ld1, 1, 0, B, ldb, st));
+  } else if (kind == 1) {   // A = L U (U unit upper): L Y = B, then U X = Y
+    SF_CUDA(lu_usolve_rec<T>(n, nrhs, F1, ld1, B, ldb, fail, st));
+    SF_CUDA(trsm_upper_rec<T>(n, nrhs, F1, ld1, 0, 1, B, ldb, st));
+  } else {                  // A = Q R: Y = Q^T B, R X = Y
+    T* Y = ws.take<T>((size_t)n * nrhs);
+    Gemm<T> g{n, nrhs, n, F1, ld1, 1, B, ldb, 1, nullptr, 0, Y, n, 1.0, 0, kMaskNone, 1, nullptr, fail};
+    SF_CUDA(run_gemm(g, st));
+    SF_CUDA(trsm_upper_rec<T>(n, nrhs, F2, ld2, 0, 0, Y, n, st));
+    SF_CUDA(copy_matrix<T>(n, nrhs, Y, n, B, ldb, st));
+  }
+  return SF_OK;
+}
+
 }  // namespace sf
 
 using namespace sf;
@@ -504,6 +528,41 @@ int qr_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype, 
   const Sched S(n, steps, nsteps);
   if (dtype == SF_F32) return qr_run<float>(n, S, (const float*)dA, lda, (float*)dQ, ldq, (float*)dR, ldr, d_info, st);
   return qr_run<double>(n, S, (const double*)dA, lda, (double*)dQ, ldq, (double*)dR, ldr, d_info, st);
+}
+
+// ------------------------------------------------------------------ solves with the factors (f4)
+static int check_solve(int64_t n, int64_t nrhs, int dtype, const void* f, int64_t ldf, const void* b, int64_t ldb) {
+  if (n < 1 || nrhs < 0) return fail_with(SF_EINVAL, "bad solve sizes");
+  if (dtype != SF_F64 && dtype != SF_F32) return fail_with(SF_EINVAL, "unknown dtype %d", dtype);
+  if (!f || !b || ldf < n || ldb < n) return fail_with(SF_EINVAL, "bad solve pointers / leading dimensions");
+  return SF_OK;
+}
+
+int chol_solve(int64_t n, int64_t nrhs, int dtype, const void* dL, int64_t ldl, void* dB, int64_t ldb, void* stream) {
+  int rc = check_solve(n, nrhs, dtype, dL, ldl, dB, ldb);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SF_F32) return solve_run<float>(0, n, nrhs, (const float*)dL, ldl, nullptr, 0, (float*)dB, ldb, st);
+  return solve_run<double>(0, n, nrhs, (const double*)dL, ldl, nullptr, 0, (double*)dB, ldb, st);
+}
+
+int lu_solve(int64_t n, int64_t nrhs, int dtype, const void* dLU, int64_t ldlu, void* dB, int64_t ldb, void* stream) {
+  int rc = check_solve(n, nrhs, dtype, dLU, ldlu, dB, ldb);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SF_F32) return solve_run<float>(1, n, nrhs, (const float*)dLU, ldlu, nullptr, 0, (float*)dB, ldb, st);
+  return solve_run<double>(1, n, nrhs, (const double*)dLU, ldlu, nullptr, 0, (double*)dB, ldb, st);
+}
+
+int qr_solve(int64_t n, int64_t nrhs, int dtype, const void* dQ, int64_t ldq, const void* dR, int64_t ldr, void* dB,
+             int64_t ldb, void* stream) {
+  int rc = check_solve(n, nrhs, dtype, dQ, ldq, dB, ldb);
+  if (!rc) rc = check_solve(n, nrhs, dtype, dR, ldr, dB, ldb);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SF_F32)
+    return solve_run<float>(2, n, nrhs, (const float*)dQ, ldq, (const float*)dR, ldr, (float*)dB, ldb, st);
+  return solve_run<double>(2, n, nrhs, (const double*)dQ, ldq, (const double*)dR, ldr, (double*)dB, ldb, st);
 }
 
 // ------------------------------------------------------------------ host-buffer variants

@@ -326,6 +326,27 @@ inline cudaError_t lu_usolve_rec(int64_t w, int64_t ncols, const T* l11, int64_t
   return lu_usolve_rec<T>(w - h, ncols, l11 + h + h * ldl, ldl, U + h, ldu, fail, st);
 }
 
+// ------------------------------------------------------------------ triangular solves (f4)
+// Forward: L X = B, L lower non-unit (w x w at l, ldl), B w x ncols in place — the U-row
+// solve of the LU panel is exactly this (lu_usolve_rec).
+// Backward: T X = B, T upper (trans = 0: T = U or R as stored; trans = 1: T = L^T), unit or
+// not; recursive halving, bottom half first, the coupling by one GEMM.
+template <typename T>
+inline cudaError_t trsm_upper_rec(int64_t w, int64_t ncols, const T* t, int64_t ldt, int trans, int unit, T* B,
+                                  int64_t ldb, cudaStream_t st) {
+  const int leaf = leaf_width();
+  if (w <= leaf) return trsm_upper_leaf<T>(ncols, (int)w, t, ldt, trans, unit, B, ldb, st);
+  const int64_t h = half_of(w, leaf);
+  // bottom rows [h, w): T22 at (h, h)
+  cudaError_t e = trsm_upper_rec<T>(w - h, ncols, t + h + h * ldt, ldt, trans, unit, B + h, ldb, st);
+  if (e != cudaSuccess) return e;
+  // B[0:h] -= T12 X2,  T12(i, k) = T(i, h + k): trans 0 -> t[i + (h+k)*ldt] ; trans 1 -> t[(h+k) + i*ldt]
+  if (trans) e = gemm_sub<T>(h, ncols, w - h, t + h, ldt, 1, B + h, ldb, 1, B, ldb, B, ldb, kMaskNone, nullptr, st);
+  else e = gemm_sub<T>(h, ncols, w - h, t + h * ldt, ldt, 0, B + h, ldb, 1, B, ldb, B, ldb, kMaskNone, nullptr, st);
+  if (e != cudaSuccess) return e;
+  return trsm_upper_rec<T>(h, ncols, t, ldt, trans, unit, B, ldb, st);
+}
+
 // ------------------------------------------------------------------ QR
 inline int splitk_for(int64_t M, int64_t N, int64_t K) {
   const int64_t tiles = ((M + 127) / 128) * ((N + 63) / 64);   // gemm_f64 CTA tile 128 x 64, 2 CTAs/SM

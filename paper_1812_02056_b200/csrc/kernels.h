@@ -88,6 +88,12 @@ template <typename T>
 cudaError_t lu_usolve_leaf(int64_t ncols, int w, const T* l11, int64_t ldl, const T* src, int64_t lds, T* dst,
                            int64_t ldd, const long long* fail, cudaStream_t st);
 
+// Upper-triangular solve T X = B in place (ncols right-hand sides, w <= 32 rows): trans = 0:
+// T_ck = t[c + k*ldt]; trans = 1: T_ck = t[k + c*ldt] (L^T of a lower L); unit: T_cc = 1.
+template <typename T>
+cudaError_t trsm_upper_leaf(int64_t ncols, int w, const T* t, int64_t ldt, int trans, int unit, T* B, int64_t ldb,
+                            cudaStream_t st);
+
 // QR panel, modified Gram-Schmidt (Alg. 3) on n x w columns.
 template <typename T>
 cudaError_t qr_mgs_panel(int64_t n, int w, const T* src, int64_t lds, T* dst, int64_t ldd,

@@ -423,6 +423,75 @@ cudaError_t lu_usolve_leaf(int64_t ncols, int w, const T* l11, int64_t ldl, cons
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ back substitution
+// Upper-triangular solve T X = B for ncols right-hand sides in place, w <= W rows:
+//   x_c = (y_c - sum_{k>c} T_ck x_k) / T_ck   (c descending; UNIT: no division)
+// with T given by its storage: TRANS = 0 -> T_ck = t[c + k*ldt] (an upper factor: U, R);
+// TRANS = 1 -> T_ck = t[k + c*ldt] (the transpose of a lower factor: L^T).  Columns staged
+// through shared memory so each column's w contiguous entries move coalesced.  Used by the
+// triangular solves with the factors (chol/lu/qr_solve).
+template <typename T, int W, bool TRANS, bool UNIT>
+__global__ void __launch_bounds__(kLeafT) trsm_upper_kernel(int64_t ncols_total, int w, const T* __restrict__ t,
+                                                            int64_t ldt, T* __restrict__ B, int64_t ldb) {
+  __shared__ T Ts[W][W + 1];
+  __shared__ T inv[W];
+  __shared__ T S[kUCols][W + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < W * W; idx += kLeafT) {
+    const int c = idx % W, k = idx / W;
+    T v = T(0);
+    if (c < w && k < w && k >= c) v = TRANS ? __ldcg(t + k + (int64_t)c * ldt) : __ldcg(t + c + (int64_t)k * ldt);
+    Ts[c][k] = v;
+  }
+  __syncthreads();
+  if (!UNIT && tid < w) inv[tid] = T(1) / Ts[tid][tid];
+  const int64_t j0 = (int64_t)blockIdx.x * kUCols;
+  const int ncols = (int)((ncols_total - j0) < kUCols ? (ncols_total - j0) : kUCols);
+  for (int jj = warp; jj < ncols; jj += kLeafT / 32)
+    if (lane < w) S[jj][lane] = __ldcg(B + lane + (j0 + jj) * ldb);
+  __syncthreads();
+  if (tid < ncols) {
+    T y[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) y[k] = (k < w) ? S[tid][k] : T(0);
+#pragma unroll
+    for (int c = W - 1; c >= 0; --c) {
+      if (c < w) {
+        T a0 = y[c], a1 = T(0);
+#pragma unroll
+        for (int k = c + 1; k < W; ++k) {
+          if ((k & 1) == 0) a0 = fma(-Ts[c][k], y[k], a0);
+          else a1 = fma(-Ts[c][k], y[k], a1);
+        }
+        y[c] = UNIT ? (a0 + a1) : (a0 + a1) * inv[c];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) S[tid][k] = y[k];
+  }
+  __syncthreads();
+  for (int jj = warp; jj < ncols; jj += kLeafT / 32)
+    if (lane < w) B[lane + (j0 + jj) * ldb] = S[jj][lane];
+}
+
+template <typename T>
+cudaError_t trsm_upper_leaf(int64_t ncols, int w, const T* t, int64_t ldt, int trans, int unit, T* B, int64_t ldb,
+                            cudaStream_t st) {
+  if (w <= 0 || ncols <= 0) return cudaSuccess;
+  if (w > 32) return cudaErrorInvalidValue;
+  const int grid = (int)((ncols + kUCols - 1) / kUCols);
+#define SF_TRSM(TR, UN)                                                                                  \
+  if (w <= 16) trsm_upper_kernel<T, 16, TR, UN><<<grid, kLeafT, 0, st>>>(ncols, w, t, ldt, B, ldb);      \
+  else trsm_upper_kernel<T, 32, TR, UN><<<grid, kLeafT, 0, st>>>(ncols, w, t, ldt, B, ldb);
+  if (trans && unit) { SF_TRSM(true, true) }
+  else if (trans) { SF_TRSM(true, false) }
+  else if (unit) { SF_TRSM(false, true) }
+  else { SF_TRSM(false, false) }
+#undef SF_TRSM
+  count_launch();
+  return cudaGetLastError();
+}
+
 template cudaError_t chol_leaf<double>(int64_t, int, const double*, int64_t, double*, int64_t, int64_t, long long*,
                                        cudaStream_t);
 template cudaError_t chol_leaf<float>(int64_t, int, const float*, int64_t, float*, int64_t, int64_t, long long*,
@@ -436,5 +505,10 @@ template cudaError_t lu_usolve_leaf<double>(int64_t, int, const double*, int64_t
                                             int64_t, const long long*, cudaStream_t);
 template cudaError_t lu_usolve_leaf<float>(int64_t, int, const float*, int64_t, const float*, int64_t, float*, int64_t,
                                            const long long*, cudaStream_t);
+
+template cudaError_t trsm_upper_leaf<double>(int64_t, int, const double*, int64_t, int, int, double*, int64_t,
+                                             cudaStream_t);
+template cudaError_t trsm_upper_leaf<float>(int64_t, int, const float*, int64_t, int, int, float*, int64_t,
+                                            cudaStream_t);
 
 }  // namespace sf

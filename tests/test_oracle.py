@@ -262,3 +262,29 @@ def test_variable_steps_pins():
             Qq, Rq, info, _ = oracle.qr(np.array(ex["A"], float), list(seq))
             Q1, R1, _, _ = oracle.qr(np.array(ex["A"], float), 1)
             assert info == 0 and np.array_equal(Qq, Q1) and np.array_equal(Rq, R1), (seq, ex["cite"])
+
+
+# ------------------------------------------------------------------ solves with the factors
+
+@pytest.mark.parametrize("n", [1, 5, 60])
+def test_oracle_solves_pinned(n):
+    """orc_solve against scipy's triangular solves and the residual of A x = b."""
+    rng = np.random.default_rng(n)
+    B = rng.standard_normal((n, 3))
+    A = synth.gen_numpy("paper_spd", n, seed=n)
+    L, _ = oracle.chol(A, 8 if n > 8 else n)
+    X = oracle.solve("chol", L, B)
+    Y = scipy.linalg.solve_triangular(L, B, lower=True)
+    assert np.allclose(X, scipy.linalg.solve_triangular(L.T, Y, lower=False), rtol=1e-12, atol=1e-14)
+    assert np.abs(A @ X - B).max() <= 1e-12 * np.abs(B).max() * n
+    D = synth.gen_numpy("diag_dominant", n, seed=n)
+    Ld, Ud, _ = oracle.lu(D, 8 if n > 8 else n)
+    X = oracle.solve("lu", np.tril(Ld) + np.triu(Ud, 1), B)
+    assert np.allclose(X, scipy.linalg.solve_triangular(Ud, scipy.linalg.solve_triangular(Ld, B, lower=True),
+                                                        lower=False, unit_diagonal=True), rtol=1e-12, atol=1e-14)
+    assert np.abs(D @ X - B).max() <= 1e-12 * np.abs(B).max() * n * np.abs(D).max()
+    G = synth.gen_numpy("gaussian", n, seed=n) + 4 * np.eye(n)
+    Q, R, _, _ = oracle.qr(G, 8 if n > 8 else n)
+    X = oracle.solve("qr", Q, B, R)
+    assert np.allclose(X, scipy.linalg.solve_triangular(R, Q.T @ B, lower=False), rtol=1e-10, atol=1e-12)
+    assert np.abs(G @ X - B).max() <= 1e-11 * np.abs(B).max() * n * np.abs(G).max()
