@@ -55,6 +55,19 @@ inline int leaf_width() {
   return w;
 }
 
+// Cholesky leaf width: 32 (default) or 64 (chol_leaf_warp_kernel<T, 64>: one launch instead
+// of two 32-wide leaves and the GEMM between them — measured slower: its 64-step diagonal
+// Crout and 168-register substitution cost more than they save).  SF_CHOL_LEAF = 16/32/64.
+inline int chol_leaf_width() {
+  static int w = [] {
+    const char* e = getenv("SF_CHOL_LEAF");
+    int v = e ? atoi(e) : 32;
+    if (v != 16 && v != 32 && v != 64) v = 32;
+    return v;
+  }();
+  return w;
+}
+
 inline int64_t half_of(int64_t w, int leaf) {
   int64_t h = (w / 2 + leaf - 1) / leaf * leaf;
   if (h >= w) h = w - leaf;
@@ -241,7 +254,7 @@ inline cudaError_t gemm_sub(int64_t M, int64_t N, int64_t K, const T* A, int64_t
 template <typename T>
 inline cudaError_t chol_panel_rec(int64_t m, int64_t w, const T* src, int64_t lds, T* dst, int64_t ldd,
                                   int64_t col0, long long* fail, cudaStream_t st) {
-  const int leaf = leaf_width();
+  const int leaf = chol_leaf_width();
   if (w <= leaf) return chol_leaf<T>(m, (int)w, src, lds, dst, ldd, col0, fail, st);
   const int64_t h = half_of(w, leaf);
   cudaError_t e = chol_panel_rec<T>(m, h, src, lds, dst, ldd, col0, fail, st);
@@ -273,7 +286,7 @@ inline cudaError_t syrk_tf32(int64_t M, int64_t N, int64_t K, const SplitBuf& a,
 // for the flush.
 inline cudaError_t chol_panel_rec_f32(int64_t m, int64_t w, const float* src, int64_t lds, float* dst, int64_t ldd,
                                       int64_t col0, SplitBuf sb, long long* fail, cudaStream_t st) {
-  const int leaf = leaf_width();
+  const int leaf = chol_leaf_width();
   if (w <= leaf) return chol_leaf<float>(m, (int)w, src, lds, dst, ldd, col0, fail, st);
   const int64_t h = half_of(w, leaf);
   cudaError_t e = chol_panel_rec_f32(m, h, src, lds, dst, ldd, col0, sb, fail, st);

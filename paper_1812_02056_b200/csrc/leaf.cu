@@ -145,33 +145,50 @@ __global__ void __launch_bounds__(kLeafT) chol_leaf_warp_kernel(int64_t m, int w
   const int64_t r = w + (int64_t)blockIdx.x * kLeafT + tid;
   T x[W];
   if (warp == 0) {
-    if (lane < W)
-      for (int k = 0; k < W; ++k) Ls[lane][k] = (lane < w && k <= lane && k < w) ? __ldcg(src + lane + (int64_t)k * lds) : T(0);
+    constexpr int RPL = (W + 31) / 32;   // diagonal-block rows per lane: lane + 32*rr
+#pragma unroll
+    for (int rr = 0; rr < RPL; ++rr) {
+      const int i = lane + 32 * rr;
+      if (i < W)
+        for (int k = 0; k < W; ++k) Ls[i][k] = (i < w && k <= i && k < w) ? __ldcg(src + i + (int64_t)k * lds) : T(0);
+    }
     __syncwarp();
     int okc = 1;
     for (int c = 0; c < w; ++c) {
-      T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
-      const int i = lane;
-      if (i >= c && i < w) {
-        int k = 0;
-        for (; k + 3 < c; k += 4) {
-          a0 = fma(Ls[i][k], Ls[c][k], a0);
-          a1 = fma(Ls[i][k + 1], Ls[c][k + 1], a1);
-          a2 = fma(Ls[i][k + 2], Ls[c][k + 2], a2);
-          a3 = fma(Ls[i][k + 3], Ls[c][k + 3], a3);
+      T tv[RPL];
+#pragma unroll
+      for (int rr = 0; rr < RPL; ++rr) {
+        const int i = lane + 32 * rr;
+        T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+        if (i >= c && i < w) {
+          int k = 0;
+          for (; k + 3 < c; k += 4) {
+            a0 = fma(Ls[i][k], Ls[c][k], a0);
+            a1 = fma(Ls[i][k + 1], Ls[c][k + 1], a1);
+            a2 = fma(Ls[i][k + 2], Ls[c][k + 2], a2);
+            a3 = fma(Ls[i][k + 3], Ls[c][k + 3], a3);
+          }
+          for (; k < c; ++k) a0 = fma(Ls[i][k], Ls[c][k], a0);
         }
-        for (; k < c; ++k) a0 = fma(Ls[i][k], Ls[c][k], a0);
+        tv[rr] = (i < w) ? Ls[i][c] - ((a0 + a1) + (a2 + a3)) : T(0);
       }
-      const T t = (i < w) ? Ls[i][c] - ((a0 + a1) + (a2 + a3)) : T(0);
-      const T d = __shfl_sync(kFull, t, c);
+      T tc = tv[0];
+#pragma unroll
+      for (int rr = 1; rr < RPL; ++rr)
+        if ((c >> 5) == rr) tc = tv[rr];
+      const T d = __shfl_sync(kFull, tc, c & 31);
       if (!(d > T(0))) {
         okc = 0;
         if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
         break;
       }
       const T Lcc = leaf_sqrt(d);
-      if (i == c) { Ls[c][c] = Lcc; inv[c] = T(1) / Lcc; }
-      else if (i > c && i < w) Ls[i][c] = t / Lcc;
+#pragma unroll
+      for (int rr = 0; rr < RPL; ++rr) {
+        const int i = lane + 32 * rr;
+        if (i == c) { Ls[c][c] = Lcc; inv[c] = T(1) / Lcc; }
+        else if (i > c && i < w) Ls[i][c] = tv[rr] / Lcc;
+      }
       __syncwarp();
     }
     if (lane == 0) bad = !okc;
@@ -221,6 +238,7 @@ cudaError_t chol_leaf(int64_t m, int w, const T* src, int64_t lds, T* dst, int64
   if (leaf_warp_on()) {
     if (w <= 16) chol_leaf_warp_kernel<T, 16><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
     else if (w <= 32) chol_leaf_warp_kernel<T, 32><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+    else if (w <= 64) chol_leaf_warp_kernel<T, 64><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
     else return cudaErrorInvalidValue;
     count_launch();
     return cudaGetLastError();
