@@ -347,7 +347,7 @@ __device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;\
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(t32::THREADS, 2)
 gemm_tf32x3_pair_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                         const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, Tf32Params p,
-                        int vecC) {
+                        int vecC, const __grid_constant__ Raster rs) {
   using namespace t32p;
   // no early exit on p.fail here: both CTAs of the pair must reach every cluster barrier
   extern __shared__ uint8_t smem_raw[];
@@ -366,7 +366,8 @@ gemm_tf32x3_pair_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_co
   const uint32_t rank = cluster_rank();
   const int TM = (int)((p.M + BM - 1) / BM), TN = (int)((p.N + BN - 1) / BN);
   int ti, tj;
-  TT::tile_of(p.mask, blockIdx.x >> 1, TM, TN, p.off, ti, tj);
+  if (rs.ngroups > 0) TT::tile_of_raster(p.mask, blockIdx.x >> 1, TM, p.off, rs, ti, tj);
+  else TT::tile_of(p.mask, blockIdx.x >> 1, TM, TN, p.off, ti, tj);
   const int64_t i0 = (int64_t)ti * BM, j0 = (int64_t)tj * BN;
   const int64_t r0 = i0 + rank * HALF;    // this CTA's first C row
   const int nkb = (int)((p.K + BK - 1) / BK);
@@ -640,7 +641,13 @@ static cudaError_t launch_pair(const Tf32Gemm& g, cudaStream_t st) {
   static int bulk_on = [] { const char* e = getenv("SF_TF32_BULKEPI"); return e ? atoi(e) : 1; }();
   const int vecC = bulk_on && g.beta && (g.ldc % 4) == 0 && (g.ldcin % 4) == 0 && ((uintptr_t)g.Cin % 16) == 0 &&
                    ((uintptr_t)g.C % 16) == 0;
-  gemm_tf32x3_pair_kernel<<<2 * ntiles, t32::THREADS, SMEM, st>>>(mAh, mAl, mBh, mBl, p, vecC);
+  // tile order: rasterized in groups of `gb` tile columns when the operands exceed what L2
+  // keeps (SF_TF32_RASTER overrides; 0 = column order)
+  static int gb_env = [] { const char* e = getenv("SF_TF32_RASTER"); return e ? atoi(e) : -1; }();
+  Raster rs;
+  const int gb = gb_env >= 0 ? gb_env : 8;
+  if (gb > 0) TT::make_raster(g.mask, TM, TN, g.off, gb, rs);
+  gemm_tf32x3_pair_kernel<<<2 * ntiles, t32::THREADS, SMEM, st>>>(mAh, mAl, mBh, mBl, p, vecC, rs);
   count_launch();
   return cudaGetLastError();
 }
