@@ -49,19 +49,25 @@ def stale():
 def build(force=False, verbose=False):
     if not force and not stale():
         return LIB
-    objs = []
     os.makedirs(os.path.join(PKG, "build"), exist_ok=True)
-    for src in sources():
+
+    def compile_one(src):
         obj = os.path.join(PKG, "build", os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *[f for f in FLAGS if f != "-shared"], "-dc" if False else "-c",
+        cmd = [NVCC, *ARCH, *[f for f in FLAGS if f != "-shared"], "-c",
                "-I", os.path.join(ROOT, "include"), "-I", NCCL_INC, "-o", obj, src]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError(f"nvcc failed on {src}")
-        if verbose:
-            sys.stderr.write(r.stderr)
-        objs.append(obj)
+        return src, obj, r
+
+    from concurrent.futures import ThreadPoolExecutor
+    objs = []
+    with ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1))) as ex:
+        for src, obj, r in ex.map(compile_one, sources()):
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"nvcc failed on {src}")
+            if verbose:
+                sys.stderr.write(r.stderr)
+            objs.append(obj)
     cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", LIB, *objs, "-lcudart_static", "-ldl", "-lrt", "-lpthread",
            "-L" + NCCL_LIB, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + NCCL_LIB]
     subprocess.check_call(cmd)
