@@ -438,3 +438,37 @@ def test_variable_steps_invalid():
         sf.chol_steps_colmajor(4, [2, 0], d, 4, d, 4, info)
     with pytest.raises(sf.StepfactError):
         sf.chol_steps_colmajor(4, [], d, 4, d, 4, info)
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_chol_cfg5_full_size_sampled(dtype):
+    """BASELINE.json configs[4] at its full size, n = 65536, s = 512, in bench.py's launch
+    configuration (single GPU, out of place): the first K columns of L against the restricted
+    oracle (bitwise the full oracle's first K columns), a Freivalds residual of the whole
+    factor (torch fp64, an independent checker), info 0 and a positive diagonal.
+    fp64 bar R2 <= 1e-10 / residual <= 1e-13 n; fp32 (3xTF32, the fp32-rounded input) 2e-4 /
+    1e-5 n."""
+    n, s, K = 65536, 512, 256
+    A = synth.gen_torch("spd_scaled", n, seed=0)
+    if dtype == 1:
+        A = A.float()
+    info = torch.zeros(1, dtype=torch.int64, device="cuda")
+    L = torch.empty_like(A)
+    sf.chol_colmajor(n, s, A, n, L, n, info, dtype=dtype)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    Ak = np.asfortranarray(A[:K].double().cpu().numpy().T)        # first K columns (A symmetric)
+    Lo, io = oracle.chol(Ak, s, kcols=K)
+    assert io == 0
+    Lk = L[:K].double().cpu().numpy().T                            # first K columns of L (column-major rows)
+    Lk = np.tril(Lk)
+    tol = TOL64 if dtype == 0 else 2e-4
+    assert synth.r2_error(Lk, Lo[:, :K]) <= tol
+    assert bool((torch.diagonal(L.mT) > 0).all())
+    g = torch.Generator(device="cuda"); g.manual_seed(7)
+    x = torch.randn(n, 2, device="cuda", dtype=torch.float64, generator=g)
+    Ll = torch.tril(L.mT)
+    Ad = A.double() if dtype == 1 else A
+    y = Ll.double() @ (Ll.mT.double() @ x) if dtype == 1 else Ll @ (Ll.mT @ x)
+    r = float((Ad @ x - y).norm() / (Ad @ x).norm())
+    assert r <= (1e-13 if dtype == 0 else 1e-5) * n
