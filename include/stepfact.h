@@ -26,6 +26,9 @@
  *   - dtype: SF_F64 (double storage and arithmetic; the update runs on the FP64 tensor
  *     cores, DMMA) or SF_F32 (float storage; see each function).
  *   - Alignment: any; 16-byte aligned pointers with even ld take the vectorised path.
+ *   - Threads: every entry point may be called from any host thread; calls are serialized
+ *     on the host while they enqueue (the library's side streams and caches are shared),
+ *     the device work stays asynchronous.
  */
 #ifndef STEPFACT_H
 #define STEPFACT_H

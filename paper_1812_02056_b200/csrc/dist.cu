@@ -664,6 +664,7 @@ int sf_get_unique_id(uint8_t id[128]) {
 }
 
 int sf_comm_init(sf_comm_t* comm, int nranks, int rank, const uint8_t id[128]) {
+  SF_API_LOCK;
   if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks) return fail_with(SF_EINVAL, "bad communicator arguments");
   sf_comm_* c = new sf_comm_();
   c->nranks = nranks; c->rank = rank;
@@ -678,6 +679,7 @@ int sf_comm_init(sf_comm_t* comm, int nranks, int rank, const uint8_t id[128]) {
 }
 
 int sf_comm_init_loopback(sf_comm_t* comm, int nranks) {
+  SF_API_LOCK;
   if (!comm || nranks < 1) return fail_with(SF_EINVAL, "bad communicator arguments");
   sf_comm_* c = new sf_comm_();
   c->nranks = nranks; c->rank = 0;
@@ -688,6 +690,7 @@ int sf_comm_init_loopback(sf_comm_t* comm, int nranks) {
 }
 
 int sf_comm_destroy(sf_comm_t comm) {
+  SF_API_LOCK;
   if (!comm) return SF_OK;
   int rc = SF_OK;
   if (comm->nccl) {
@@ -724,6 +727,7 @@ static int check_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* con
 
 int chol_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* const* dA_local, void* const* dL_local,
                      int64_t ld_local, int64_t* const* d_info, void* stream) {
+  SF_API_LOCK;
   int rc = check_dist(comm, n, s, dtype, dA_local, dL_local, ld_local, d_info);
   if (rc) return rc;
   if (dtype == SF_F32) return chol_dist_run<float>(comm, n, s, dA_local, dL_local, ld_local, d_info, (cudaStream_t)stream);
@@ -732,6 +736,7 @@ int chol_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* cons
 
 int lu_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* const* dA_local, void* const* dLU_local,
                    int64_t ld_local, int64_t* const* d_info, void* stream) {
+  SF_API_LOCK;
   int rc = check_dist(comm, n, s, dtype, dA_local, dLU_local, ld_local, d_info);
   if (rc) return rc;
   if (dtype == SF_F32) return lu_dist_run<float>(comm, n, s, dA_local, dLU_local, ld_local, d_info, (cudaStream_t)stream);
@@ -740,6 +745,7 @@ int lu_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* const*
 
 int qr_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* const* dA_local, void* const* dQ_local,
                    void* const* dR_local, int64_t ld_local, int64_t* const* d_info, void* stream) {
+  SF_API_LOCK;
   int rc = check_dist(comm, n, s, dtype, dA_local, dQ_local, ld_local, d_info);
   if (rc) return rc;
   if (!dR_local) return fail_with(SF_EINVAL, "null pointer array");

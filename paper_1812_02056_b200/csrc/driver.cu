@@ -39,6 +39,11 @@ cudaEvent_t pool_event() {
 }
 
 
+std::recursive_mutex& api_mutex() {
+  static std::recursive_mutex m;
+  return m;
+}
+
 int fail_with(int code, const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
@@ -441,6 +446,7 @@ extern "C" {
 
 int chol_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dL, int64_t ldl, int64_t* d_info,
                 void* stream) {
+  SF_API_LOCK;
   int rc = check_common(n, s, dtype, dA, lda, dL, ldl);
   if (rc) return rc;
   if (!d_info) return fail_with(SF_EINVAL, "null d_info");
@@ -455,6 +461,7 @@ int chol_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, vo
 
 int lu_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dLU, int64_t ldlu, int64_t* d_info,
               void* stream) {
+  SF_API_LOCK;
   int rc = check_common(n, s, dtype, dA, lda, dLU, ldlu);
   if (rc) return rc;
   if (!d_info) return fail_with(SF_EINVAL, "null d_info");
@@ -469,6 +476,7 @@ int lu_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void
 
 int qr_factor(int64_t n, int64_t s, int dtype, const void* dA, int64_t lda, void* dQ, int64_t ldq, void* dR,
               int64_t ldr, int64_t* d_info, void* stream) {
+  SF_API_LOCK;
   int rc = check_common(n, s, dtype, dA, lda, dQ, ldq);
   if (rc) return rc;
   rc = check_common(n, s, dtype, dA, lda, dR, ldr);
@@ -494,6 +502,7 @@ static int check_steps(int64_t nsteps, const int64_t* steps) {
 
 int chol_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype, const void* dA, int64_t lda, void* dL,
                       int64_t ldl, int64_t* d_info, void* stream) {
+  SF_API_LOCK;
   int rc = check_common(n, 1, dtype, dA, lda, dL, ldl);
   if (!rc) rc = check_steps(nsteps, steps);
   if (rc) return rc;
@@ -506,6 +515,7 @@ int chol_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype
 
 int lu_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype, const void* dA, int64_t lda, void* dLU,
                     int64_t ldlu, int64_t* d_info, void* stream) {
+  SF_API_LOCK;
   int rc = check_common(n, 1, dtype, dA, lda, dLU, ldlu);
   if (!rc) rc = check_steps(nsteps, steps);
   if (rc) return rc;
@@ -518,6 +528,7 @@ int lu_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype, 
 
 int qr_factor_steps(int64_t n, int64_t nsteps, const int64_t* steps, int dtype, const void* dA, int64_t lda, void* dQ,
                     int64_t ldq, void* dR, int64_t ldr, int64_t* d_info, void* stream) {
+  SF_API_LOCK;
   int rc = check_common(n, 1, dtype, dA, lda, dQ, ldq);
   if (!rc) rc = check_common(n, 1, dtype, dA, lda, dR, ldr);
   if (!rc) rc = check_steps(nsteps, steps);
@@ -539,6 +550,7 @@ static int check_solve(int64_t n, int64_t nrhs, int dtype, const void* f, int64_
 }
 
 int chol_solve(int64_t n, int64_t nrhs, int dtype, const void* dL, int64_t ldl, void* dB, int64_t ldb, void* stream) {
+  SF_API_LOCK;
   int rc = check_solve(n, nrhs, dtype, dL, ldl, dB, ldb);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -547,6 +559,7 @@ int chol_solve(int64_t n, int64_t nrhs, int dtype, const void* dL, int64_t ldl, 
 }
 
 int lu_solve(int64_t n, int64_t nrhs, int dtype, const void* dLU, int64_t ldlu, void* dB, int64_t ldb, void* stream) {
+  SF_API_LOCK;
   int rc = check_solve(n, nrhs, dtype, dLU, ldlu, dB, ldb);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -556,6 +569,7 @@ int lu_solve(int64_t n, int64_t nrhs, int dtype, const void* dLU, int64_t ldlu, 
 
 int qr_solve(int64_t n, int64_t nrhs, int dtype, const void* dQ, int64_t ldq, const void* dR, int64_t ldr, void* dB,
              int64_t ldb, void* stream) {
+  SF_API_LOCK;
   int rc = check_solve(n, nrhs, dtype, dQ, ldq, dB, ldb);
   if (!rc) rc = check_solve(n, nrhs, dtype, dR, ldr, dB, ldb);
   if (rc) return rc;
@@ -568,6 +582,7 @@ int qr_solve(int64_t n, int64_t nrhs, int dtype, const void* dQ, int64_t ldq, co
 // ------------------------------------------------------------------ host-buffer variants
 static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hO1, int64_t ld1,
                      void* hO2, int64_t ld2, int64_t* info) {
+  SF_API_LOCK;
   if (n < 1 || !hA || !hO1 || !info || (kind == 2 && !hO2)) return fail_with(SF_EINVAL, "bad host arguments");
   if (lda < n || ld1 < n || (kind == 2 && ld2 < n)) return fail_with(SF_EINVAL, "leading dimension < n");
   if (s < 1 || s > n) return fail_with(SF_EINVAL, "step s=%lld outside [1, n=%lld]", (long long)s, (long long)n);
@@ -674,6 +689,7 @@ int qr_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda,
 
 // ------------------------------------------------------------------ building blocks
 int sf_chol_panel(int64_t m, int64_t w, int dtype, void* dP, int64_t ld, int64_t col0, int64_t* d_info, void* stream) {
+  SF_API_LOCK;
   if (m < 1 || w < 1 || w > m || ld < m || !dP || !d_info) return fail_with(SF_EINVAL, "bad panel arguments");
   if (dtype != SF_F64 && dtype != SF_F32) return fail_with(SF_EINVAL, "unknown dtype %d", dtype);
   cudaStream_t st = (cudaStream_t)stream;
@@ -694,6 +710,7 @@ int sf_chol_panel(int64_t m, int64_t w, int dtype, void* dP, int64_t ld, int64_t
 }
 
 int sf_syrk_sub(int64_t m, int64_t k, int dtype, const void* dR, int64_t ldr, void* dC, int64_t ldc, void* stream) {
+  SF_API_LOCK;
   if (m < 0 || k < 0 || !dR || !dC || ldr < m || ldc < m) return fail_with(SF_EINVAL, "bad syrk arguments");
   if (dtype != SF_F64 && dtype != SF_F32) return fail_with(SF_EINVAL, "unknown dtype %d", dtype);
   cudaStream_t st = (cudaStream_t)stream;
@@ -716,6 +733,7 @@ int sf_syrk_sub(int64_t m, int64_t k, int dtype, const void* dR, int64_t ldr, vo
 
 int sf_gemm_sub(int64_t m, int64_t n, int64_t k, int dtype, const void* dA, int64_t lda, int ta, const void* dB,
                 int64_t ldb, int tb, void* dC, int64_t ldc, void* stream) {
+  SF_API_LOCK;
   if (m < 0 || n < 0 || k < 0 || !dA || !dB || !dC || ldc < m) return fail_with(SF_EINVAL, "bad gemm arguments");
   if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp64 only");
   SF_CUDA(gemm_sub<double>(m, n, k, (const double*)dA, lda, ta ? 1 : 0, (const double*)dB, ldb, tb ? 0 : 1,
@@ -725,6 +743,7 @@ int sf_gemm_sub(int64_t m, int64_t n, int64_t k, int dtype, const void* dA, int6
 
 int sf_lu_panel(int64_t m, int64_t w, int64_t ncr, int dtype, void* dP, int64_t ld, int64_t col0, double tol,
                 int64_t* d_info, void* stream) {
+  SF_API_LOCK;
   if (m < 1 || w < 1 || w > m || ncr < 0 || ld < m || !dP || !d_info) return fail_with(SF_EINVAL, "bad panel arguments");
   if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp64 only");
   cudaStream_t st = (cudaStream_t)stream;
@@ -742,6 +761,7 @@ int sf_lu_panel(int64_t m, int64_t w, int64_t ncr, int dtype, void* dP, int64_t 
 
 int sf_qr_panel(int64_t n, int64_t w, int dtype, void* dV, int64_t ld, int64_t col0, double tol, int64_t* d_info,
                 void* stream) {
+  SF_API_LOCK;
   if (n < 1 || w < 1 || w > n || ld < n || !dV || !d_info) return fail_with(SF_EINVAL, "bad panel arguments");
   if (dtype != SF_F64) return fail_with(SF_ENOTSUP, "fp64 only");
   cudaStream_t st = (cudaStream_t)stream;
@@ -776,9 +796,13 @@ int64_t sf_flush_count(int64_t n, int64_t s) {
 
 int64_t sf_launch_counter(void) { return g_launches.load(); }
 
-void sf_profile_enable(int on) { g_prof = on != 0; }
+void sf_profile_enable(int on) {
+  SF_API_LOCK;
+  g_prof = on != 0;
+}
 
 int sf_profile_collect(double* ms, int64_t* count, double* flops) {
+  SF_API_LOCK;
   for (int k = 0; k < 3; ++k) { ms[k] = 0.0; count[k] = 0; flops[k] = 0.0; }
   int rc = SF_OK;
   for (auto& r : g_prof_recs) {

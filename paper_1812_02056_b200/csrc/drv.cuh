@@ -3,6 +3,7 @@
 // dispatch and the recursive panel factorizations.
 #pragma once
 #include <atomic>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -15,6 +16,12 @@
 namespace sf {
 
 int fail_with(int code, const char* fmt, ...);
+
+// Host-side serialization of the public entry points: the drivers share per-device side
+// streams, events, graph and stream caches, so concurrent calls from several host threads
+// enqueue one at a time (the GPU work itself stays asynchronous).
+std::recursive_mutex& api_mutex();
+#define SF_API_LOCK std::lock_guard<std::recursive_mutex> sf_api_lock_(sf::api_mutex())
 
 // ------------------------------------------------------------------ profiling hook
 // When enabled, CUDA event pairs are recorded on the factorization stream around every
