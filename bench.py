@@ -402,6 +402,11 @@ def main():
                      "flops_per_launch": upd_fl / upd_n if upd_n else None,
                      "update_share_of_step": upd_ms / ms if ms else None,
                      "panel_ms_per_step": pan_ms / args.steps, "qr_r_ms_per_step": qr_ms / args.steps})
+    # panel kernels: minimal HBM bytes (read + write each panel once: elt * 2 * (n - z) * w,
+    # QR: all n rows) over their device time (they run concurrently on the lookahead stream)
+    elt = 4 if dtype == "f32" else 8
+    pbytes = sum(2 * elt * ((n if kind == "qr" else n - z) * min(s, n - z)) for z in range(0, n, s))
+    roofline["panel_hbm_gbs"] = (pbytes / (pan_ms / args.steps * 1e-3) / 1e9) if pan_ms > 0 else None
 
     # ---- end to end through the public API with HOST buffers (copies inside the timed region)
     e2e = None
