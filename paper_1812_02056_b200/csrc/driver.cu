@@ -93,9 +93,10 @@ static int chol_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* L, in
       }
       if (m > w2) {  // flush, part 2: the rest of the trailing matrix, concurrently with the panel
         const int64_t c2 = c + w2;
-        ProfScope ps(0, (double)w * (double)(m - w2) * (double)(m - w2 + 1), st);
+        const double fl = (double)w * (double)(m - w2) * (double)(m - w2 + 1);
+        ProfScope ps(0, fl, st);
         SF_CUDA(gemm_sub<T>(m - w2, m - w2, w, R + w2, ldl, 0, R + w2, ldl, 0, src + c2 + c2 * lds, lds,
-                            L + c2 + c2 * ldl, ldl, kMaskLower, fail, st));
+                            L + c2 + c2 * ldl, ldl, kMaskLower, fail, st, flush_ctas_for_panel(fl)));
       }
       SF_CUDA(fork_join(*sd, sd->st, st));
     } else {
@@ -225,9 +226,10 @@ static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int
     if (la) {
       if (m > w2) {  // flush, part 2: the remaining trailing block, concurrently with the panel
         const int64_t c2 = c + w2;
-        ProfScope ps(0, 2.0 * w * (double)(m - w2) * (double)(m - w2), st);
+        const double fl = 2.0 * w * (double)(m - w2) * (double)(m - w2);
+        ProfScope ps(0, fl, st);
         SF_CUDA(gemm_sub<T>(m - w2, m - w2, w, RL + w2, ldd, 0, RU + w2 * ldd, ldd, 1, src + c2 + c2 * lds, lds,
-                            LU + c2 + c2 * ldd, ldd, kMaskNone, fail, st));
+                            LU + c2 + c2 * ldd, ldd, kMaskNone, fail, st, flush_ctas_for_panel(fl)));
       }
       SF_CUDA(fork_join(*sd, pst, st));
     }

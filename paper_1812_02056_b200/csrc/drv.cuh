@@ -210,12 +210,14 @@ struct Gemm {
   int splits; T* work;
   const long long* fail;
   int64_t off = 0;   // mask diagonal offset (lower: i >= j + off, upper: i <= j + off)
+  int max_ctas = 0;  // fp64: bounded grid (0 = one CTA per tile)
 };
 
 inline cudaError_t run_gemm(const Gemm<double>& g, cudaStream_t st) {
   GemmF64 p{g.M, g.N, g.K, g.A, g.lda, g.B, g.ldb, g.Cin, g.ldcin, g.C, g.ldc,
             g.alpha, g.beta, g.splits, g.work, g.fail};
   p.off = g.off;
+  p.max_ctas = g.max_ctas;
   return gemm_f64(p, g.ak, g.bk, g.mask, st);
 }
 // fp32: split op(A) and op(B) once into K-major hi/lo copies (stream-ordered scratch), then
@@ -252,9 +254,32 @@ inline cudaError_t run_gemm(const Gemm<float>& g, cudaStream_t st) {
 template <typename T>
 inline cudaError_t gemm_sub(int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, int ak, const T* B,
                             int64_t ldb, int bk, const T* Cin, int64_t ldcin, T* C, int64_t ldc, int mask,
-                            const long long* fail, cudaStream_t st) {
+                            const long long* fail, cudaStream_t st, int max_ctas = 0) {
   Gemm<T> g{M, N, K, A, lda, ak, B, ldb, bk, Cin, ldcin, C, ldc, -1.0, 1, mask, 1, nullptr, fail};
+  g.max_ctas = max_ctas;
   return run_gemm(g, st);
+}
+
+// SM reservation for the lookahead panel.  The flush's second part runs concurrently with
+// the factorization of the next panel; the panel is a chain of ~30 short dependent kernels,
+// and when the flush holds every SM each of them waits for a flush CTA to retire.  When the
+// remaining flush is small (its flops per panel-step below SF_RESERVE_FLOPS, default 4e10,
+// i.e. ~1.5 ms), the flush can run on a bounded grid that leaves SF_PANEL_SMS SMs to the
+// panel stream.  Off by default: measured on cfg2/cfg3/cfg5 it changes the time by < 1%
+// (the panel chain is bound by its own latency, not by waiting for SMs) and costs cfg2 3%.
+// Returns the CTA bound for gemm_sub (0 = unbounded).
+inline int flush_ctas_for_panel(double flush_flops) {
+  static const int reserve = [] { const char* e = getenv("SF_PANEL_SMS"); return e ? atoi(e) : 0; }();
+  static const double thresh = [] { const char* e = getenv("SF_RESERVE_FLOPS"); return e ? atof(e) : 4e10; }();
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  if (reserve <= 0 || flush_flops > thresh || reserve >= sms) return 0;
+  return 2 * (sms - reserve);   // two CTAs per SM on the others
 }
 
 // ------------------------------------------------------------------ Cholesky

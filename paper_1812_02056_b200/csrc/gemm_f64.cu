@@ -269,6 +269,17 @@ __global__ void __launch_bounds__(g64::THREADS, 2) gemm_f64_kernel(GemmF64 p, in
   gemm_f64_body<AK, BKC, V16, MASK>(p, blockIdx.x, vecC);
 }
 
+// Bounded grid (max_ctas > 0): each CTA loops over tiles, leaving SMs to a concurrent stream.
+template <bool AK, bool BKC, bool V16, int MASK>
+__global__ void __launch_bounds__(g64::THREADS, 2) gemm_f64_loop_kernel(GemmF64 p, int vecC) {
+  if (p.fail && failed(p.fail)) return;
+#pragma unroll 1
+  for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+    gemm_f64_body<AK, BKC, V16, MASK>(p, t, vecC);
+    __syncthreads();   // shared memory is reused by the next tile
+  }
+}
+
 // Grouped launch: several independent C blocks sharing K, the operand leading dimensions
 // and the mask, one CTA grid (the block-cyclic distributed updates).
 template <bool AK, bool BKC, bool V16, int MASK>
@@ -304,12 +315,18 @@ static cudaError_t launch_t(const GemmF64& p, const GemmGroups* gs, int ntiles, 
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_f64_grouped_kernel<AK, BKC, V16, MASK>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g64::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_f64_loop_kernel<AK, BKC, V16, MASK>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g64::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   dim3 grid(ntiles, p.splits);
   if (gs) gemm_f64_grouped_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, *gs, vecC);
-  else gemm_f64_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, vecC);
+  else if (p.max_ctas > 0 && p.max_ctas < ntiles) {
+    grid.x = p.max_ctas;
+    gemm_f64_loop_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, vecC);
+  } else gemm_f64_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, vecC);
   count_launch();
   return cudaGetLastError();
 }
@@ -354,6 +371,7 @@ cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStre
   const int ntiles = masked_tiles(mask, TM, TN, p.off);
   if (ntiles == 0) return cudaSuccess;
   T64::make_raster(mask, TM, TN, p.off, kGroupCols, p.rs);
+  p.ntiles = ntiles;
   const bool v16 = aligned16(p.A, p.lda) && aligned16(p.B, p.ldb);
   const int vecC = aligned16(p.C, p.ldc) && (!p.beta || aligned16(p.Cin, p.ldcin));
   cudaError_t e = launch_key(p, nullptr, a_kcontig, b_kcontig, v16, mask, ntiles, vecC, st);

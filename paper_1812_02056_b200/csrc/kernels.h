@@ -30,6 +30,8 @@ struct GemmF64 {
   const long long* fail;   // device "first failed column" word; kernels exit early if set
   int64_t off = 0;         // mask diagonal offset: lower keeps i >= j + off, upper i <= j + off
   Raster rs;               // tile rasterization (filled by the launcher)
+  int max_ctas = 0;        // > 0: at most this many CTAs, each looping over tiles (leaves SMs free)
+  int ntiles = 0;          // set by the launcher
 };
 cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStream_t st);
 
