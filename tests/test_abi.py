@@ -88,3 +88,25 @@ def test_sass_is_sm100a_tensor_core():
     out = subprocess.run([exe, "-sass", sf.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     assert "DMMA.8x8x4" in out
+
+
+def test_new_entry_points_reject_bad_arguments(L):
+    """Argument errors of the variable-step, solve and distributed entry points come back
+    synchronously as SF_EINVAL with nothing enqueued (no GPU needed)."""
+    buf = (ctypes.c_double * 64)()
+    p = ctypes.addressof(buf)
+    info = ctypes.addressof(ctypes.c_int64(0))
+    steps_bad = (ctypes.c_int64 * 2)(2, 0)
+    steps_ok = (ctypes.c_int64 * 1)(2)
+    assert L.chol_factor_steps(4, 2, steps_bad, 0, p, 4, p, 4, info, None) == 1
+    assert L.chol_factor_steps(4, 0, steps_ok, 0, p, 4, p, 4, info, None) == 1
+    assert L.lu_factor_steps(4, 1, steps_ok, 0, p, 3, p, 3, info, None) == 1          # lda < n
+    assert L.qr_factor_steps(4, 1, steps_ok, 7, p, 4, p, 4, p, 4, info, None) == 1    # dtype
+    assert L.chol_solve(0, 1, 0, p, 4, p, 4, None) == 1
+    assert L.lu_solve(4, 1, 0, p, 3, p, 4, None) == 1
+    assert L.qr_solve(4, 1, 0, None, 4, p, 4, p, 4, None) == 1
+    arr = (ctypes.c_void_p * 1)(p)
+    iarr = (ctypes.c_void_p * 1)(info)
+    assert L.chol_factor_dist(None, 4, 2, 0, arr, arr, 4, iarr, None) == 1             # null comm
+    assert L.sf_comm_init_loopback(None, 2) == 1
+    assert L.sf_local_cols(10, 3, 2, 5) == 0
