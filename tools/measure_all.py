@@ -32,9 +32,9 @@ def run(kind, n, s, A, dtype=sf.SF_F64, reps=5, warm=2):
         if kind == "chol":
             sf.chol_colmajor(n, s, A, n, o1, n, info, dtype=dtype, stream=st)
         elif kind == "lu":
-            sf.lu_colmajor(n, s, A, n, o1, n, info, stream=st)
+            sf.lu_colmajor(n, s, A, n, o1, n, info, dtype=dtype, stream=st)
         else:
-            sf.qr_colmajor(n, s, A, n, o1, n, o2, n, info, stream=st)
+            sf.qr_colmajor(n, s, A, n, o1, n, o2, n, info, dtype=dtype, stream=st)
     for _ in range(warm):
         once()
     torch.cuda.synchronize()
@@ -79,12 +79,14 @@ def configs():
     res.append(run("chol", 256, 16, A) | {"config": "configs[0]"})
     A = colmajor(torch.from_numpy(synth.gen_numpy("diag_dominant", 4096, 0)).cuda())
     res.append(run("lu", 4096, 64, A) | {"config": "configs[1]"})
+    res.append(run("lu", 4096, 64, A.float(), dtype=sf.SF_F32) | {"config": "configs[1] fp32"})
     A = synth.gen_torch("spd_scaled", 16384, 0)
     res.append(run("chol", 16384, 512, A) | {"config": "configs[2] s=512"})
     res.append(run("chol", 16384, 512, A.float(), dtype=sf.SF_F32) | {"config": "configs[2] s=512, fp32"})
     del A
     A = colmajor(synth.gen_torch("gaussian", 8192, 0))
     res.append(run("qr", 8192, 128, A) | {"config": "configs[3]"})
+    res.append(run("qr", 8192, 128, A.float(), dtype=sf.SF_F32) | {"config": "configs[3] fp32"})
     del A
     torch.cuda.empty_cache()
     A = synth.gen_torch("spd_scaled", 65536, 0)
