@@ -363,6 +363,128 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_kernel(int64_t m, int64_t ncr,
     if (lane < w) dst[lane + (j0 + jj) * ldd] = S[jj][lane];
 }
 
+// Variant (default): ONE warp runs the diagonal-block Crout in shared memory (lane i: row i
+// of L and column i of U; no shuffle chains) while the other warps already load their rows
+// below / stage their U columns; then one __syncthreads and the independent substitutions.
+// Same per-element arithmetic as lu_leaf_kernel (interleaved partial sums, one subtraction,
+// U_ci = t / L_cc in the block, * 1/L_cc for the U columns).
+template <typename T, int W>
+__global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t ncr, int w, const T* __restrict__ src,
+                                                              int64_t lds, T* __restrict__ dst, int64_t ldd,
+                                                              int64_t col0, const T* tolp, long long* fail,
+                                                              int nrow_blocks) {
+  if (failed(fail)) return;
+  __shared__ T Ls[W][W + 1];     // L11 (Ls[i][k] = L_ik)
+  __shared__ T Us[W][W + 1];     // U11 (Us[k][j] = U_kj)
+  __shared__ T inv[W];
+  __shared__ T S[kUCols][W + 1]; // staging for the U columns
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool rowblock = (int)blockIdx.x < nrow_blocks;
+  const int64_t r = w + (int64_t)blockIdx.x * kLeafT + tid;
+  const int64_t j0 = w + (int64_t)(blockIdx.x - nrow_blocks) * kUCols;
+  const int ncols = rowblock ? 0 : (int)((w + ncr - j0) < kUCols ? (w + ncr - j0) : kUCols);
+  if (warp == 0) {
+    const T tol = __ldcg(tolp);
+    if (lane < W)
+      for (int k = 0; k < W; ++k) {
+        const bool in = lane < w && k < w;
+        Ls[lane][k] = (in && k <= lane) ? __ldcg(src + lane + (int64_t)k * lds) : T(0);
+        Us[k][lane] = (in && k < lane) ? __ldcg(src + k + (int64_t)lane * lds) : T(0);
+      }
+    __syncwarp();
+    int okc = 1;
+    for (int c = 0; c < w; ++c) {
+      const int i = lane;
+      T a0 = T(0), a1 = T(0), b0 = T(0), b1 = T(0);
+      if (i >= c && i < w) {
+        for (int k = 0; k < c; ++k) {
+          if (k & 1) { a1 = fma(-Ls[i][k], Us[k][c], a1); b1 = fma(-Ls[c][k], Us[k][i], b1); }
+          else { a0 = fma(-Ls[i][k], Us[k][c], a0); b0 = fma(-Ls[c][k], Us[k][i], b0); }
+        }
+      }
+      const T tL = (i < w) ? Ls[i][c] + (a0 + a1) : T(0);
+      const T tU = (i < w) ? Us[c][i] + (b0 + b1) : T(0);
+      const T Lcc = __shfl_sync(kFull, tL, c);
+      if (!(fabs(Lcc) >= tol)) {
+        okc = 0;
+        if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
+        break;
+      }
+      if (i >= c && i < w) Ls[i][c] = tL;
+      if (i > c && i < w) Us[c][i] = tU / Lcc;
+      if (i == c) inv[c] = T(1) / Lcc;
+      __syncwarp();
+    }
+    if (lane == 0) bad = !okc;
+  } else if (!rowblock) {
+    // warps 1..3 stage the U columns while warp 0 factors the block
+    for (int jj = warp - 1; jj < ncols; jj += kLeafT / 32 - 1)
+      if (lane < w) S[jj][lane] = __ldcg(src + lane + (j0 + jj) * lds);
+  }
+  T x[W];
+  if (rowblock && r < m) {
+#pragma unroll
+    for (int k = 0; k < W; ++k) x[k] = (k < w) ? __ldcg(src + r + (int64_t)k * lds) : T(0);
+  }
+  __syncthreads();
+  if (bad) return;
+  if (last_reader(fail + 1)) {   // see chol_leaf_kernel
+    for (int idx = tid; idx < w * w; idx += kLeafT) {
+      const int i = idx % w, k = idx / w;
+      dst[i + (int64_t)k * ldd] = (k <= i) ? Ls[i][k] : Us[i][k];   // L incl. diagonal / U strict upper
+    }
+  }
+  if (rowblock) {
+    // L rows below: L_rc = A_rc - sum_{k<c} L_rk U_kc
+    if (r >= m) return;
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
+#pragma unroll
+      for (int k = 0; k < c; ++k) {
+        if ((k & 3) == 0) a0 = fma(-x[k], Us[k][c], a0);
+        else if ((k & 3) == 1) a1 = fma(-x[k], Us[k][c], a1);
+        else if ((k & 3) == 2) a2 = fma(-x[k], Us[k][c], a2);
+        else a3 = fma(-x[k], Us[k][c], a3);
+      }
+      x[c] = (a0 + a1) + (a2 + a3);
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+      if (k < w) dst[r + (int64_t)k * ldd] = x[k];
+    return;
+  }
+  // U columns to the right: U_cj = (A_cj - sum_{k<c} L_ck U_kj) / L_cc
+  if (tid < ncols) {
+    T y[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) y[k] = (k < w) ? S[tid][k] : T(0);
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      T a0 = y[c], a1 = T(0), a2 = T(0), a3 = T(0);
+#pragma unroll
+      for (int k = 0; k < c; ++k) {
+        if ((k & 3) == 0) a0 = fma(-Ls[c][k], y[k], a0);
+        else if ((k & 3) == 1) a1 = fma(-Ls[c][k], y[k], a1);
+        else if ((k & 3) == 2) a2 = fma(-Ls[c][k], y[k], a2);
+        else a3 = fma(-Ls[c][k], y[k], a3);
+      }
+      y[c] = ((a0 + a1) + (a2 + a3)) * inv[c];
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) S[tid][k] = y[k];
+  }
+  __syncthreads();
+  for (int jj = warp; jj < ncols; jj += kLeafT / 32)
+    if (lane < w) dst[lane + (j0 + jj) * ldd] = S[jj][lane];
+}
+
+static bool lu_leaf_warp_on() {
+  static int on = [] { const char* e = getenv("SF_LU_LEAF_WARP"); return e ? atoi(e) : 1; }();
+  return on != 0;
+}
+
 template <typename T>
 cudaError_t lu_leaf(int64_t m, int64_t ncr, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
                     const T* tol, long long* fail, cudaStream_t st) {
@@ -372,7 +494,12 @@ cudaError_t lu_leaf(int64_t m, int64_t ncr, int w, const T* src, int64_t lds, T*
   const int ncb = ncr > 0 ? (int)((ncr + kUCols - 1) / kUCols) : 0;
   int grid = nrb + ncb;
   if (grid == 0) grid = 1;
-  if (w <= 16) lu_leaf_kernel<T, 16><<<grid, kLeafT, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
+  if (lu_leaf_warp_on()) {
+    if (w <= 16) lu_leaf_warp_kernel<T, 16><<<grid, kLeafT, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
+    else if (w <= 32)
+      lu_leaf_warp_kernel<T, 32><<<grid, kLeafT, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
+    else return cudaErrorInvalidValue;
+  } else if (w <= 16) lu_leaf_kernel<T, 16><<<grid, kLeafT, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
   else if (w <= 32) lu_leaf_kernel<T, 32><<<grid, kLeafT, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
   else return cudaErrorInvalidValue;
   count_launch();
