@@ -133,8 +133,8 @@ __global__ void __launch_bounds__(kLeafT) chol_leaf_kernel(int64_t m, int w, con
 // their rows below from HBM; one __syncthreads, then the substitutions.  Same arithmetic per
 // element as chol_leaf_kernel (k-sums in four interleaved partial sums, then one
 // subtraction, sqrt, division by L_cc in the block, multiplication by 1/L_cc below).
-template <typename T, int W>
-__global__ void __launch_bounds__(kLeafT) chol_leaf_warp_kernel(int64_t m, int w, const T* __restrict__ src,
+template <typename T, int W, int NT>
+__global__ void __launch_bounds__(NT) chol_leaf_warp_kernel(int64_t m, int w, const T* __restrict__ src,
                                                                 int64_t lds, T* __restrict__ dst, int64_t ldd,
                                                                 int64_t col0, long long* fail) {
   if (failed(fail)) return;
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kLeafT) chol_leaf_warp_kernel(int64_t m, int w
   __shared__ T inv[W];
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t r = w + (int64_t)blockIdx.x * kLeafT + tid;
+  const int64_t r = w + (int64_t)blockIdx.x * NT + tid;
   T x[W];
   if (warp == 0) {
     constexpr int RPL = (W + 31) / 32;   // diagonal-block rows per lane: lane + 32*rr
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kLeafT) chol_leaf_warp_kernel(int64_t m, int w
   __syncthreads();
   if (bad) return;
   if (last_reader(fail + 1)) {
-    for (int idx = tid; idx < w * w; idx += kLeafT) {
+    for (int idx = tid; idx < w * w; idx += NT) {
       const int i = idx % w, k = idx / w;
       if (k <= i) dst[i + (int64_t)k * ldd] = Ls[i][k];
     }
@@ -236,10 +236,22 @@ cudaError_t chol_leaf(int64_t m, int w, const T* src, int64_t lds, T* dst, int64
   const int64_t below = m - w;
   const int grid = below > 0 ? (int)((below + kLeafT - 1) / kLeafT) : 1;
   if (leaf_warp_on()) {
-    if (w <= 16) chol_leaf_warp_kernel<T, 16><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-    else if (w <= 32) chol_leaf_warp_kernel<T, 32><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-    else if (w <= 64) chol_leaf_warp_kernel<T, 64><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-    else return cudaErrorInvalidValue;
+    // SF_LEAF_NT=64: 64-thread CTAs (~6.4K registers) fit on an SM next to two flush CTAs, so
+    // the lookahead panel's leaves need not wait for flush CTAs to retire — measured no
+    // faster (cfg3 61.4 vs 61.5 ms), default 128
+    static const int nt = [] { const char* e = getenv("SF_LEAF_NT"); return (e && atoi(e) == 64) ? 64 : 128; }();
+    if (nt == 64) {
+      const int g64 = below > 0 ? (int)((below + 63) / 64) : 1;
+      if (w <= 16) chol_leaf_warp_kernel<T, 16, 64><<<g64, 64, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+      else if (w <= 32) chol_leaf_warp_kernel<T, 32, 64><<<g64, 64, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+      else if (w <= 64) chol_leaf_warp_kernel<T, 64, 64><<<g64, 64, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+      else return cudaErrorInvalidValue;
+    } else {
+      if (w <= 16) chol_leaf_warp_kernel<T, 16, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+      else if (w <= 32) chol_leaf_warp_kernel<T, 32, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+      else if (w <= 64) chol_leaf_warp_kernel<T, 64, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+      else return cudaErrorInvalidValue;
+    }
     count_launch();
     return cudaGetLastError();
   }
