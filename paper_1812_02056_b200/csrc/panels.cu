@@ -23,8 +23,12 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 
 namespace sf {
@@ -58,7 +62,11 @@ static MgsGeom mgs_geom(int64_t n, int w, int elt) {
 size_t qr_mgs_work_elems(int64_t n, int w, int elt) {
   MgsGeom g = mgs_geom(n, w, elt);
   // flags[2][G] (int) + partials[2][w][G] (T), in units of T
-  return (2 * (size_t)g.G * sizeof(int) + elt - 1) / elt + 2 * (size_t)g.G * (size_t)w + 2;
+  const size_t flag = (2 * (size_t)g.G * sizeof(int) + elt - 1) / elt + 2 * (size_t)g.G * (size_t)w + 2;
+  // LL exchange: words[2][Q][w] of 16 (fp64) / 8 (fp32) bytes, Q <= ceil(n / 128) clusters, + alignment
+  const size_t Q = (size_t)((n + 127) / 128);
+  const size_t ll = (2 * Q * (size_t)w * (elt == 8 ? 16 : 8) + 256) / elt;
+  return flag > ll ? flag : ll;
 }
 
 // Inter-CTA exchange for a cooperative (co-resident) grid, without atomics: CTA g publishes
@@ -329,10 +337,228 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_reg_kernel(int64_t n, int 
   }
 }
 
+// ---------------------------------------------------------------- cluster + LL exchange
+// The variant used whenever it fits (w <= 128, <= 128 rows per CTA, the clusters
+// co-resident): the same register-resident column step as qr_mgs_reg_kernel, but the
+// Gram-row exchange is two-level.
+//   1. inside a thread-block cluster of CL CTAs the partial rows meet in distributed shared
+//      memory: after a cluster barrier, CTA k of the cluster sums (in rank order) the CL
+//      partials of columns j = c + k (mod CL) and publishes the cluster sum;
+//   2. the Q = G / CL cluster sums go through global memory as "LL" words: each 64-bit word
+//      carries 32 data bits and the 32-bit epoch (col0 + c + 1) of the column they belong
+//      to, so a reader polls the data itself — a word whose epoch matches is valid (64-bit
+//      accesses are single-copy atomic), no separate flag, no fence, one L2 round trip.
+//      Every CTA reads all Q sums of every remaining column and adds them in cluster order,
+//      so all CTAs hold bitwise the same Gram row (and take the same break decision).
+// Measured on B200 (calib/mgs_probe.cu, n = 8192, w = 128): 3.8 us per column against
+// 5.6 us for the flag exchange of qr_mgs_reg_kernel (its partial reads alone took 2.8 us).
+// Buffer reuse: slot (c & 1, q, j) is rewritten at column c + 2 only after the writer's
+// cluster passed the cluster barrier of column c + 2, i.e. after every CTA of every cluster
+// polled column c + 1, hence finished reading column c.  Epochs grow across the launches of
+// one factorization and the buffer is zeroed at its start, so a stale word never matches.
+template <typename T> struct LL;
+template <> struct LL<double> {
+  static constexpr int kWords = 2;
+  static __device__ __forceinline__ void put(unsigned long long* p, double v, unsigned ep) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const unsigned long long w0 = ((unsigned long long)ep << 32) | (b & 0xffffffffull);
+    const unsigned long long w1 = ((unsigned long long)ep << 32) | (b >> 32);
+    asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+  }
+  static __device__ __forceinline__ bool get(const unsigned long long* p, unsigned ep, double& v) {
+    unsigned long long w0, w1;
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+    if ((unsigned)(w0 >> 32) != ep || (unsigned)(w1 >> 32) != ep) return false;
+    v = __longlong_as_double((long long)((w1 << 32) | (w0 & 0xffffffffull)));
+    return true;
+  }
+};
+template <> struct LL<float> {
+  static constexpr int kWords = 1;
+  static __device__ __forceinline__ void put(unsigned long long* p, float v, unsigned ep) {
+    const unsigned long long w0 = ((unsigned long long)ep << 32) | (unsigned long long)__float_as_uint(v);
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(w0) : "memory");
+  }
+  static __device__ __forceinline__ bool get(const unsigned long long* p, unsigned ep, float& v) {
+    unsigned long long w0;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(w0) : "l"(p) : "memory");
+    if ((unsigned)(w0 >> 32) != ep) return false;
+    v = __uint_as_float((unsigned)(w0 & 0xffffffffull));
+    return true;
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w, int RB, const T* __restrict__ src,
+                                                                int64_t lds, T* __restrict__ dst, int64_t ldd,
+                                                                int64_t col0, const T* tolp,
+                                                                unsigned long long* ll, long long* fail) {
+  if (failed(fail)) return;      // stable during the launch: every CTA of a cluster agrees
+  constexpr int QP = kMgsRPT + 2;
+  __shared__ T qs[2 * QP], vs[2 * QP];
+  __shared__ T gsum[128];
+  __shared__ T mypart[2][128];
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* cval = reinterpret_cast<T*>(smraw);   // cval[q * w + j]: cluster q's sum for column j
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks(), k = (int)cluster.block_rank();
+  const int tid = threadIdx.x;
+  const int G = gridDim.x, g = blockIdx.x, Q = G / CL, q = g / CL;
+  const int64_t r0 = (int64_t)g * RB;
+  const int rows = (int)((r0 + RB <= n) ? RB : (n > r0 ? n - r0 : 0));
+  const T tol = __ldcg(tolp);
+  const int cp = tid >> 1, h = tid & 1;        // my column and half
+  const int rbase = h * kMgsRPT;
+  const bool mine = cp < w;
+  T x[kMgsRPT];
+#pragma unroll
+  for (int r = 0; r < kMgsRPT; ++r) {
+    const int rr = rbase + r;
+    x[r] = (mine && rr < rows) ? __ldcg(src + r0 + rr + (int64_t)cp * lds) : T(0);
+  }
+  if (cp == 0) {
+#pragma unroll
+    for (int r = 0; r < kMgsRPT; ++r) vs[h * QP + r] = x[r];
+  }
+  __syncthreads();
+  {
+    T acc = T(0);
+#pragma unroll
+    for (int r = 0; r < kMgsRPT; ++r) acc = fma(vs[h * QP + r], x[r], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (mine && h == 0) mypart[0][cp] = acc;
+  }
+
+  bool ok = true;
+  for (int c = 0; c < w; ++c) {
+    const int buf = c & 1;
+    const unsigned ep = (unsigned)(col0 + c + 1);
+    cluster.sync();   // every CTA of the cluster wrote its partial row of column c
+    for (int j = c + k + CL * tid; j < w; j += CL * kMgsThreads) {
+      T a = T(0);
+      for (int rr = 0; rr < CL; ++rr) a += cluster.map_shared_rank(&mypart[buf][0], rr)[j];
+      LL<T>::put(ll + LL<T>::kWords * ((size_t)(buf * Q + q) * w + j), a, ep);
+    }
+    const int wc = w - c, cnt = Q * wc;
+    for (int idx = tid; idx < cnt; idx += kMgsThreads) {
+      const int qq = idx / wc, j = c + idx % wc;
+      const unsigned long long* p = ll + LL<T>::kWords * ((size_t)(buf * Q + qq) * w + j);
+      T v;
+      while (!LL<T>::get(p, ep, v)) {}
+      cval[qq * w + j] = v;
+    }
+    __syncthreads();
+    for (int j = c + tid; j < w; j += kMgsThreads) {
+      T a = T(0);
+      for (int qq = 0; qq < Q; ++qq) a += cval[qq * w + j];
+      gsum[j] = a;
+    }
+    __syncthreads();
+    const T nv = dsqrt(gsum[c]);
+    if (!(nv >= tol)) {
+      if (g == 0 && tid == 0) record_fail(fail, col0 + c + 1);
+      ok = false;
+      break;
+    }
+    const T rnv = T(1) / nv;
+    if (cp == c) {
+#pragma unroll
+      for (int r = 0; r < kMgsRPT; ++r) { x[r] = x[r] * rnv; qs[h * QP + r] = x[r]; }
+    }
+    if (cp == c + 1) {
+#pragma unroll
+      for (int r = 0; r < kMgsRPT; ++r) vs[h * QP + r] = x[r];
+    }
+    __syncthreads();
+    const bool act = mine && cp > c;
+    T acc = T(0);
+    if (act) {
+      const T coef = gsum[cp] * rnv;                        // q_c^T v_cp
+      const T cn = (c + 1 < w) ? gsum[c + 1] * rnv : T(0);  // q_c^T v_{c+1}
+#pragma unroll
+      for (int r = 0; r < kMgsRPT; ++r) {
+        const T qr = qs[h * QP + r];
+        x[r] = fma(-qr, coef, x[r]);                         // v_cp -= q_c (q_c^T v_cp)
+        acc = fma(fma(-qr, cn, vs[h * QP + r]), x[r], acc);  // <v_{c+1}, v_cp> (both updated)
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (act && h == 0 && c + 1 < w) mypart[buf ^ 1][cp] = acc;
+  }
+  cluster.sync();   // no CTA leaves while a cluster peer may still read its shared memory
+  if (!ok || !mine) return;
+#pragma unroll
+  for (int r = 0; r < kMgsRPT; ++r) {
+    const int rr = rbase + r;
+    if (rr < rows) dst[r0 + rr + (int64_t)cp * ldd] = x[r];
+  }
+}
+
+struct LLGeom { int G = 0, CL = 0, RB = 0; size_t dyn = 0; };
+
+// Grid for the LL kernel, or G = 0 when it does not apply (then the flag-exchange kernels).
+template <typename T>
+static LLGeom ll_geom(int64_t n, int w) {
+  LLGeom r;
+  if (w > 128 || getenv("SF_MGS_NOLL") != nullptr) return r;
+  const int64_t G0 = (n + 2 * kMgsRPT - 1) / (2 * kMgsRPT);
+  static int maxcl[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};   // co-resident clusters per size
+  auto fits = [&](int CL, int G) -> bool {
+    if (maxcl[CL] < 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(kMgsThreads);
+      cfg.dynamicSmemBytes = 0;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int m = 0;
+      if (cudaOccupancyMaxActiveClusters(&m, (void*)qr_mgs_ll_kernel<T>, &cfg) != cudaSuccess) { cudaGetLastError(); m = 0; }
+      maxcl[CL] = m;
+    }
+    return G / CL <= maxcl[CL];
+  };
+  int G = 0, CL = 0;
+  if (G0 <= 8) { G = (int)G0; CL = (int)G0; }
+  else {
+    for (int cl : {8, 4}) {
+      const int g = (int)((G0 + cl - 1) / cl * cl);
+      if (fits(cl, g)) { G = g; CL = cl; break; }
+    }
+  }
+  if (G == 0 || (G <= 8 && !fits(CL, G))) return r;
+  r.G = G; r.CL = CL;
+  r.RB = (int)((n + G - 1) / G);
+  if (r.RB > 2 * kMgsRPT) return LLGeom{};
+  r.dyn = sizeof(T) * (size_t)(G / CL) * (size_t)w;
+  return r;
+}
+
 template <typename T>
 cudaError_t qr_mgs_panel(int64_t n, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
                          const T* tol, T* work, long long* fail, cudaStream_t st) {
   if (w <= 0) return cudaSuccess;
+  const LLGeom lg = ll_geom<T>(n, w);
+  if (lg.G > 0) {
+    unsigned long long* ll = reinterpret_cast<unsigned long long*>(((uintptr_t)work + 255) & ~(uintptr_t)255);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(lg.G);
+    cfg.blockDim = dim3(kMgsThreads);
+    cfg.dynamicSmemBytes = lg.dyn;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = lg.CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;   // all clusters co-resident (they wait on each other)
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    int RB = lg.RB;
+    count_launch();
+    return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
+  }
   MgsGeom g = mgs_geom(n, w, (int)sizeof(T));
   if (g.smem > 220 * 1024) return cudaErrorInvalidValue;   // caller splits wider panels
   if (g.RB > 32 * kMgsRJ) return cudaErrorNotSupported;     // rows per CTA beyond the register budget
