@@ -496,6 +496,34 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
 
 struct LLGeom { int G = 0, CL = 0, RB = 0; size_t dyn = 0; };
 
+// The MGS grids are persistent: their CTAs wait on each other, so two of them running at
+// once on one device (two QR calls on different streams) could each hold part of the SMs
+// and wait forever for the rest.  Eager launches are therefore chained per device: a launch
+// on another stream than the previous one first waits for the previous launch's event.
+// (Launches recorded into a CUDA graph are not chained; DESIGN.md §5 K7.)
+struct MgsOrder {
+  static constexpr int kMaxDev = 64;
+  static cudaEvent_t ev[kMaxDev];
+  static cudaStream_t last[kMaxDev];
+  int dev = -1;
+  cudaStream_t st;
+  explicit MgsOrder(cudaStream_t s) : st(s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (getenv("SF_MGS_NOORDER") != nullptr) return;   // experiment switch only
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) { cudaGetLastError(); return; }
+    if (cs != cudaStreamCaptureStatusNone || cudaGetDevice(&dev) != cudaSuccess || dev >= kMaxDev) { dev = -1; return; }
+    if (ev[dev] != nullptr && last[dev] != st) cudaStreamWaitEvent(st, ev[dev], 0);
+  }
+  ~MgsOrder() {
+    if (dev < 0) return;
+    if (ev[dev] == nullptr && cudaEventCreateWithFlags(&ev[dev], cudaEventDisableTiming) != cudaSuccess) { ev[dev] = nullptr; return; }
+    cudaEventRecord(ev[dev], st);
+    last[dev] = st;
+  }
+};
+cudaEvent_t MgsOrder::ev[MgsOrder::kMaxDev] = {};
+cudaStream_t MgsOrder::last[MgsOrder::kMaxDev] = {};
+
 // Grid for the LL kernel, or G = 0 when it does not apply (then the flag-exchange kernels).
 template <typename T>
 static LLGeom ll_geom(int64_t n, int w) {
@@ -540,6 +568,7 @@ template <typename T>
 cudaError_t qr_mgs_panel(int64_t n, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
                          const T* tol, T* work, long long* fail, cudaStream_t st) {
   if (w <= 0) return cudaSuccess;
+  MgsOrder order(st);
   const LLGeom lg = ll_geom<T>(n, w);
   if (lg.G > 0) {
     unsigned long long* ll = reinterpret_cast<unsigned long long*>(((uintptr_t)work + 255) & ~(uintptr_t)255);

@@ -472,3 +472,29 @@ def test_chol_cfg5_full_size_sampled(dtype):
     y = Ll.double() @ (Ll.mT.double() @ x) if dtype == 1 else Ll @ (Ll.mT @ x)
     r = float((Ad @ x - y).norm() / (Ad @ x).norm())
     assert r <= (1e-13 if dtype == 0 else 1e-5) * n
+
+
+@pytest.mark.timeout(300, method="thread")
+def test_qr_concurrent_streams():
+    """The MGS panel grid is persistent (its CTAs wait on each other).  Several QR calls on
+    different streams at once must neither deadlock (DESIGN.md §5 K7: eager panel launches
+    are chained per device) nor change a bit of each other's results."""
+    n, s = 8192, 128
+    A = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    info = torch.zeros(1, dtype=torch.int64, device="cuda")
+    Q0, R0 = torch.empty_like(A), torch.empty_like(A)
+    sf.qr_colmajor(n, s, A, n, Q0, n, R0, n, info)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    outs = []
+    for st in streams:
+        Q, R = torch.empty_like(A), torch.empty_like(A)
+        inf = torch.zeros(1, dtype=torch.int64, device="cuda")
+        torch.cuda.current_stream().synchronize()
+        sf.qr_colmajor(n, s, A, n, Q, n, R, n, inf, stream=st)
+        outs.append((Q, R, inf))
+    torch.cuda.synchronize()
+    for Q, R, inf in outs:
+        assert int(inf.item()) == 0
+        assert torch.equal(Q, Q0) and torch.equal(torch.triu(R), torch.triu(R0))
