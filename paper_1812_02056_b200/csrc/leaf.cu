@@ -224,6 +224,92 @@ __global__ void __launch_bounds__(NT) chol_leaf_warp_kernel(int64_t m, int w, co
     if (k < w) dst[r + (int64_t)k * ldd] = x[k];
 }
 
+// Variant (default for W <= 32): RIGHT-looking, the paper's per-element order.  Warp 0
+// holds the diagonal block in registers (lane i = row i, a[k] = running A_ik); at column c
+// lane c's a[c] is final, L_cc = sqrt(a[c]) is broadcast, every lane scales its a[c] by
+// 1/L_cc, publishes L_ic to a shared vector, and subtracts L_ic L_jc from its a[j], j > c.
+// Each entry thus receives  A_ij - L_i0 L_j0 - L_i1 L_j1 - ...  one term at a time in k
+// order — exactly PAPER.md:59-64 ("L_ic -= L_ik L_ck" for k = z..c-1) — and the
+// critical path of a column is one shuffle, sqrt, reciprocal, a shared store/load and ONE
+// fma (the j = c+1 update): the remaining fmas are independent and overlap the next column.
+// The division by L_cc is a multiplication by the warp-uniform 1/L_cc (<= 1 ulp apart,
+// DESIGN.md reading P11): a per-lane division next to lane c's different branch cost
+// ~500 cycles per column (calib/leaf_probe.cu: Crout 33.5K -> 18.2K cycles, w = 32).
+// Rows below: the same right-looking order in registers (x_c *= 1/L_cc, x_j -= x_c L_jc),
+// L stored transposed (Lt[c][j] = L_jc) so the broadcast operands of a column are
+// contiguous (16-byte shared loads).
+template <typename T, int W, int NT>
+__global__ void __launch_bounds__(NT) chol_leaf_rl_kernel(int64_t m, int w, const T* __restrict__ src,
+                                                              int64_t lds, T* __restrict__ dst, int64_t ldd,
+                                                              int64_t col0, long long* fail) {
+  static_assert(W <= 32, "one row per lane");
+  if (failed(fail)) return;
+  __shared__ __align__(16) T Lt[W][W + 2];   // Lt[c][j] = L_jc (j >= c), 0 above
+  __shared__ T inv[W];
+  __shared__ T lc[2][W];
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r = w + (int64_t)blockIdx.x * NT + tid;
+  if (warp == 0) {
+    T a[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) a[k] = (lane < w && k <= lane && k < w) ? __ldcg(src + lane + (int64_t)k * lds) : T(0);
+    int okc = 1;
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      if (c < w) {
+        const T d = __shfl_sync(kFull, a[c], c);
+        if (!(d > T(0))) {
+          okc = 0;
+          if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
+          break;
+        }
+        const T Lcc = leaf_sqrt(d);
+        const T ri = T(1) / Lcc;                       // warp-uniform
+        const T l = (lane == c) ? Lcc : a[c] * ri;     // lanes < c: unused (upper part)
+        a[c] = l;
+        if (lane < W) { lc[c & 1][lane] = l; Lt[c][lane] = (lane >= c) ? l : T(0); }
+        if (lane == c) inv[c] = ri;
+        __syncwarp();
+#pragma unroll
+        for (int j = c + 1; j < W; ++j) a[j] = fma(-l, lc[c & 1][j], a[j]);   // row lane, col j (used iff j <= lane)
+      } else {
+        if (lane < W) Lt[c][lane] = T(0);
+        if (lane == 0) inv[c] = T(0);
+      }
+    }
+    if (lane == 0) bad = !okc;
+  }
+  T x[W];
+  if (r < m) {
+#pragma unroll
+    for (int k = 0; k < W; ++k) x[k] = (k < w) ? __ldcg(src + r + (int64_t)k * lds) : T(0);
+  }
+  __syncthreads();
+  if (bad) return;
+  if (last_reader(fail + 1)) {
+    for (int idx = tid; idx < w * w; idx += NT) {
+      const int i = idx % w, k = idx / w;
+      if (k <= i) dst[i + (int64_t)k * ldd] = Lt[k][i];
+    }
+  }
+  if (r >= m) return;
+#pragma unroll
+  for (int c = 0; c < W; ++c) {
+    x[c] = x[c] * inv[c];
+#pragma unroll
+    for (int j = c + 1; j < W; ++j) x[j] = fma(-x[c], Lt[c][j], x[j]);
+  }
+#pragma unroll
+  for (int k = 0; k < W; ++k)
+    if (k < w) dst[r + (int64_t)k * ldd] = x[k];
+}
+
+static bool leaf_rl_on() {
+  static int on = [] { const char* e = getenv("SF_LEAF_RL"); return e ? atoi(e) : 1; }();
+  return on != 0;
+}
+
 static bool leaf_warp_on() {
   static int on = [] { const char* e = getenv("SF_LEAF_WARP"); return e ? atoi(e) : 1; }();
   return on != 0;
@@ -235,6 +321,12 @@ cudaError_t chol_leaf(int64_t m, int w, const T* src, int64_t lds, T* dst, int64
   if (w <= 0 || m <= 0) return cudaSuccess;
   const int64_t below = m - w;
   const int grid = below > 0 ? (int)((below + kLeafT - 1) / kLeafT) : 1;
+  if (leaf_rl_on() && w <= 32) {
+    if (w <= 16) chol_leaf_rl_kernel<T, 16, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+    else chol_leaf_rl_kernel<T, 32, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+    count_launch();
+    return cudaGetLastError();
+  }
   if (leaf_warp_on()) {
     // SF_LEAF_NT=64: 64-thread CTAs (~6.4K registers) fit on an SM next to two flush CTAs, so
     // the lookahead panel's leaves need not wait for flush CTAs to retire — measured no
