@@ -478,8 +478,8 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t
                                                               int64_t col0, const T* tolp, long long* fail,
                                                               int nrow_blocks) {
   if (failed(fail)) return;
-  __shared__ T Ls[W][W + 1];     // L11 (Ls[i][k] = L_ik)
-  __shared__ T Us[W][W + 1];     // U11 (Us[k][j] = U_kj)
+  __shared__ __align__(16) T Lt[W][W + 2];   // L11 transposed (Lt[k][i] = L_ik): column k contiguous
+  __shared__ __align__(16) T Us[W][W + 2];   // U11 (Us[k][j] = U_kj): row k contiguous
   __shared__ T inv[W];
   __shared__ T S[kUCols][W + 1]; // staging for the U columns
   __shared__ int bad;
@@ -489,36 +489,49 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t
   const int64_t j0 = w + (int64_t)(blockIdx.x - nrow_blocks) * kUCols;
   const int ncols = rowblock ? 0 : (int)((w + ncr - j0) < kUCols ? (w + ncr - j0) : kUCols);
   if (warp == 0) {
+    // Right-looking in registers, the paper's per-element order (every
+    // entry receives its -L_ik U_k* terms one at a time in k order): lane i holds row i of
+    // the block; at column c lane c's a[c] is L_cc, lane c scales its row right of c by the
+    // warp-uniform 1/L_cc (U_c*, reading P11) and publishes it, every lane below subtracts
+    // L_ic U_cj.  Critical path per column: shuffle, reciprocal, one multiply, a shared
+    // store/load and one fma (was: a c-term dot product and a per-lane division).
+    __shared__ T uc[2][W];
     const T tol = __ldcg(tolp);
-    if (lane < W)
-      for (int k = 0; k < W; ++k) {
-        const bool in = lane < w && k < w;
-        Ls[lane][k] = (in && k <= lane) ? __ldcg(src + lane + (int64_t)k * lds) : T(0);
-        Us[k][lane] = (in && k < lane) ? __ldcg(src + k + (int64_t)lane * lds) : T(0);
-      }
-    __syncwarp();
+    T a[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) a[k] = (lane < w && k < w) ? __ldcg(src + lane + (int64_t)k * lds) : T(0);
     int okc = 1;
-    for (int c = 0; c < w; ++c) {
-      const int i = lane;
-      T a0 = T(0), a1 = T(0), b0 = T(0), b1 = T(0);
-      if (i >= c && i < w) {
-        for (int k = 0; k < c; ++k) {
-          if (k & 1) { a1 = fma(-Ls[i][k], Us[k][c], a1); b1 = fma(-Ls[c][k], Us[k][i], b1); }
-          else { a0 = fma(-Ls[i][k], Us[k][c], a0); b0 = fma(-Ls[c][k], Us[k][i], b0); }
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      if (c < w) {
+        const T Lcc = __shfl_sync(kFull, a[c], c);
+        if (!(fabs(Lcc) >= tol)) {
+          okc = 0;
+          if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
+          break;
         }
+        const T ri = T(1) / Lcc;
+        if (lane == c) {
+          inv[c] = ri;
+#pragma unroll
+          for (int j = c + 1; j < W; ++j) { a[j] = a[j] * ri; uc[c & 1][j] = a[j]; }
+        }
+        __syncwarp();
+        if (lane > c) {
+          const T l = a[c];
+#pragma unroll
+          for (int j = c + 1; j < W; ++j) a[j] = fma(-l, uc[c & 1][j], a[j]);
+        }
+      } else if (lane == 0) {
+        inv[c] = T(0);
       }
-      const T tL = (i < w) ? Ls[i][c] + (a0 + a1) : T(0);
-      const T tU = (i < w) ? Us[c][i] + (b0 + b1) : T(0);
-      const T Lcc = __shfl_sync(kFull, tL, c);
-      if (!(fabs(Lcc) >= tol)) {
-        okc = 0;
-        if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
-        break;
+    }
+    if (okc && lane < W) {
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        Lt[k][lane] = (k <= lane) ? a[k] : T(0);
+        Us[lane][k] = (k > lane) ? a[k] : T(0);
       }
-      if (i >= c && i < w) Ls[i][c] = tL;
-      if (i > c && i < w) Us[c][i] = tU / Lcc;
-      if (i == c) inv[c] = T(1) / Lcc;
-      __syncwarp();
     }
     if (lane == 0) bad = !okc;
   } else if (!rowblock) {
@@ -536,23 +549,17 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t
   if (last_reader(fail + 1)) {   // see chol_leaf_kernel
     for (int idx = tid; idx < w * w; idx += kLeafT) {
       const int i = idx % w, k = idx / w;
-      dst[i + (int64_t)k * ldd] = (k <= i) ? Ls[i][k] : Us[i][k];   // L incl. diagonal / U strict upper
+      dst[i + (int64_t)k * ldd] = (k <= i) ? Lt[k][i] : Us[i][k];   // L incl. diagonal / U strict upper
     }
   }
   if (rowblock) {
-    // L rows below: L_rc = A_rc - sum_{k<c} L_rk U_kc
+    // L rows below: L_rc = A_rc - sum_{k<c} L_rk U_kc, right-looking (terms in k order)
     if (r >= m) return;
 #pragma unroll
     for (int c = 0; c < W; ++c) {
-      T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
+      const T xc = x[c];
 #pragma unroll
-      for (int k = 0; k < c; ++k) {
-        if ((k & 3) == 0) a0 = fma(-x[k], Us[k][c], a0);
-        else if ((k & 3) == 1) a1 = fma(-x[k], Us[k][c], a1);
-        else if ((k & 3) == 2) a2 = fma(-x[k], Us[k][c], a2);
-        else a3 = fma(-x[k], Us[k][c], a3);
-      }
-      x[c] = (a0 + a1) + (a2 + a3);
+      for (int j = c + 1; j < W; ++j) x[j] = fma(-xc, Us[c][j], x[j]);
     }
 #pragma unroll
     for (int k = 0; k < W; ++k)
@@ -565,16 +572,10 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t
 #pragma unroll
     for (int k = 0; k < W; ++k) y[k] = (k < w) ? S[tid][k] : T(0);
 #pragma unroll
-    for (int c = 0; c < W; ++c) {
-      T a0 = y[c], a1 = T(0), a2 = T(0), a3 = T(0);
+    for (int c = 0; c < W; ++c) {   // right-looking: y_c *= 1/L_cc, then y_j -= L_jc y_c
+      y[c] = y[c] * inv[c];
 #pragma unroll
-      for (int k = 0; k < c; ++k) {
-        if ((k & 3) == 0) a0 = fma(-Ls[c][k], y[k], a0);
-        else if ((k & 3) == 1) a1 = fma(-Ls[c][k], y[k], a1);
-        else if ((k & 3) == 2) a2 = fma(-Ls[c][k], y[k], a2);
-        else a3 = fma(-Ls[c][k], y[k], a3);
-      }
-      y[c] = ((a0 + a1) + (a2 + a3)) * inv[c];
+      for (int j = c + 1; j < W; ++j) y[j] = fma(-Lt[c][j], y[c], y[j]);
     }
 #pragma unroll
     for (int k = 0; k < W; ++k) S[tid][k] = y[k];
