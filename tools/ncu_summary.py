@@ -61,10 +61,16 @@ def launches(path):
         except ValueError:
             pass
     tot = sum(sum(v) for v in agg.values())
-    print(f"{'kernel':72s} {'launches':>8s} {'total us':>10s} {'avg us':>8s} {'share':>6s}")
+    # the library's own kernels (namespace sf::) vs everything else in the process (torch's input
+    # generation, e.g. the G G^T product, runs once outside the timed region)
+    lib = sum(sum(v) for k, v in agg.items() if "sf::" in k)
+    print("serialised, cold-cache durations (ncu); 'lib share' = share among the library's kernels")
+    print(f"{'kernel':72s} {'launches':>8s} {'total us':>10s} {'avg us':>8s} {'share':>6s} {'lib share':>9s}")
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-        print(f"{k:72s} {len(v):8d} {sum(v) / 1e3:10.1f} {sum(v) / len(v) / 1e3:8.2f} {sum(v) / tot:6.3f}")
+        ls = f"{sum(v) / lib:9.3f}" if ("sf::" in k and lib) else f"{'-':>9s}"
+        print(f"{k:72s} {len(v):8d} {sum(v) / 1e3:10.1f} {sum(v) / len(v) / 1e3:8.2f} {sum(v) / tot:6.3f} {ls}")
     print(f"{'TOTAL':72s} {sum(len(v) for v in agg.values()):8d} {tot / 1e3:10.1f}")
+    print(f"{'TOTAL sf:: kernels':72s} {sum(len(v) for k, v in agg.items() if 'sf::' in k):8d} {lib / 1e3:10.1f}")
 
 
 if __name__ == "__main__":
