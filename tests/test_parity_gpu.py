@@ -498,3 +498,21 @@ def test_qr_concurrent_streams():
     for Q, R, inf in outs:
         assert int(inf.item()) == 0
         assert torch.equal(Q, Q0) and torch.equal(torch.triu(R), torch.triu(R0))
+
+
+@pytest.mark.parametrize("n,s", [(1500, 96), (16384, 128)])
+def test_qr_mgs_cluster_geometries(n, s):
+    """The MGS panel's grid changes with n (DESIGN.md §5 K7): one cluster of <= 8 CTAs
+    (n <= 1024), 8-CTA clusters, 4-CTA clusters when 8-CTA ones do not all fit (n = 16384),
+    with ragged last CTAs (n = 1500).  First K columns / rows against the restricted oracle,
+    orthogonality and residual in full."""
+    K = 2 * s
+    A = synth.gen_numpy("gaussian", n, seed=7)
+    Qg, Rg, ig = run_qr(A, s)
+    Qo, Ro, io, _ = oracle.qr(A, s, kcols=K)
+    assert io == ig == 0
+    assert synth.r2_error(Qg[:, :K], Qo[:, :K]) <= TOL64
+    assert synth.r2_error(Rg[:K, :], Ro[:K, :]) <= TOL64
+    Qt = torch.from_numpy(Qg).cuda(); At = torch.from_numpy(A).cuda(); Rt = torch.from_numpy(Rg).cuda()
+    assert float((Qt.mT @ Qt - torch.eye(n, device="cuda", dtype=torch.float64)).norm()) <= 1e-12 * n
+    assert float((At - Qt @ Rt).norm() / At.norm()) <= 1e-13 * n
