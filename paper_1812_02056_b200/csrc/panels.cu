@@ -494,6 +494,121 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
   }
 }
 
+// Shared-memory-resident variant of the cluster + LL exchange for panels wider than 128
+// columns (or more rows per CTA than the register variant holds): the panel rows live in
+// shared memory as in qr_mgs_kernel (a warp per column, lanes over rows), the Gram-row
+// exchange is the two-level one of qr_mgs_ll_kernel.
+template <typename T>
+__global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_smem_kernel(int64_t n, int w, int RB, const T* __restrict__ src,
+                                                                     int64_t lds, T* __restrict__ dst, int64_t ldd,
+                                                                     int64_t col0, const T* tolp,
+                                                                     unsigned long long* ll, long long* fail) {
+  if (failed(fail)) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* V = reinterpret_cast<T*>(smraw);          // V[c * RB + r]: this CTA's rows of the panel
+  T* gsum = V + (size_t)RB * w;                // reduced Gram row of the current column
+  T* mypart = gsum + w;                        // [2][w] this CTA's partial Gram rows
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CL = (int)cluster.num_blocks(), k = (int)cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kMgsThreads / 32;
+  const int G = gridDim.x, g = blockIdx.x, Q = G / CL, q = g / CL;
+  T* cval = mypart + 2 * w;                    // [Q][w] cluster sums
+  T* qs = cval + (size_t)Q * w;                // [RB] q_c of this CTA's rows
+  T* vs = qs + RB;                             // [RB] updated v_{c+1}
+  const int64_t r0 = (int64_t)g * RB;
+  const int rows = (int)((r0 + RB <= n) ? RB : (n > r0 ? n - r0 : 0));
+  const T tol = __ldcg(tolp);
+  const int RJ = (RB + 31) / 32;
+
+  for (int idx = tid; idx < RB * w; idx += kMgsThreads) {
+    const int r = idx % RB, c = idx / RB;
+    V[idx] = (r < rows) ? __ldcg(src + r0 + r + (int64_t)c * lds) : T(0);
+  }
+  __syncthreads();
+  {
+    T v0[kMgsRJ];
+#pragma unroll
+    for (int j = 0; j < kMgsRJ; ++j) v0[j] = (j < RJ && lane + 32 * j < RB) ? V[lane + 32 * j] : T(0);
+    for (int cp = warp; cp < w; cp += nwarps) {
+      T acc = T(0);
+#pragma unroll
+      for (int j = 0; j < kMgsRJ; ++j)
+        if (j < RJ && lane + 32 * j < RB) acc = fma(v0[j], V[(size_t)cp * RB + lane + 32 * j], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) mypart[cp] = acc;
+    }
+  }
+
+  bool ok = true;
+  for (int c = 0; c < w; ++c) {
+    const int buf = c & 1;
+    const unsigned ep = (unsigned)(col0 + c + 1);
+    cluster.sync();
+    for (int j = c + k + CL * tid; j < w; j += CL * kMgsThreads) {
+      T a = T(0);
+      for (int rr = 0; rr < CL; ++rr) a += cluster.map_shared_rank(mypart + buf * w, rr)[j];
+      LL<T>::put(ll + LL<T>::kWords * ((size_t)(buf * Q + q) * w + j), a, ep);
+    }
+    const int wc = w - c, cnt = Q * wc;
+    for (int idx = tid; idx < cnt; idx += kMgsThreads) {
+      const int qq = idx / wc, j = c + idx % wc;
+      const unsigned long long* p = ll + LL<T>::kWords * ((size_t)(buf * Q + qq) * w + j);
+      T v;
+      while (!LL<T>::get(p, ep, v)) {}
+      cval[qq * w + j] = v;
+    }
+    __syncthreads();
+    for (int j = c + tid; j < w; j += kMgsThreads) {
+      T a = T(0);
+      for (int qq = 0; qq < Q; ++qq) a += cval[qq * w + j];
+      gsum[j] = a;
+    }
+    __syncthreads();
+    const T nv = dsqrt(gsum[c]);
+    if (!(nv >= tol)) {
+      if (g == 0 && tid == 0) record_fail(fail, col0 + c + 1);
+      ok = false;
+      break;
+    }
+    // q_c = v_c / ||v_c|| and the updated v_{c+1} as shared vectors, then a THREAD per later
+    // column (no per-column warp reduction): v_cp -= q_c (q_c^T v_cp) row by row, with its
+    // dot against the updated v_{c+1} formed in the same pass (the next partial Gram row)
+    const T rnv = T(1) / nv;
+    const T cn = (c + 1 < w) ? gsum[c + 1] * rnv : T(0);
+    for (int r = tid; r < RB; r += kMgsThreads) {
+      const T qr = V[(size_t)c * RB + r] * rnv;
+      qs[r] = qr;
+      V[(size_t)c * RB + r] = qr;
+      vs[r] = (c + 1 < w) ? fma(-qr, cn, V[(size_t)(c + 1) * RB + r]) : T(0);
+    }
+    __syncthreads();
+    for (int cp = c + 1 + tid; cp < w; cp += kMgsThreads) {
+      const T coef = gsum[cp] * rnv;
+      T* col = V + (size_t)cp * RB;
+      T acc = T(0);
+      if (cp == c + 1) {
+        for (int r = 0; r < RB; ++r) { const T v = vs[r]; col[r] = v; acc = fma(v, v, acc); }
+      } else {
+#pragma unroll 4
+        for (int r = 0; r < RB; ++r) {
+          const T v = fma(-qs[r], coef, col[r]);
+          col[r] = v;
+          acc = fma(vs[r], v, acc);
+        }
+      }
+      mypart[(buf ^ 1) * w + cp] = acc;
+    }
+    __syncthreads();
+  }
+  cluster.sync();
+  if (!ok) return;
+  __syncthreads();
+  for (int idx = tid; idx < RB * w; idx += kMgsThreads) {
+    const int r = idx % RB, c = idx / RB;
+    if (r < rows) dst[r0 + r + (int64_t)c * ldd] = V[idx];
+  }
+}
+
 struct LLGeom { int G = 0, CL = 0, RB = 0; size_t dyn = 0; };
 
 // The MGS grids are persistent: their CTAs wait on each other, so two of them running at
@@ -524,43 +639,58 @@ struct MgsOrder {
 cudaEvent_t MgsOrder::ev[MgsOrder::kMaxDev] = {};
 cudaStream_t MgsOrder::last[MgsOrder::kMaxDev] = {};
 
-// Grid for the LL kernel, or G = 0 when it does not apply (then the flag-exchange kernels).
+// Grid for the LL kernels, or G = 0 when they do not apply (then the flag-exchange kernels).
+// reg: the register-resident variant (w <= 128, <= 128 rows per CTA); otherwise the
+// shared-memory one (the panel rows + exchange buffers within 220 KB per CTA).
 template <typename T>
-static LLGeom ll_geom(int64_t n, int w) {
+static LLGeom ll_geom(int64_t n, int w, bool reg) {
   LLGeom r;
-  if (w > 128 || getenv("SF_MGS_NOLL") != nullptr) return r;
+  if (getenv("SF_MGS_NOLL") != nullptr) return r;
+  if (reg && w > 128) return r;
   const int64_t G0 = (n + 2 * kMgsRPT - 1) / (2 * kMgsRPT);
-  static int maxcl[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};   // co-resident clusters per size
+  static int maxcl[2][9] = {{-1, -1, -1, -1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1, -1, -1, -1}};
+  auto dyn_for = [&](int G, int CL) -> size_t {
+    if (reg) return sizeof(T) * (size_t)(G / CL) * (size_t)w;
+    const int RB = (int)((n + G - 1) / G);
+    return sizeof(T) * ((size_t)RB * w + 3 * (size_t)w + (size_t)(G / CL) * w + 2 * (size_t)RB);
+  };
   auto fits = [&](int CL, int G) -> bool {
-    if (maxcl[CL] < 0) {
+    const size_t dyn = dyn_for(G, CL);
+    if (dyn > 220 * 1024) return false;
+    int& mc = maxcl[reg ? 0 : 1][CL];
+    if (mc < 0 || !reg) {   // the shared-memory variant's occupancy depends on its size
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(G);
       cfg.blockDim = dim3(kMgsThreads);
-      cfg.dynamicSmemBytes = 0;
+      cfg.dynamicSmemBytes = dyn;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
       at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
+      const void* kf = reg ? (const void*)qr_mgs_ll_kernel<T> : (const void*)qr_mgs_ll_smem_kernel<T>;
+      if (!reg) cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
       int m = 0;
-      if (cudaOccupancyMaxActiveClusters(&m, (void*)qr_mgs_ll_kernel<T>, &cfg) != cudaSuccess) { cudaGetLastError(); m = 0; }
-      maxcl[CL] = m;
+      if (cudaOccupancyMaxActiveClusters(&m, kf, &cfg) != cudaSuccess) { cudaGetLastError(); m = 0; }
+      if (reg) mc = m;
+      else return G / CL <= m;
     }
-    return G / CL <= maxcl[CL];
+    return G / CL <= mc;
   };
   int G = 0, CL = 0;
-  if (G0 <= 8) { G = (int)G0; CL = (int)G0; }
-  else {
+  if (G0 <= 8) {
+    if (fits((int)G0, (int)G0)) { G = (int)G0; CL = (int)G0; }
+  } else {
     for (int cl : {8, 4}) {
       const int g = (int)((G0 + cl - 1) / cl * cl);
       if (fits(cl, g)) { G = g; CL = cl; break; }
     }
   }
-  if (G == 0 || (G <= 8 && !fits(CL, G))) return r;
+  if (G == 0) return r;
   r.G = G; r.CL = CL;
   r.RB = (int)((n + G - 1) / G);
-  if (r.RB > 2 * kMgsRPT) return LLGeom{};
-  r.dyn = sizeof(T) * (size_t)(G / CL) * (size_t)w;
+  if (r.RB > (reg ? 2 * kMgsRPT : 32 * kMgsRJ)) return LLGeom{};
+  r.dyn = dyn_for(G, CL);
   return r;
 }
 
@@ -569,7 +699,9 @@ cudaError_t qr_mgs_panel(int64_t n, int w, const T* src, int64_t lds, T* dst, in
                          const T* tol, T* work, long long* fail, cudaStream_t st) {
   if (w <= 0) return cudaSuccess;
   MgsOrder order(st);
-  const LLGeom lg = ll_geom<T>(n, w);
+  LLGeom lg = ll_geom<T>(n, w, true);
+  const bool lreg = lg.G > 0;
+  if (!lreg) lg = ll_geom<T>(n, w, false);
   if (lg.G > 0) {
     unsigned long long* ll = reinterpret_cast<unsigned long long*>(((uintptr_t)work + 255) & ~(uintptr_t)255);
     cudaLaunchConfig_t cfg = {};
@@ -586,7 +718,8 @@ cudaError_t qr_mgs_panel(int64_t n, int w, const T* src, int64_t lds, T* dst, in
     cfg.numAttrs = 2;
     int RB = lg.RB;
     count_launch();
-    return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
+    if (lreg) return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
+    return cudaLaunchKernelEx(&cfg, qr_mgs_ll_smem_kernel<T>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
   }
   MgsGeom g = mgs_geom(n, w, (int)sizeof(T));
   if (g.smem > 220 * 1024) return cudaErrorInvalidValue;   // caller splits wider panels
