@@ -709,13 +709,16 @@ cudaError_t qr_mgs_panel(int64_t n, int w, const T* src, int64_t lds, T* dst, in
     cfg.blockDim = dim3(kMgsThreads);
     cfg.dynamicSmemBytes = lg.dyn;
     cfg.stream = st;
+    // Every cluster waits on every other, so all must be co-resident: ll_geom admits the grid
+    // only if cudaOccupancyMaxActiveClusters says they all fit, and eager launches are chained
+    // (MgsOrder).  Not launched cooperative: Nsight Compute rejects cooperative cluster launches.
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = lg.CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeCooperative;   // all clusters co-resident (they wait on each other)
+    at[1].id = cudaLaunchAttributeCooperative;
     at[1].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = getenv("SF_MGS_COOP") ? 2 : 1;
     int RB = lg.RB;
     count_launch();
     if (lreg) return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
