@@ -305,6 +305,84 @@ __global__ void __launch_bounds__(NT) chol_leaf_rl_kernel(int64_t m, int w, cons
     if (k < w) dst[r + (int64_t)k * ldd] = x[k];
 }
 
+// Same arithmetic as chol_leaf_rl_kernel with ROLLED column loops: the registers rotate
+// (a[0] is always the current column), so a column step is one small loop body (~100
+// instructions instead of ~2.7K unrolled) — the leaf's code is fetched cold at every
+// launch between GEMMs, and ncu attributes ~30% of its stalls to instruction fetch.
+// Lr[c][j] = L_{c+1+j, c} (0 past the block): the operands of column c, 16-byte aligned.
+template <typename T, int W, int NT>
+__global__ void __launch_bounds__(NT) chol_leaf_rot_kernel(int64_t m, int w, const T* __restrict__ src,
+                                                               int64_t lds, T* __restrict__ dst, int64_t ldd,
+                                                               int64_t col0, long long* fail) {
+  static_assert(W <= 32, "one row per lane");
+  if (failed(fail)) return;
+  __shared__ __align__(16) T Lr[W][W];
+  __shared__ T inv[W];
+  __shared__ T Ld[W][W + 1];
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r = w + (int64_t)blockIdx.x * NT + tid;
+  if (warp == 0) {
+    T a[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) a[k] = (lane < w && k <= lane && k < w) ? __ldcg(src + lane + (int64_t)k * lds) : T(0);
+    int okc = 1;
+#pragma unroll 1
+    for (int c = 0; c < w; ++c) {
+      const T d = __shfl_sync(kFull, a[0], c);     // a[0] = column c of my row
+      if (!(d > T(0))) {
+        okc = 0;
+        if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
+        break;
+      }
+      const T Lcc = leaf_sqrt(d);
+      const T ri = T(1) / Lcc;
+      const T l = (lane == c) ? Lcc : a[0] * ri;
+      if (lane < W) {
+        Ld[lane][c] = (lane >= c) ? l : T(0);
+        Lr[c][lane] = T(0);
+      }
+      __syncwarp();
+      if (lane > c && lane < W) Lr[c][lane - c - 1] = l;
+      if (lane == c) inv[c] = ri;
+      __syncwarp();
+      const T* v = &Lr[c][0];
+#pragma unroll
+      for (int j = 1; j < W; ++j) a[j - 1] = fma(-l, v[j - 1], a[j]);
+      a[W - 1] = T(0);
+    }
+    if (lane == 0) bad = !okc;
+  }
+  T x[W];
+  if (r < m) {
+#pragma unroll
+    for (int k = 0; k < W; ++k) x[k] = (k < w) ? __ldcg(src + r + (int64_t)k * lds) : T(0);
+  }
+  __syncthreads();
+  if (bad) return;
+  if (last_reader(fail + 1)) {
+    for (int idx = tid; idx < w * w; idx += NT) {
+      const int i = idx % w, k = idx / w;
+      if (k <= i) dst[i + (int64_t)k * ldd] = Ld[i][k];
+    }
+  }
+  if (r >= m) return;
+#pragma unroll 1
+  for (int c = 0; c < w; ++c) {
+    const T xc = x[0] * inv[c];
+    dst[r + (int64_t)c * ldd] = xc;
+    const T* v = &Lr[c][0];
+#pragma unroll
+    for (int j = 1; j < W; ++j) x[j - 1] = fma(-xc, v[j - 1], x[j]);
+    x[W - 1] = T(0);
+  }
+}
+
+static bool leaf_rot_on() {
+  static int on = [] { const char* e = getenv("SF_LEAF_ROT"); return e ? atoi(e) : 0; }();
+  return on != 0;
+}
+
 static bool leaf_rl_on() {
   static int on = [] { const char* e = getenv("SF_LEAF_RL"); return e ? atoi(e) : 1; }();
   return on != 0;
@@ -321,6 +399,12 @@ cudaError_t chol_leaf(int64_t m, int w, const T* src, int64_t lds, T* dst, int64
   if (w <= 0 || m <= 0) return cudaSuccess;
   const int64_t below = m - w;
   const int grid = below > 0 ? (int)((below + kLeafT - 1) / kLeafT) : 1;
+  if (leaf_rot_on() && w <= 32) {
+    if (w <= 16) chol_leaf_rot_kernel<T, 16, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+    else chol_leaf_rot_kernel<T, 32, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+    count_launch();
+    return cudaGetLastError();
+  }
   if (leaf_rl_on() && w <= 32) {
     if (w <= 16) chol_leaf_rl_kernel<T, 16, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
     else chol_leaf_rl_kernel<T, 32, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
