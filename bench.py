@@ -184,6 +184,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--loopback", type=int, default=0,
                     help="test mode: run the distributed driver with G ranks emulated on this one GPU")
+    ap.add_argument("--strassen", type=int, default=0, metavar="MIN_DIM",
+                    help="f1: one Strassen-Winograd level in fp64 flushes with sides >= MIN_DIM (0 = off)")
     return ap.parse_args()
 
 
@@ -328,6 +330,8 @@ def main():
         else:
             sf.qr_colmajor(n, s, A, n, out1, n, out2, n, info, stream=stream)
 
+    if args.strassen:
+        sf.set_strassen(1, args.strassen)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -486,6 +490,9 @@ def main():
                 "vs_baseline": None, "dtype": dtype, "data": "synthetic",
                 "config": {"workload": args.workload, "kind": kind, "n": n, "s": s, "baseline_config": cfgname,
                            "generator": gen, "seed": args.seed, "parallelism": par,
+                           **({"strassen": {"levels": 1, "min_dim": args.strassen,
+                                            "note": "roofline.achieved counts classical-equivalent flops"}}
+                              if args.strassen else {}),
                            "l2": f"inputs larger than L2 ({A.numel() * A.element_size() / 1e9:.2f} GB per rank "
                                  "> 126 MB); out-of-place factorization, A re-read from HBM every step"},
                 "pct_tensor_peak": (value / ws / 1e3 / peak) if peak else None,

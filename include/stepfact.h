@@ -190,6 +190,17 @@ int lu_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* const*
 int qr_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* const* dA_local, void* const* dQ_local,
                    void* const* dR_local, int64_t ld_local, int64_t* const* d_info, void* stream);
 
+/* Fast multiplication in the flush ("using a fast
+ * rectangular matrix multiplication algorithm", 186-188).  levels = 1: fp64 flushes whose
+ * two output sides are >= min_dim use ONE Strassen-Winograd level (7 half-size DMMA
+ * products, operand/output block sums elementwise; uneven halves zero-padded) — LU's
+ * A -= R_L R_U, QR's M -= B_Q C, and the off-diagonal half of Cholesky's A -= R R^T.
+ * levels = 0 (default): classical products only.  Process-wide, single-GPU drivers, fp64;
+ * clears the library's captured CUDA graphs.  Rounding differs from the classical product
+ * (normwise error bound, not componentwise).  Errors: SF_EINVAL if levels not in {0, 1} or
+ * min_dim < 64. */
+int sf_set_strassen(int levels, int64_t min_dim);
+
 /* Number of flushes the c = z+s schedule performs: floor((n-1)/s). */
 int64_t sf_flush_count(int64_t n, int64_t s);
 /* Cumulative number of kernel launches this library has enqueued in this process

@@ -93,6 +93,8 @@ def lib():
     L.sf_flush_count.restype = i64
     L.sf_launch_counter.argtypes = []
     L.sf_launch_counter.restype = i64
+    L.sf_set_strassen.argtypes = [i32, i64]
+    L.sf_set_strassen.restype = i32
     L.sf_strerror.argtypes = [i32]
     L.sf_strerror.restype = ctypes.c_char_p
     L.sf_last_error.argtypes = []
@@ -112,7 +114,7 @@ EXPORTS = ("chol_factor", "lu_factor", "qr_factor", "chol_factor_host", "lu_fact
            "sf_profile_collect", "sf_get_unique_id", "sf_comm_init", "sf_comm_init_loopback", "sf_comm_destroy",
            "sf_comm_size", "sf_comm_local_ranks", "sf_local_cols", "chol_factor_dist", "lu_factor_dist",
            "qr_factor_dist", "chol_factor_steps", "lu_factor_steps", "qr_factor_steps", "chol_solve", "lu_solve",
-           "qr_solve")
+           "qr_solve", "sf_set_strassen")
 
 
 def _check(rc):
@@ -147,6 +149,11 @@ def flush_count(n, s):
 
 def launch_counter():
     return int(lib().sf_launch_counter())
+
+
+def set_strassen(levels, min_dim=4096):
+    """sf_set_strassen: one Strassen-Winograd level in fp64 flushes with sides >= min_dim (f1)."""
+    _check(lib().sf_set_strassen(int(levels), int(min_dim)))
 
 
 def profile_enable(on=True):

@@ -95,15 +95,14 @@ static int chol_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* L, in
         const int64_t c2 = c + w2;
         const double fl = (double)w * (double)(m - w2) * (double)(m - w2 + 1);
         ProfScope ps(0, fl, st);
-        SF_CUDA(gemm_sub<T>(m - w2, m - w2, w, R + w2, ldl, 0, R + w2, ldl, 0, src + c2 + c2 * lds, lds,
-                            L + c2 + c2 * ldl, ldl, kMaskLower, fail, st, flush_ctas_for_panel(fl)));
+        SF_CUDA(flush_lower<T>(m - w2, w, R + w2, ldl, src + c2 + c2 * lds, lds, L + c2 + c2 * ldl, ldl, fail, st,
+                               flush_ctas_for_panel(fl)));
       }
       SF_CUDA(fork_join(*sd, sd->st, st));
     } else {
       {  // flush: A[c:n,c:n] -= R R^T
         ProfScope ps(0, (double)w * (double)m * (double)(m + 1), st);
-        SF_CUDA(gemm_sub<T>(m, m, w, R, ldl, 0, R, ldl, 0, src + c + c * lds, lds, L + c + c * ldl, ldl, kMaskLower,
-                            fail, st));
+        SF_CUDA(flush_lower<T>(m, w, R, ldl, src + c + c * lds, lds, L + c + c * ldl, ldl, fail, st));
       }
       ProfScope ps(1, 0.0, st);
       SF_CUDA(chol_panel_rec<T>(m, w2, L + c + c * ldl, ldl, L + c + c * ldl, ldl, c, fail, st));
@@ -216,8 +215,8 @@ static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int
       SF_CUDA(fork_join(*sd, st, pst));
     } else {
       ProfScope ps(0, 2.0 * w * (double)m * (double)m, st);
-      SF_CUDA(gemm_sub<T>(m, m, w, RL, ldd, 0, RU, ldd, 1, src + c + c * lds, lds, LU + c + c * ldd, ldd, kMaskNone,
-                          fail, st));
+      SF_CUDA(flush_general<T>(m, m, w, RL, ldd, 0, RU, ldd, 1, src + c + c * lds, lds, LU + c + c * ldd, ldd, fail,
+                               st));
     }
     {
       ProfScope ps(1, 0.0, pst);
@@ -228,8 +227,8 @@ static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int
         const int64_t c2 = c + w2;
         const double fl = 2.0 * w * (double)(m - w2) * (double)(m - w2);
         ProfScope ps(0, fl, st);
-        SF_CUDA(gemm_sub<T>(m - w2, m - w2, w, RL + w2, ldd, 0, RU + w2 * ldd, ldd, 1, src + c2 + c2 * lds, lds,
-                            LU + c2 + c2 * ldd, ldd, kMaskNone, fail, st, flush_ctas_for_panel(fl)));
+        SF_CUDA(flush_general<T>(m - w2, m - w2, w, RL + w2, ldd, 0, RU + w2 * ldd, ldd, 1, src + c2 + c2 * lds, lds,
+                                 LU + c2 + c2 * ldd, ldd, fail, st, flush_ctas_for_panel(fl)));
       }
       SF_CUDA(fork_join(*sd, pst, st));
     }
@@ -797,6 +796,17 @@ int64_t sf_flush_count(int64_t n, int64_t s) {
 }
 
 int64_t sf_launch_counter(void) { return g_launches.load(); }
+
+int sf_set_strassen(int levels, int64_t min_dim) {
+  SF_API_LOCK;
+  if (levels < 0 || levels > 1 || min_dim < 64) return fail_with(SF_EINVAL, "strassen: levels must be 0 or 1, min_dim >= 64");
+  strassen_cfg().levels = levels;
+  strassen_cfg().min_dim = min_dim;
+  for (auto& g : g_graphs)   // captured factorizations embed the old choice
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  g_graphs.clear();
+  return SF_OK;
+}
 
 void sf_profile_enable(int on) {
   SF_API_LOCK;

@@ -260,6 +260,110 @@ inline cudaError_t gemm_sub(int64_t M, int64_t N, int64_t K, const T* A, int64_t
   return run_gemm(g, st);
 }
 
+// ------------------------------------------------------------------ f1: Strassen-Winograd flush
+// the step-s method is "fast" because the rectangular product of
+// each flush can use a fast matrix multiplication.  Optional (sf_set_strassen; off by
+// default): ONE Strassen-Winograd level for fp64 flushes whose sides are >= min_dim —
+// 7 half-size DMMA products instead of 8 plus 8 operand block sums and 4 output block
+// sums (elementwise, HBM-bound).  Uneven halves are zero-padded (ceil/floor split).  On
+// B200 the flush is tensor-bound with a ridge near 6 flop/B, so the saved 1/8 of the flops
+// costs ~12 extra passes over half-size blocks (DESIGN.md §9 f1 has the measurement).
+struct StrassenCfg { int levels = 0; int64_t min_dim = 4096; };
+inline StrassenCfg& strassen_cfg() { static StrassenCfg c; return c; }
+
+// op(X) sub-block at (r0, c0): element (i, k) of op(X) is X[kc ? k + i*ld : i + k*ld]
+template <typename T>
+inline const T* opblk(const T* X, int64_t ld, int kc, int64_t r0, int64_t c0) {
+  return X + (kc ? c0 + r0 * ld : r0 + c0 * ld);
+}
+
+// C = Cin - op(A) op(B), one Strassen-Winograd level (fp64).  C may equal Cin (in place).
+template <typename T>
+inline cudaError_t strassen_sub(int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, int ak, const T* B,
+                                int64_t ldb, int bk, const T* Cin, int64_t ldcin, T* C, int64_t ldc,
+                                const long long* fail, cudaStream_t st) {
+  const int64_t m1 = (M + 1) / 2, m2 = M - m1, k1 = (K + 1) / 2, k2 = K - k1, n1 = (N + 1) / 2, n2 = N - n1;
+  // op(B)(k, j): bk ? B[k + j*ldb] : B[j + k*ldb]  ->  as an "op(X)(row k, col j)" with kc = !bk
+  const int bkc = bk ? 0 : 1;
+  const T *A11 = opblk(A, lda, ak, 0, 0), *A12 = opblk(A, lda, ak, 0, k1), *A21 = opblk(A, lda, ak, m1, 0),
+          *A22 = opblk(A, lda, ak, m1, k1);
+  const T *B11 = opblk(B, ldb, bkc, 0, 0), *B12 = opblk(B, ldb, bkc, 0, n1), *B21 = opblk(B, ldb, bkc, k1, 0),
+          *B22 = opblk(B, ldb, bkc, k1, n1);
+  Workspace ws;
+  cudaError_t e = ws.init(sizeof(T) * (size_t)(4 * m1 * k1 + 4 * k1 * n1 + 3 * m1 * n1) + 16 * 256, st);
+  if (e != cudaSuccess) return e;
+  T *S1 = ws.take<T>(m1 * k1), *S2 = ws.take<T>(m1 * k1), *S3 = ws.take<T>(m1 * k1), *S4 = ws.take<T>(m1 * k1);
+  T *T1 = ws.take<T>(k1 * n1), *T2 = ws.take<T>(k1 * n1), *T3 = ws.take<T>(k1 * n1), *T4 = ws.take<T>(k1 * n1);
+  T *W = ws.take<T>(m1 * n1), *V = ws.take<T>(m1 * n1), *X = ws.take<T>(m1 * n1);
+  const T one = T(1), mone = T(-1);
+#define SF_TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
+  // operand block sums (zero padded to m1 x k1 / k1 x n1)
+  SF_TRY(comb<T>(m1, k1, one, A21, lda, ak, m2, k1, one, A22, lda, ak, m2, k2, S1, m1, st));   // S1 = A21 + A22
+  SF_TRY(comb<T>(m1, k1, one, S1, m1, 0, m1, k1, mone, A11, lda, ak, m1, k1, S2, m1, st));     // S2 = S1 - A11
+  SF_TRY(comb<T>(m1, k1, one, A11, lda, ak, m1, k1, mone, A21, lda, ak, m2, k1, S3, m1, st));  // S3 = A11 - A21
+  SF_TRY(comb<T>(m1, k1, one, A12, lda, ak, m1, k2, mone, S2, m1, 0, m1, k1, S4, m1, st));     // S4 = A12 - S2
+  SF_TRY(comb<T>(k1, n1, one, B12, ldb, bkc, k1, n2, mone, B11, ldb, bkc, k1, n1, T1, k1, st)); // T1 = B12 - B11
+  SF_TRY(comb<T>(k1, n1, one, B22, ldb, bkc, k2, n2, mone, T1, k1, 0, k1, n1, T2, k1, st));     // T2 = B22 - T1
+  SF_TRY(comb<T>(k1, n1, one, B22, ldb, bkc, k2, n2, mone, B12, ldb, bkc, k1, n2, T3, k1, st)); // T3 = B22 - B12
+  SF_TRY(comb<T>(k1, n1, one, T2, k1, 0, k1, n1, mone, B21, ldb, bkc, k2, n1, T4, k1, st));     // T4 = T2 - B21
+  auto prod = [&](int64_t mm, int64_t nn, int64_t kk, const T* a, int64_t la, int aak, const T* b, int64_t lb, int bbk,
+                  double alpha, int beta, const T* cin, int64_t lci, T* c, int64_t lc) -> cudaError_t {
+    if (mm <= 0 || nn <= 0) return cudaSuccess;
+    Gemm<T> g{mm, nn, kk, a, la, aak, b, lb, bbk, cin, lci, c, lc, alpha, beta, kMaskNone, 1, nullptr, fail};
+    return run_gemm(g, st);
+  };
+  // products (gemm operands: plain temps are idx-contiguous: ak = 0; as B: bk = 1 means B[k + j*ld])
+  SF_TRY(prod(m1, n1, k1, A11, lda, ak, B11, ldb, bk, 1.0, 0, nullptr, 0, W, m1));  // W = P1
+  SF_TRY(comb<T>(m1, n1, one, Cin, ldcin, 0, m1, n1, mone, W, m1, 0, m1, n1, C, ldc, st));            // C11 = Cin11 - P1
+  SF_TRY(prod(m1, n1, k2, A12, lda, ak, B21, ldb, bk, -1.0, 1, C, ldc, C, ldc));   // C11 -= P2
+  SF_TRY(prod(m1, n1, k1, S2, m1, 0, T2, k1, 1, 1.0, 1, W, m1, W, m1));             // W = U2
+  SF_TRY(prod(m1, n1, k1, S3, m1, 0, T3, k1, 1, 1.0, 1, W, m1, V, m1));             // V = U3
+  SF_TRY(prod(m1, n1, k1, S1, m1, 0, T1, k1, 1, 1.0, 0, nullptr, 0, X, m1));        // X = P5
+  T* C21 = C + m1;
+  const T* Cin21 = Cin + m1;
+  SF_TRY(comb<T>(m2, n1, one, Cin21, ldcin, 0, m2, n1, mone, V, m1, 0, m1, n1, C21, ldc, st));         // C21 = Cin21 - U3
+  SF_TRY(prod(m2, n1, k2, A22, lda, ak, T4, k1, 1, 1.0, 1, C21, ldc, C21, ldc)); // C21 += P4
+  SF_TRY(comb<T>(m1, n1, one, V, m1, 0, m1, n1, one, X, m1, 0, m1, n1, V, m1, st));                    // V = U7
+  SF_TRY(comb<T>(m2, n2, one, Cin21 + n1 * ldcin, ldcin, 0, m2, n2, mone, V, m1, 0, m1, n1, C21 + n1 * ldc, ldc, st));
+  SF_TRY(comb<T>(m1, n1, one, W, m1, 0, m1, n1, one, X, m1, 0, m1, n1, W, m1, st));                    // W = U4
+  SF_TRY(comb<T>(m1, n2, one, Cin + n1 * ldcin, ldcin, 0, m1, n2, mone, W, m1, 0, m1, n1, C + n1 * ldc, ldc, st));
+  SF_TRY(prod(m1, n2, k2, S4, m1, 0, B22, ldb, bk, -1.0, 1, C + n1 * ldc, ldc, C + n1 * ldc, ldc));                                                                       // C12 -= P3
+#undef SF_TRY
+  return cudaSuccess;
+}
+
+inline bool strassen_applies(int64_t M, int64_t N, int64_t K) {
+  const StrassenCfg& c = strassen_cfg();
+  return c.levels > 0 && M >= c.min_dim && N >= c.min_dim && K >= 32;
+}
+
+// The flush C = Cin - op(A) op(B) (no mask): LU's A[c:n,c:n] -= R_L R_U, QR's M -= B_Q C.
+template <typename T>
+inline cudaError_t flush_general(int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, int ak, const T* B,
+                                 int64_t ldb, int bk, const T* Cin, int64_t ldcin, T* C, int64_t ldc,
+                                 const long long* fail, cudaStream_t st, int max_ctas = 0) {
+  if (sizeof(T) == 8 && strassen_applies(M, N, K))
+    return strassen_sub<T>(M, N, K, A, lda, ak, B, ldb, bk, Cin, ldcin, C, ldc, fail, st);
+  return gemm_sub<T>(M, N, K, A, lda, ak, B, ldb, bk, Cin, ldcin, C, ldc, kMaskNone, fail, st, max_ctas);
+}
+
+// The Cholesky flush C = Cin - R R^T on the lower triangle.  With Strassen on: the two
+// diagonal halves stay lower-masked SYRKs, the off-diagonal block C21 -= R2 R1^T is the
+// Strassen product.
+template <typename T>
+inline cudaError_t flush_lower(int64_t M, int64_t K, const T* R, int64_t ldr, const T* Cin, int64_t ldcin, T* C,
+                               int64_t ldc, const long long* fail, cudaStream_t st, int max_ctas = 0) {
+  const int64_t h = (M + 1) / 2;
+  if (!(sizeof(T) == 8 && strassen_applies(M - h, h, K)))
+    return gemm_sub<T>(M, M, K, R, ldr, 0, R, ldr, 0, Cin, ldcin, C, ldc, kMaskLower, fail, st, max_ctas);
+  cudaError_t e = gemm_sub<T>(h, h, K, R, ldr, 0, R, ldr, 0, Cin, ldcin, C, ldc, kMaskLower, fail, st);
+  if (e != cudaSuccess) return e;
+  e = strassen_sub<T>(M - h, h, K, R + h, ldr, 0, R, ldr, 0, Cin + h, ldcin, C + h, ldc, fail, st);
+  if (e != cudaSuccess) return e;
+  return gemm_sub<T>(M - h, M - h, K, R + h, ldr, 0, R + h, ldr, 0, Cin + h + h * ldcin, ldcin, C + h + h * ldc, ldc,
+                     kMaskLower, fail, st);
+}
+
 // SM reservation for the lookahead panel.  The flush's second part runs concurrently with
 // the factorization of the next panel; the panel is a chain of ~30 short dependent kernels,
 // and when the flush holds every SM each of them waits for a flush CTA to retire.  When the
@@ -418,7 +522,7 @@ inline cudaError_t qr_project(int64_t n, int64_t k, int64_t wc, const T* Qb, int
   Gemm<T> g1{k, wc, n, Qb, ldq, 1, Vin, ldvin, 1, nullptr, 0, Cw, k, 1.0, 0, kMaskNone, sp, split, fail};
   cudaError_t e = run_gemm(g1, st);
   if (e != cudaSuccess) return e;
-  return gemm_sub<T>(n, wc, k, Qb, ldq, 0, Cw, k, 1, Vin, ldvin, V, ldv, kMaskNone, fail, st);
+  return flush_general<T>(n, wc, k, Qb, ldq, 0, Cw, k, 1, Vin, ldvin, V, ldv, fail, st);
 }
 
 template <typename T>

@@ -74,6 +74,11 @@ cudaError_t split_tf32_kmajor(int64_t m, int64_t k, const float* X, int64_t ld, 
 // ---------------------------------------------------------------- panels (templated T)
 // Cholesky leaf (Alg. 1 inner loops) on columns [0,w) of the m x w block
 // whose top-left corner is the diagonal entry (z',z').  src may equal dst.
+// D = a op(X) + b op(Y) with zero padding outside each operand's extent (Strassen block sums)
+template <typename T>
+cudaError_t comb(int64_t rows, int64_t cols, T a, const T* X, int64_t ldx, int xkc, int64_t xr, int64_t xc, T b,
+                 const T* Y, int64_t ldy, int ykc, int64_t yr, int64_t yc, T* D, int64_t ldd, cudaStream_t st);
+
 template <typename T>
 cudaError_t chol_leaf(int64_t m, int w, const T* src, int64_t lds, T* dst, int64_t ldd,
                       int64_t col0, long long* fail, cudaStream_t st);

@@ -821,12 +821,38 @@ cudaError_t copy_matrix(int64_t m, int64_t n, const T* src, int64_t lds, T* dst,
   return cudaGetLastError();
 }
 
+// D(i, j) = a X(i, j) + b Y(i, j) over rows x cols; X(i, j) = 0 outside its xr x xc extent
+// (zero padding of the uneven Strassen blocks), op(X)(i, j) = xkc ? X[j + i ldx] : X[i + j ldx]
+// (Y likewise).  Memory-bound elementwise pass (the Strassen-Winograd block sums, f1).
+template <typename T>
+__global__ void comb_kernel(int64_t rows, int64_t cols, T a, const T* X, int64_t ldx, int xkc, int64_t xr, int64_t xc,
+                            T b, const T* Y, int64_t ldy, int ykc, int64_t yr, int64_t yc, T* D, int64_t ldd) {
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
+      const T x = (X && i < xr && j < xc) ? __ldcg(X + (xkc ? j + i * ldx : i + j * ldx)) : T(0);
+      const T y = (Y && i < yr && j < yc) ? __ldcg(Y + (ykc ? j + i * ldy : i + j * ldy)) : T(0);
+      D[i + j * ldd] = a * x + b * y;
+    }
+}
+template <typename T>
+cudaError_t comb(int64_t rows, int64_t cols, T a, const T* X, int64_t ldx, int xkc, int64_t xr, int64_t xc, T b,
+                 const T* Y, int64_t ldy, int ykc, int64_t yr, int64_t yc, T* D, int64_t ldd, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  const unsigned gx = (unsigned)((rows + 255) / 256 > 4 ? 4 : (rows + 255) / 256);
+  const unsigned gy = (unsigned)(cols < 4096 ? cols : 4096);
+  comb_kernel<T><<<dim3(gx, gy), 256, 0, st>>>(rows, cols, a, X, ldx, xkc, xr, xc, b, Y, ldy, ykc, yr, yc, D, ldd);
+  count_launch();
+  return cudaGetLastError();
+}
+
 #define SF_INST(T)                                                                                             \
   template cudaError_t qr_mgs_panel<T>(int64_t, int, const T*, int64_t, T*, int64_t, int64_t, const T*, T*,  \
                                        long long*, cudaStream_t);                                             \
   template cudaError_t frob_norm_tol<T>(int64_t, const T*, int64_t, T*, double*, cudaStream_t);                   \
   template cudaError_t zero_strict_lower<T>(int64_t, T*, int64_t, cudaStream_t);                             \
-  template cudaError_t copy_matrix<T>(int64_t, int64_t, const T*, int64_t, T*, int64_t, cudaStream_t);
+  template cudaError_t copy_matrix<T>(int64_t, int64_t, const T*, int64_t, T*, int64_t, cudaStream_t);             \
+  template cudaError_t comb<T>(int64_t, int64_t, T, const T*, int64_t, int, int64_t, int64_t, T, const T*, int64_t, int, \
+                               int64_t, int64_t, T*, int64_t, cudaStream_t);
 SF_INST(double)
 SF_INST(float)
 

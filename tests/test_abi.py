@@ -110,3 +110,12 @@ def test_new_entry_points_reject_bad_arguments(L):
     assert L.chol_factor_dist(None, 4, 2, 0, arr, arr, 4, iarr, None) == 1             # null comm
     assert L.sf_comm_init_loopback(None, 2) == 1
     assert L.sf_local_cols(10, 3, 2, 5) == 0
+
+
+def test_set_strassen_arguments(L):
+    """sf_set_strassen validates synchronously (no GPU needed) and 0 restores the default."""
+    SF_EINVAL = 1
+    assert L.sf_set_strassen(2, 4096) == SF_EINVAL
+    assert L.sf_set_strassen(1, 10) == SF_EINVAL
+    assert L.sf_set_strassen(-1, 4096) == SF_EINVAL
+    assert L.sf_set_strassen(0, 4096) == 0
