@@ -19,7 +19,8 @@
 // Right-looking form (each column sees the same projections in the same order): when q_c
 // is done every later panel column is projected once.  The norm of v_c and its dot
 // products with the later columns come from ONE grid-wide reduction (Gram row), so the
-// persistent cooperative kernel needs one grid barrier per column.
+// persistent kernel needs one grid-wide exchange per column (qr_mgs_ll_kernel below: two-level,
+// through distributed shared memory within clusters and epoch-tagged words across them).
 #include <math.h>
 #include <stdlib.h>
 
