@@ -556,22 +556,28 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_kernel(int64_t m, int64_t ncr,
 // below / stage their U columns; then one __syncthreads and the independent substitutions.
 // Same per-element arithmetic as lu_leaf_kernel (interleaved partial sums, one subtraction,
 // U_ci = t / L_cc in the block, * 1/L_cc for the U columns).
-template <typename T, int W>
+template <typename T, int W, bool ROT>
 __global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t ncr, int w, const T* __restrict__ src,
                                                               int64_t lds, T* __restrict__ dst, int64_t ldd,
                                                               int64_t col0, const T* tolp, long long* fail,
                                                               int nrow_blocks) {
   if (failed(fail)) return;
-  __shared__ __align__(16) T Lt[W][W + 2];   // L11 transposed (Lt[k][i] = L_ik): column k contiguous
-  __shared__ __align__(16) T Us[W][W + 2];   // U11 (Us[k][j] = U_kj): row k contiguous
+  // ROT: rows of Lt / Us zero-padded to 2W so the rolled (register-rotating) substitutions can
+  // read past the block; dynamic shared memory (about 50 KB for fp64)
+  constexpr int LW = ROT ? 2 * W : W + 2;
+  extern __shared__ __align__(16) unsigned char lusm[];
+  T (*Lt)[LW] = reinterpret_cast<T (*)[LW]>(lusm);              // L11 transposed (Lt[k][i] = L_ik)
+  T (*Us)[LW] = reinterpret_cast<T (*)[LW]>(lusm + sizeof(T) * W * LW);   // U11 (Us[k][j] = U_kj)
+  T (*S)[W + 1] = reinterpret_cast<T (*)[W + 1]>(lusm + 2 * sizeof(T) * W * LW);   // U column staging
   __shared__ T inv[W];
-  __shared__ T S[kUCols][W + 1]; // staging for the U columns
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool rowblock = (int)blockIdx.x < nrow_blocks;
   const int64_t r = w + (int64_t)blockIdx.x * kLeafT + tid;
   const int64_t j0 = w + (int64_t)(blockIdx.x - nrow_blocks) * kUCols;
   const int ncols = rowblock ? 0 : (int)((w + ncr - j0) < kUCols ? (w + ncr - j0) : kUCols);
+  if (ROT)
+    for (int idx = tid; idx < W * W; idx += kLeafT) { Lt[idx / W][W + idx % W] = T(0); Us[idx / W][W + idx % W] = T(0); }
   if (warp == 0) {
     // Right-looking in registers, the paper's per-element order (every
     // entry receives its -L_ik U_k* terms one at a time in k order): lane i holds row i of
@@ -639,6 +645,18 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t
   if (rowblock) {
     // L rows below: L_rc = A_rc - sum_{k<c} L_rk U_kc, right-looking (terms in k order)
     if (r >= m) return;
+    if (ROT) {
+#pragma unroll 1
+      for (int c = 0; c < w; ++c) {   // x[0] is column c of my row
+        const T x0 = x[0];
+        dst[r + (int64_t)c * ldd] = x0;
+        const T* u = &Us[c][c];       // u[j] = U_{c, c+j}, 0 past the block
+#pragma unroll
+        for (int j = 1; j < W; ++j) x[j - 1] = fma(-x0, u[j], x[j]);
+        x[W - 1] = T(0);
+      }
+      return;
+    }
 #pragma unroll
     for (int c = 0; c < W; ++c) {
       const T xc = x[c];
@@ -655,14 +673,26 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t
     T y[W];
 #pragma unroll
     for (int k = 0; k < W; ++k) y[k] = (k < w) ? S[tid][k] : T(0);
+    if (ROT) {
+#pragma unroll 1
+      for (int c = 0; c < w; ++c) {   // y[0] is row c of my column
+        const T y0 = y[0] * inv[c];
+        S[tid][c] = y0;
+        const T* l = &Lt[c][c];       // l[j] = L_{c+j, c}, 0 past the block
 #pragma unroll
-    for (int c = 0; c < W; ++c) {   // right-looking: y_c *= 1/L_cc, then y_j -= L_jc y_c
-      y[c] = y[c] * inv[c];
+        for (int j = 1; j < W; ++j) y[j - 1] = fma(-l[j], y0, y[j]);
+        y[W - 1] = T(0);
+      }
+    } else {
 #pragma unroll
-      for (int j = c + 1; j < W; ++j) y[j] = fma(-Lt[c][j], y[c], y[j]);
+      for (int c = 0; c < W; ++c) {   // right-looking: y_c *= 1/L_cc, then y_j -= L_jc y_c
+        y[c] = y[c] * inv[c];
+#pragma unroll
+        for (int j = c + 1; j < W; ++j) y[j] = fma(-Lt[c][j], y[c], y[j]);
+      }
+#pragma unroll
+      for (int k = 0; k < W; ++k) S[tid][k] = y[k];
     }
-#pragma unroll
-    for (int k = 0; k < W; ++k) S[tid][k] = y[k];
   }
   __syncthreads();
   for (int jj = warp; jj < ncols; jj += kLeafT / 32)
@@ -684,10 +714,20 @@ cudaError_t lu_leaf(int64_t m, int64_t ncr, int w, const T* src, int64_t lds, T*
   int grid = nrb + ncb;
   if (grid == 0) grid = 1;
   if (lu_leaf_warp_on()) {
-    if (w <= 16) lu_leaf_warp_kernel<T, 16><<<grid, kLeafT, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
-    else if (w <= 32)
-      lu_leaf_warp_kernel<T, 32><<<grid, kLeafT, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
+    static const bool rot = [] { const char* e = getenv("SF_LU_LEAF_ROT"); return e && atoi(e) != 0; }();
+    auto go = [&](auto kern, int W) -> cudaError_t {
+      const int lw = rot ? 2 * W : W + 2;
+      const size_t smem = sizeof(T) * ((size_t)2 * W * lw + (size_t)kUCols * (W + 1));
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, kLeafT, smem, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
+      return cudaSuccess;
+    };
+    cudaError_t e;
+    if (w <= 16) e = rot ? go(lu_leaf_warp_kernel<T, 16, true>, 16) : go(lu_leaf_warp_kernel<T, 16, false>, 16);
+    else if (w <= 32) e = rot ? go(lu_leaf_warp_kernel<T, 32, true>, 32) : go(lu_leaf_warp_kernel<T, 32, false>, 32);
     else return cudaErrorInvalidValue;
+    if (e != cudaSuccess) return e;
   } else if (w <= 16) lu_leaf_kernel<T, 16><<<grid, kLeafT, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
   else if (w <= 32) lu_leaf_kernel<T, 32><<<grid, kLeafT, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
   else return cudaErrorInvalidValue;
