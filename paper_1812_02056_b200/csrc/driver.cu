@@ -238,6 +238,13 @@ static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int
 }
 
 
+// Early R row blocks on a low-priority stream (SF_QR_EARLY_R=1): measured slower — the
+// long-K R tiles hold SM slots the flushes need (cfg4 89.3 vs 83.8 ms) — off by default.
+static bool qr_early_r_on() {
+  static const int on = [] { const char* e = getenv("SF_QR_EARLY_R"); return e ? atoi(e) : 0; }();
+  return on != 0;
+}
+
 template <typename T>
 static int qr_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* Q, int64_t ldq, T* R, int64_t ldr,
                   int64_t* d_info, cudaStream_t st) {
@@ -275,11 +282,33 @@ static int qr_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* Q, int6
   Side* sd = nullptr;
   const bool la = lookahead_on() && S.P() > 1;
   if (la) SF_CUDA(side_stream(sd));
+  // R := Q^T A by row blocks as soon as their Q columns are final: the
+  // rows [z, z+w) of R need only Q[:, z:z+w) (later flushes never touch it), so each block
+  // runs on a low-priority stream in the SM slots the short-K flushes leave idle, instead
+  // of one n^3 product after the last panel.  Every element is the same K-ordered dot
+  // product as in the one-shot product (tile-local DMMA accumulation over k = 0..n-1).
+  Side* rs = nullptr;
+  const bool early_r = qr_early_r_on();
+  if (early_r) {
+    SF_CUDA(low_stream(rs));
+    SF_CUDA(fork_join(*rs, st, rs->st));
+    SF_CUDA(zero_strict_lower<T>(n, R, ldr, rs->st));
+  }
+  auto r_rows = [&](int64_t z, int64_t w, cudaStream_t from) -> int {
+    if (!early_r) return SF_OK;
+    SF_CUDA(fork_join(*rs, from, rs->st));
+    ProfScope ps(2, (double)w * (double)n * (double)(2 * (n - z) - w + 1), rs->st);
+    Gemm<T> g{w, n - z, n, Q + z * ldq, ldq, 1, A + z * lda, lda, 1, nullptr, 0, R + z + z * ldr, ldr, 1.0, 0,
+              kMaskUpper, 1, nullptr, fail};
+    SF_CUDA(run_gemm(g, rs->st));
+    return SF_OK;
+  };
   {
     ProfScope ps(1, 0.0, st);
     const int64_t w0 = S.w(0);
     SF_CUDA(qr_panel<T>(n, w0, A, lda, Q, ldq, 0, tol, mgsw, Cw, split, split_elems, fail, st));
   }
+  if (int rc = r_rows(0, S.w(0), st)) return rc;
   for (int64_t p = 0; p + 1 < S.P(); ++p) {
     const int64_t z = S.z(p), w = S.w(p), c = z + w;
     const int64_t w2 = S.w(p + 1), m = n - c;
@@ -301,6 +330,7 @@ static int qr_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* Q, int6
       SF_CUDA(qr_panel<T>(n, w2, Q + c * ldq, ldq, Q + c * ldq, ldq, c, tol, mgsw, Cw2, split2, split_elems, fail,
                           pst));
     }
+    if (int rc = r_rows(c, w2, pst)) return rc;
     if (la) {
       if (m > w2) {
         const int64_t c2 = c + w2;
@@ -311,9 +341,11 @@ static int qr_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* Q, int6
       SF_CUDA(fork_join(*sd, sd->st, st));
     }
   }
-  // R := Q^T A: upper triangle on the tensor cores, exact zeros below
-  SF_CUDA(zero_strict_lower<T>(n, R, ldr, st));
-  {
+  if (early_r) {
+    SF_CUDA(fork_join(*rs, rs->st, st));   // the caller's stream waits for the last R block
+  } else {
+    // R := Q^T A: upper triangle on the tensor cores, exact zeros below
+    SF_CUDA(zero_strict_lower<T>(n, R, ldr, st));
     ProfScope ps(2, (double)n * (double)n * (double)(n + 1), st);
     Gemm<T> g{n, n, n, Q, ldq, 1, A, lda, 1, nullptr, 0, R, ldr, 1.0, 0, kMaskUpper, 1, nullptr, fail};
     SF_CUDA(run_gemm(g, st));

@@ -190,6 +190,24 @@ inline cudaError_t side_stream(Side*& out) {
   out = &sd;
   return cudaSuccess;
 }
+// A second, LOW-priority side stream: background work that only fills SM slots the
+// factorization's own kernels leave free (QR's early R row blocks).
+inline cudaError_t low_stream(Side*& out) {
+  static Side sides[16];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  Side& sd = sides[dev & 15];
+  if (!sd.st) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    e = cudaStreamCreateWithPriority(&sd.st, cudaStreamNonBlocking, lo);
+    if (e != cudaSuccess) return e;
+    for (int i = 0; i < 8; ++i) { cudaEvent_t ev; cudaEventCreateWithFlags(&ev, cudaEventDisableTiming); sd.ev.push_back(ev); }
+  }
+  out = &sd;
+  return cudaSuccess;
+}
 // record on `from`, make `to` wait
 inline cudaError_t fork_join(Side& sd, cudaStream_t from, cudaStream_t to) {
   cudaEvent_t e = sd.event();
