@@ -19,6 +19,8 @@
 // the (now idle) pipeline shared memory, then every warp streams whole 1 KB columns of C:
 // all loads of a thread are issued before the first store, in 16-byte vectors, so the
 // read-modify-write costs about one L2/HBM round trip per tile instead of one per atom.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "tiles.cuh"
@@ -35,7 +37,7 @@ constexpr int PAD_KI = BK + 4;    // smem row stride (doubles) for k-contiguous 
 template <int NIDX> struct Slice {
   static constexpr int PAD_IK = NIDX + 4;   // row stride for idx-contiguous slices (== 4 mod 16)
   static constexpr int ELEMS = (BK * PAD_IK > NIDX * PAD_KI) ? BK * PAD_IK : NIDX * PAD_KI;
-  static constexpr int CHUNKS = NIDX * BK / 2 / THREADS;   // 16-byte chunks per thread
+  template <int NT> static constexpr int chunks() { return NIDX * BK / 2 / NT; }   // 16-byte chunks per thread
 };
 constexpr int OPER_A = Slice<BM>::ELEMS, OPER_B = Slice<BN>::ELEMS;
 constexpr int STAGE = OPER_A + OPER_B;
@@ -49,14 +51,14 @@ static_assert(2 * SMEM <= 227 * 1024, "two CTAs per SM");
 // Load an NIDX (idx) x BK (k) slice of op(X) into shared memory.
 //  KC=false: op(X)(idx,k) = X[idx + k*ld]  (idx contiguous)  -> Xs[k*PAD_IK + idx]
 //  KC=true : op(X)(idx,k) = X[k + idx*ld]  (k contiguous)    -> Xs[idx*PAD_KI + k]
-template <int NIDX, bool KC, bool V16>
+template <int NIDX, bool KC, bool V16, int NT = g64::THREADS>
 __device__ __forceinline__ void load_slice(double* Xs, const double* __restrict__ X, int64_t ld,
                                            int64_t idx0, int64_t nidx, int64_t k0, int64_t K, int tid) {
   using namespace g64;
   using S = Slice<NIDX>;
 #pragma unroll
-  for (int r = 0; r < S::CHUNKS; ++r) {
-    const int id = tid + r * THREADS;
+  for (int r = 0; r < S::template chunks<NT>(); ++r) {
+    const int id = tid + r * NT;
     int64_t idx, kg;
     double* dst;
     if (!KC) {
@@ -104,15 +106,18 @@ __host__ __device__ __forceinline__ int masked_tiles(int mask, int TM, int TN, i
   return T64::count(mask, TM, TN, off);
 }
 
-template <bool AK, bool BKC, bool V16, int MASK>
+template <bool AK, bool BKC, bool V16, int MASK, int NT = g64::THREADS>
 __device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vecC) {
   using namespace g64;
+  // NT = 128: 4 warps as 2 (i) x 2 (j), warp tile 64 x 32; NT = 256 (short K): 8 warps as
+  // 4 x 2, warp tile 32 x 32 — twice the issuing warps per SM sub-partition
+  constexpr int NWARP = NT / 32, WARPS_M = NWARP / 2, WTM = BM / WARPS_M, ATM = WTM / 8;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;                       // [STAGES][OPER_A]
   double* Bs = smem + STAGES * OPER_A;     // [STAGES][OPER_B]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   const int TM = (int)((p.M + BM - 1) / BM), TN = (int)((p.N + BN - 1) / BN);
   int ti, tj;
   if (p.rs.ngroups > 0) T64::tile_of_raster(MASK, bid, TM, p.off, p.rs, ti, tj);
@@ -130,16 +135,16 @@ __device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vec
   // Warm L2 with the C tile we will read-modify-write in the epilogue.
   if (p.beta && p.splits == 1) {
 #pragma unroll
-    for (int r = 0; r < BN * 8 / THREADS; ++r) {
-      const int id = tid + r * THREADS;      // BN columns x 8 lines of 128 B
+    for (int r = 0; r < BN * 8 / NT; ++r) {
+      const int id = tid + r * NT;           // BN columns x 8 lines of 128 B
       const int64_t jj = j0 + (id >> 3), ii = i0 + (id & 7) * 16;
       if (jj < p.N && ii < p.M) prefetch_l2(p.Cin + ii + jj * p.ldcin);
     }
   }
 
-  double acc[8][4][2];
+  double acc[ATM][4][2];
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < ATM; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
@@ -147,8 +152,8 @@ __device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vec
     if (kb < nk) {
       const int slot = kb % STAGES;
       const int64_t k0 = kbeg + (int64_t)kb * BK;
-      load_slice<BM, AK, V16>(As + slot * OPER_A, p.A, p.lda, i0, p.M, k0, kend, tid);
-      load_slice<BN, BKC, V16>(Bs + slot * OPER_B, p.B, p.ldb, j0, p.N, k0, kend, tid);
+      load_slice<BM, AK, V16, NT>(As + slot * OPER_A, p.A, p.lda, i0, p.M, k0, kend, tid);
+      load_slice<BN, BKC, V16, NT>(Bs + slot * OPER_B, p.B, p.ldb, j0, p.N, k0, kend, tid);
     }
     cp_async_commit();
   };
@@ -162,9 +167,9 @@ __device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vec
     issue(kb + STAGES - 1);
     const double* as = As + (kb % STAGES) * OPER_A;
     const double* bs = Bs + (kb % STAGES) * OPER_B;
-    double fa[2][8], fb[2][4];
+    double fa[2][ATM], fb[2][4];
 #pragma unroll
-    for (int a = 0; a < 8; ++a) fa[0][a] = frag<BM, AK>(as, wm * 64 + a * 8, 0, lane);
+    for (int a = 0; a < ATM; ++a) fa[0][a] = frag<BM, AK>(as, wm * WTM + a * 8, 0, lane);
 #pragma unroll
     for (int b = 0; b < 4; ++b) fb[0][b] = frag<BN, BKC>(bs, wn * 32 + b * 8, 0, lane);
 #pragma unroll
@@ -172,12 +177,12 @@ __device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vec
       const int cur = kk & 1, nxt = cur ^ 1;
       if (kk + 1 < BK / 4) {
 #pragma unroll
-        for (int a = 0; a < 8; ++a) fa[nxt][a] = frag<BM, AK>(as, wm * 64 + a * 8, kk + 1, lane);
+        for (int a = 0; a < ATM; ++a) fa[nxt][a] = frag<BM, AK>(as, wm * WTM + a * 8, kk + 1, lane);
 #pragma unroll
         for (int b = 0; b < 4; ++b) fb[nxt][b] = frag<BN, BKC>(bs, wn * 32 + b * 8, kk + 1, lane);
       }
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
+      for (int a = 0; a < ATM; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b)
           // D = C^T: the MMA's A operand is op(B) (rows j), its B operand is op(A) (cols i)
@@ -190,8 +195,8 @@ __device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vec
   // ---- epilogue, step 1: park the accumulator tile in shared memory, Cs[j*CPAD + i]
   double* Cs = smem;
 #pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const int il = wm * 64 + a * 8 + 2 * (lane & 3);
+  for (int a = 0; a < ATM; ++a) {
+    const int il = wm * WTM + a * 8 + 2 * (lane & 3);
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int jl = wn * 32 + b * 8 + (lane >> 2);
@@ -202,7 +207,7 @@ __device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vec
 
   // ---- step 2: each warp streams BN/4 whole columns; lane owns rows 2*lane+{0,1} and
   //      64+2*lane+{0,1} (each warp instruction covers 512 contiguous bytes of a column)
-  constexpr int COLS = BN / (THREADS / 32);
+  constexpr int COLS = BN / NWARP;
   if (p.splits > 1) {
     double* W = p.work + (int64_t)sp * p.M * p.N;
     for (int q = 0; q < COLS; ++q) {
@@ -263,10 +268,10 @@ __device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vec
   }
 }
 
-template <bool AK, bool BKC, bool V16, int MASK>
-__global__ void __launch_bounds__(g64::THREADS, 2) gemm_f64_kernel(GemmF64 p, int vecC) {
+template <bool AK, bool BKC, bool V16, int MASK, int NT = g64::THREADS>
+__global__ void __launch_bounds__(NT, 2) gemm_f64_kernel(GemmF64 p, int vecC) {
   if (p.fail && failed(p.fail)) return;
-  gemm_f64_body<AK, BKC, V16, MASK>(p, blockIdx.x, vecC);
+  gemm_f64_body<AK, BKC, V16, MASK, NT>(p, blockIdx.x, vecC);
 }
 
 // Bounded grid (max_ctas > 0): each CTA loops over tiles, leaving SMs to a concurrent stream.
@@ -306,6 +311,11 @@ __global__ void splitk_reduce_f64(GemmF64 p) {
   }
 }
 
+static bool short_k_wide() {
+  static const int on = [] { const char* e = getenv("SF_GEMM_SHORTK8"); return e ? atoi(e) : 1; }();
+  return on != 0;
+}
+
 template <bool AK, bool BKC, bool V16, int MASK>
 static cudaError_t launch_t(const GemmF64& p, const GemmGroups* gs, int ntiles, int vecC, cudaStream_t st) {
   static bool attr_set = false;  // per template instance
@@ -318,6 +328,9 @@ static cudaError_t launch_t(const GemmF64& p, const GemmGroups* gs, int ntiles, 
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_f64_loop_kernel<AK, BKC, V16, MASK>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g64::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_f64_kernel<AK, BKC, V16, MASK, 256>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g64::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -326,6 +339,10 @@ static cudaError_t launch_t(const GemmF64& p, const GemmGroups* gs, int ntiles, 
   else if (p.max_ctas > 0 && p.max_ctas < ntiles) {
     grid.x = p.max_ctas;
     gemm_f64_loop_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, vecC);
+  } else if (p.K <= 128 && short_k_wide()) {
+    // short K: the per-tile prologue/epilogue is a large share of each tile; 8-warp CTAs keep
+    // two issuing warps per SM sub-partition through the co-resident CTA's epilogue
+    gemm_f64_kernel<AK, BKC, V16, MASK, 256><<<grid, 256, g64::SMEM, st>>>(p, vecC);
   } else gemm_f64_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, vecC);
   count_launch();
   return cudaGetLastError();
