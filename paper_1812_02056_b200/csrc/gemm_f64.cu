@@ -315,6 +315,10 @@ static bool short_k_wide() {
   static const int on = [] { const char* e = getenv("SF_GEMM_SHORTK8"); return e ? atoi(e) : 1; }();
   return on != 0;
 }
+static int64_t short_k_max() {
+  static const int64_t k = [] { const char* e = getenv("SF_GEMM_SHORTK8_MAXK"); return e ? (int64_t)atoll(e) : (int64_t)256; }();
+  return k;
+}
 
 template <bool AK, bool BKC, bool V16, int MASK>
 static cudaError_t launch_t(const GemmF64& p, const GemmGroups* gs, int ntiles, int vecC, cudaStream_t st) {
@@ -339,7 +343,7 @@ static cudaError_t launch_t(const GemmF64& p, const GemmGroups* gs, int ntiles, 
   else if (p.max_ctas > 0 && p.max_ctas < ntiles) {
     grid.x = p.max_ctas;
     gemm_f64_loop_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, vecC);
-  } else if (p.K <= 128 && short_k_wide()) {
+  } else if (p.K <= short_k_max() && short_k_wide()) {
     // short K: the per-tile prologue/epilogue is a large share of each tile; 8-warp CTAs keep
     // two issuing warps per SM sub-partition through the co-resident CTA's epilogue
     gemm_f64_kernel<AK, BKC, V16, MASK, 256><<<grid, 256, g64::SMEM, st>>>(p, vecC);
