@@ -176,6 +176,11 @@ static int chol_run_f32(int64_t n, const Sched& S, const float* A, int64_t lda, 
   return SF_OK;
 }
 
+static int64_t lu_la_min_m() {
+  static const int64_t v = [] { const char* e = getenv("SF_LU_LA_MIN_M"); return e ? (int64_t)atoll(e) : (int64_t)4096; }();
+  return v;
+}
+
 template <typename T>
 static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int64_t ldd, int64_t* d_info,
                   cudaStream_t st) {
@@ -201,8 +206,12 @@ static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int
     const int64_t lds = (z == 0) ? lda : ldd;
     const T* RL = LU + c + z * ldd;   // R_L = L[c:n, z:c)
     const T* RU = LU + z + c * ldd;   // R_U = U[z:c, c:n)
-    cudaStream_t pst = la ? sd->st : st;
-    if (la) {
+    // lookahead pays only while the trailing matrix is large: below SF_LU_LA_MIN_M (4096)
+    // the L-shaped first flush part (two launches) and the fork/join cost more than the
+    // overlap gains (n = 4096: 6.44 ms with, 6.26 without; n = 8192: 24.5 vs 25.8)
+    const bool lap = la && m > lu_la_min_m();
+    cudaStream_t pst = lap ? sd->st : st;
+    if (lap) {
       ProfScope ps(0, 2.0 * w * ((double)m * m - (double)(m - w2) * (m - w2)), st);
       // flush, part 1: columns [c, c+w2) (all rows >= c) and rows [c, c+w2) right of them
       SF_CUDA(gemm_sub<T>(m, w2, w, RL, ldd, 0, RU, ldd, 1, src + c + c * lds, lds, LU + c + c * ldd, ldd, kMaskNone,
@@ -222,7 +231,7 @@ static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int
       ProfScope ps(1, 0.0, pst);
       SF_CUDA(lu_panel_rec<T>(m, w2, m - w2, LU + c + c * ldd, ldd, LU + c + c * ldd, ldd, c, tol, fail, pst));
     }
-    if (la) {
+    if (lap) {
       if (m > w2) {  // flush, part 2: the remaining trailing block, concurrently with the panel
         const int64_t c2 = c + w2;
         const double fl = 2.0 * w * (double)(m - w2) * (double)(m - w2);
