@@ -115,7 +115,9 @@ int qr_solve(int64_t n, int64_t nrhs, int dtype, const void* dQ, int64_t ldq, co
  * chol_factor_host moves only the lower triangle (incl. diagonal), panel by panel, and
  * copies each panel of L back as soon as it is final, overlapped with the remaining
  * flushes.  The strict upper triangle of hL is unspecified out of place (entries inside the
- * s x s diagonal blocks receive A's values); in place (hL == hA) it keeps A's values. */
+ * s x s diagonal blocks receive A's values); in place (hL == hA) it keeps A's values.
+ * lu_factor_host copies each panel's L columns and U rows back as soon as the panel is
+ * factored, overlapped with the remaining flushes. */
 int chol_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hL, int64_t ldl,
                      int64_t* info);
 int lu_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hLU, int64_t ldlu,

@@ -183,7 +183,7 @@ static int64_t lu_la_min_m() {
 
 template <typename T>
 static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int64_t ldd, int64_t* d_info,
-                  cudaStream_t st) {
+                  cudaStream_t st, PanelHook* hook = nullptr) {
   Workspace ws;
   SF_CUDA(ws.init(16384, st));
   long long* fail = ws.take<long long>(2);   // [0] first failed column, [1] leaf counter
@@ -198,6 +198,7 @@ static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int
     ProfScope ps(1, 0.0, st);
     const int64_t w0 = S.w(0);
     SF_CUDA(lu_panel_rec<T>(n, w0, n - w0, A, lda, LU, ldd, 0, tol, fail, st));
+    if (hook) SF_CUDA(hook->done(0, w0, st));   // L[0:n, 0:w0) and U[0:w0, w0:n) are final
   }
   for (int64_t p = 0; p + 1 < S.P(); ++p) {
     const int64_t z = S.z(p), w = S.w(p), c = z + w;
@@ -230,6 +231,7 @@ static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int
     {
       ProfScope ps(1, 0.0, pst);
       SF_CUDA(lu_panel_rec<T>(m, w2, m - w2, LU + c + c * ldd, ldd, LU + c + c * ldd, ldd, c, tol, fail, pst));
+      if (hook) SF_CUDA(hook->done(c, w2, pst));
     }
     if (lap) {
       if (m > w2) {  // flush, part 2: the remaining trailing block, concurrently with the panel
@@ -697,8 +699,40 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
   e = cudaMemcpy2DAsync(d, n * elt, hA, lda * elt, n * elt, n, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) {
     if (kind == 1) {
-      rc = lu_factor(n, s, dtype, d, n, d, n, dinfo, st);
-      if (!rc) e = cudaMemcpy2DAsync(hO1, ld1 * elt, d, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);
+      // LU: each panel's L columns [z, z+w) (rows >= z) and U rows [z, z+w) (columns >= z+w)
+      // are final once the panel is factored; return them on a copy stream while the later
+      // flushes run, as for Cholesky.
+      static cudaStream_t lstreams[16] = {};
+      static cudaEvent_t levents[16] = {};
+      if (!lstreams[devh & 15]) {
+        SF_CUDA(cudaStreamCreateWithFlags(&lstreams[devh & 15], cudaStreamNonBlocking));
+        SF_CUDA(cudaEventCreateWithFlags(&levents[devh & 15], cudaEventDisableTiming));
+      }
+      struct LuD2H : PanelHook {
+        int64_t n, ldh; size_t elt; const char* dev; char* host; cudaStream_t cs; cudaEvent_t ev;
+        cudaError_t done(int64_t z, int64_t w, cudaStream_t pst) override {
+          cudaError_t r = cudaEventRecord(ev, pst);
+          if (r == cudaSuccess) r = cudaStreamWaitEvent(cs, ev, 0);
+          if (r == cudaSuccess)   // L columns (incl. the diagonal block's U part)
+            r = cudaMemcpy2DAsync(host + elt * (z + z * ldh), ldh * elt, dev + elt * (z + z * n), n * elt,
+                                  (n - z) * elt, w, cudaMemcpyDeviceToHost, cs);
+          if (r == cudaSuccess && z + w < n)   // U rows right of the panel
+            r = cudaMemcpy2DAsync(host + elt * (z + (z + w) * ldh), ldh * elt, dev + elt * (z + (z + w) * n), n * elt,
+                                  w * elt, n - z - w, cudaMemcpyDeviceToHost, cs);
+          return r;
+        }
+      } hook;
+      hook.n = n; hook.ldh = ld1; hook.elt = elt; hook.dev = d; hook.host = (char*)hO1;
+      hook.cs = lstreams[devh & 15]; hook.ev = levents[devh & 15];
+      SF_CUDA(cudaEventRecord(hook.ev, st));   // the copy stream must not run ahead of the previous call
+      SF_CUDA(cudaStreamWaitEvent(hook.cs, hook.ev, 0));
+      const Sched S(n, s);
+      rc = dtype == SF_F64 ? lu_run<double>(n, S, (const double*)d, n, (double*)d, n, dinfo, st, &hook)
+                           : lu_run<float>(n, S, (const float*)d, n, (float*)d, n, dinfo, st, &hook);
+      if (!rc) {
+        e = cudaEventRecord(hook.ev, hook.cs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hook.ev, 0);
+      }
     } else {
       rc = qr_factor(n, s, dtype, d, n, d + bytes, n, d + 2 * bytes, n, dinfo, st);
       if (!rc) e = cudaMemcpy2DAsync(hO1, ld1 * elt, d + bytes, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);

@@ -516,3 +516,19 @@ def test_qr_mgs_cluster_geometries(n, s):
     Qt = torch.from_numpy(Qg).cuda(); At = torch.from_numpy(A).cuda(); Rt = torch.from_numpy(Rg).cuda()
     assert float((Qt.mT @ Qt - torch.eye(n, device="cuda", dtype=torch.float64)).norm()) <= 1e-12 * n
     assert float((At - Qt @ Rt).norm() / At.norm()) <= 1e-13 * n
+
+
+@pytest.mark.parametrize("n,s", [(300, 64), (4608, 256)])
+def test_lu_host_overlapped_copies(n, s):
+    """lu_factor_host returns each panel's L columns and U rows while later flushes run
+    (DESIGN.md §6 e2e): the host result must equal the device entry point's bit for bit,
+    both triangles, incl. a ragged last panel and (n = 4608) the lookahead stream."""
+    B = synth.gen_numpy("diag_dominant", n, seed=n)
+    out, info = sf.lu_host(np.asfortranarray(B.copy()), s)
+    Lg, Ug, ig = run_lu(B, s)
+    assert info == ig == 0
+    assert np.array_equal(np.tril(out), Lg)
+    assert np.array_equal(np.triu(out, 1) + np.eye(n), Ug)
+    if n <= 300:
+        Lo, Uo, _ = oracle.lu(B, s)
+        assert synth.r2_error(np.triu(out, 1) + np.eye(n), Uo) <= TOL64
