@@ -117,7 +117,8 @@ int qr_solve(int64_t n, int64_t nrhs, int dtype, const void* dQ, int64_t ldq, co
  * flushes.  The strict upper triangle of hL is unspecified out of place (entries inside the
  * s x s diagonal blocks receive A's values); in place (hL == hA) it keeps A's values.
  * lu_factor_host copies each panel's L columns and U rows back as soon as the panel is
- * factored, overlapped with the remaining flushes. */
+ * factored, qr_factor_host each panel of Q (R, computed last, follows), overlapped with
+ * the remaining work. */
 int chol_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hL, int64_t ldl,
                      int64_t* info);
 int lu_factor_host(int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hLU, int64_t ldlu,

@@ -258,7 +258,7 @@ static bool qr_early_r_on() {
 
 template <typename T>
 static int qr_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* Q, int64_t ldq, T* R, int64_t ldr,
-                  int64_t* d_info, cudaStream_t st) {
+                  int64_t* d_info, cudaStream_t st, PanelHook* hook = nullptr) {
   const int64_t s = S.maxw();
   const int64_t wmax = qr_mgs_max_width(n, (int)sizeof(T));
   const int64_t wcap = s < wmax ? s : wmax;
@@ -318,6 +318,7 @@ static int qr_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* Q, int6
     ProfScope ps(1, 0.0, st);
     const int64_t w0 = S.w(0);
     SF_CUDA(qr_panel<T>(n, w0, A, lda, Q, ldq, 0, tol, mgsw, Cw, split, split_elems, fail, st));
+    if (hook) SF_CUDA(hook->done(0, w0, st));   // Q[:, 0:w0) is final
   }
   if (int rc = r_rows(0, S.w(0), st)) return rc;
   for (int64_t p = 0; p + 1 < S.P(); ++p) {
@@ -340,6 +341,7 @@ static int qr_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* Q, int6
       ProfScope ps(1, 0.0, pst);
       SF_CUDA(qr_panel<T>(n, w2, Q + c * ldq, ldq, Q + c * ldq, ldq, c, tol, mgsw, Cw2, split2, split_elems, fail,
                           pst));
+      if (hook) SF_CUDA(hook->done(c, w2, pst));
     }
     if (int rc = r_rows(c, w2, pst)) return rc;
     if (la) {
@@ -734,10 +736,41 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
         if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hook.ev, 0);
       }
     } else {
-      rc = qr_factor(n, s, dtype, d, n, d + bytes, n, d + 2 * bytes, n, dinfo, st);
-      if (!rc) e = cudaMemcpy2DAsync(hO1, ld1 * elt, d + bytes, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);
-      if (!rc && e == cudaSuccess)
-        e = cudaMemcpy2DAsync(hO2, ld2 * elt, d + 2 * bytes, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);
+      // QR: Q[:, z:z+w) is final once panel p's MGS is done (later flushes touch columns
+      // >= z+w only): return it on a copy stream while the factorization continues; R
+      // (one product at the end) follows.
+      static cudaStream_t qstreams[16] = {};
+      static cudaEvent_t qevents[16] = {};
+      if (!qstreams[devh & 15]) {
+        SF_CUDA(cudaStreamCreateWithFlags(&qstreams[devh & 15], cudaStreamNonBlocking));
+        SF_CUDA(cudaEventCreateWithFlags(&qevents[devh & 15], cudaEventDisableTiming));
+      }
+      struct QD2H : PanelHook {
+        int64_t n, ldh; size_t elt; const char* dev; char* host; cudaStream_t cs; cudaEvent_t ev;
+        cudaError_t done(int64_t z, int64_t w, cudaStream_t pst) override {
+          cudaError_t r = cudaEventRecord(ev, pst);
+          if (r == cudaSuccess) r = cudaStreamWaitEvent(cs, ev, 0);
+          if (r == cudaSuccess)
+            r = cudaMemcpy2DAsync(host + elt * (z * ldh), ldh * elt, dev + elt * (z * n), n * elt, n * elt, w,
+                                  cudaMemcpyDeviceToHost, cs);
+          return r;
+        }
+      } hook;
+      hook.n = n; hook.ldh = ld1; hook.elt = elt; hook.dev = d + bytes; hook.host = (char*)hO1;
+      hook.cs = qstreams[devh & 15]; hook.ev = qevents[devh & 15];
+      SF_CUDA(cudaEventRecord(hook.ev, st));
+      SF_CUDA(cudaStreamWaitEvent(hook.cs, hook.ev, 0));
+      const Sched S(n, s);
+      rc = dtype == SF_F64
+               ? qr_run<double>(n, S, (const double*)d, n, (double*)(d + bytes), n, (double*)(d + 2 * bytes), n, dinfo,
+                                st, &hook)
+               : qr_run<float>(n, S, (const float*)d, n, (float*)(d + bytes), n, (float*)(d + 2 * bytes), n, dinfo,
+                               st, &hook);
+      if (!rc) e = cudaMemcpy2DAsync(hO2, ld2 * elt, d + 2 * bytes, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);
+      if (!rc && e == cudaSuccess) {
+        e = cudaEventRecord(hook.ev, hook.cs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hook.ev, 0);
+      }
     }
     if (!rc && e == cudaSuccess) e = cudaMemcpyAsync(info, dinfo, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
   }

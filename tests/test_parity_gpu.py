@@ -532,3 +532,17 @@ def test_lu_host_overlapped_copies(n, s):
     if n <= 300:
         Lo, Uo, _ = oracle.lu(B, s)
         assert synth.r2_error(np.triu(out, 1) + np.eye(n), Uo) <= TOL64
+
+
+@pytest.mark.parametrize("n,s", [(300, 64), (2000, 128)])
+def test_qr_host_overlapped_copies(n, s):
+    """qr_factor_host returns each panel of Q while the factorization continues, then R:
+    bitwise the device entry point's result (both are column-major host/device buffers)."""
+    A = synth.gen_numpy("gaussian", n, seed=n + 1)
+    hA = np.asfortranarray(A.copy())
+    hQ = np.zeros((n, n), order="F")
+    hR = np.zeros((n, n), order="F")
+    hQ, hR, info = sf.qr_host(hA, s, hQ, hR)
+    Qg, Rg, ig = run_qr(A, s)
+    assert info == ig == 0
+    assert np.array_equal(hQ, Qg) and np.array_equal(hR, Rg)
