@@ -691,9 +691,11 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
       const Sched S(n, s);
       rc = dtype == SF_F64 ? chol_run<double>(n, S, (const double*)d, n, (double*)d, n, dinfo, st, &hook)
                            : chol_run_f32(n, S, (const float*)d, n, (float*)d, n, dinfo, st, &hook);
+      // join the copy stream even on failure: the device buffer is freed on st below
+      cudaError_t ej = cudaEventRecord(ev, cs);
+      if (ej == cudaSuccess) ej = cudaStreamWaitEvent(st, ev, 0);
       if (!rc) {
-        e = cudaEventRecord(ev, cs);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev, 0);
+        e = ej;
         if (e == cudaSuccess) e = cudaMemcpyAsync(info, dinfo, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
       }
     }
@@ -731,9 +733,10 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
       const Sched S(n, s);
       rc = dtype == SF_F64 ? lu_run<double>(n, S, (const double*)d, n, (double*)d, n, dinfo, st, &hook)
                            : lu_run<float>(n, S, (const float*)d, n, (float*)d, n, dinfo, st, &hook);
-      if (!rc) {
-        e = cudaEventRecord(hook.ev, hook.cs);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hook.ev, 0);
+      {   // join the copy stream even on failure: the device buffer is freed on st below
+        cudaError_t ej = cudaEventRecord(hook.ev, hook.cs);
+        if (ej == cudaSuccess) ej = cudaStreamWaitEvent(st, hook.ev, 0);
+        if (!rc) e = ej;
       }
     } else {
       // QR: Q[:, z:z+w) is final once panel p's MGS is done (later flushes touch columns
@@ -767,9 +770,10 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
                : qr_run<float>(n, S, (const float*)d, n, (float*)(d + bytes), n, (float*)(d + 2 * bytes), n, dinfo,
                                st, &hook);
       if (!rc) e = cudaMemcpy2DAsync(hO2, ld2 * elt, d + 2 * bytes, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);
-      if (!rc && e == cudaSuccess) {
-        e = cudaEventRecord(hook.ev, hook.cs);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hook.ev, 0);
+      {   // join the copy stream even on failure: the device buffer is freed on st below
+        cudaError_t ej = cudaEventRecord(hook.ev, hook.cs);
+        if (ej == cudaSuccess) ej = cudaStreamWaitEvent(st, hook.ev, 0);
+        if (!rc && e == cudaSuccess) e = ej;
       }
     }
     if (!rc && e == cudaSuccess) e = cudaMemcpyAsync(info, dinfo, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
