@@ -13,6 +13,7 @@
 // Panels wider than the leaf width are factored recursively: factor the left half,
 // subtract its contribution from the right half with one GEMM (the same terms the paper's
 // k-loops subtract, grouped), factor the right half.  DESIGN.md §5 discusses why.
+#include <type_traits>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -176,8 +177,19 @@ static int chol_run_f32(int64_t n, const Sched& S, const float* A, int64_t lda, 
   return SF_OK;
 }
 
+static bool lu_part1_grouped() {
+  static const int on = [] { const char* e = getenv("SF_LU_PART1_GROUPED"); return e ? atoi(e) : 1; }();
+  return on != 0;
+}
+
+template <typename T>
 static int64_t lu_la_min_m() {
-  static const int64_t v = [] { const char* e = getenv("SF_LU_LA_MIN_M"); return e ? (int64_t)atoll(e) : (int64_t)4096; }();
+  // fp64 default 0 (always: the first flush part is one grouped launch); fp32 keeps two
+  // launches for it, where lookahead loses below m = 4096 (cfg2 fp32 8.7 vs 10.7 ms)
+  static const int64_t v = [] {
+    const char* e = getenv("SF_LU_LA_MIN_M");
+    return e ? (int64_t)atoll(e) : (int64_t)(std::is_same<T, double>::value ? 0 : 4096);
+  }();
   return v;
 }
 
@@ -207,20 +219,41 @@ static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int
     const int64_t lds = (z == 0) ? lda : ldd;
     const T* RL = LU + c + z * ldd;   // R_L = L[c:n, z:c)
     const T* RU = LU + z + c * ldd;   // R_U = U[z:c, c:n)
-    // lookahead pays only while the trailing matrix is large: below SF_LU_LA_MIN_M (4096)
-    // the L-shaped first flush part (two launches) and the fork/join cost more than the
-    // overlap gains (n = 4096: 6.44 ms with, 6.26 without; n = 8192: 24.5 vs 25.8)
-    const bool lap = la && m > lu_la_min_m();
+    // SF_LU_LA_MIN_M: lookahead only while the trailing matrix is larger (default 0 =
+    // always).  With the L-shaped first flush part as two launches, lookahead lost at
+    // n = 4096 (6.44 vs 6.26 ms without); as ONE grouped launch it wins everywhere
+    // (n = 4096: 5.94 ms; n = 8192 s = 64: 23.44 vs 24.47; n = 16384: 122.3 vs 123.3)
+    const bool lap = la && m > lu_la_min_m<T>();
     cudaStream_t pst = lap ? sd->st : st;
     if (lap) {
       ProfScope ps(0, 2.0 * w * ((double)m * m - (double)(m - w2) * (m - w2)), st);
-      // flush, part 1: columns [c, c+w2) (all rows >= c) and rows [c, c+w2) right of them
-      SF_CUDA(gemm_sub<T>(m, w2, w, RL, ldd, 0, RU, ldd, 1, src + c + c * lds, lds, LU + c + c * ldd, ldd, kMaskNone,
-                          fail, st));
-      if (m > w2) {
-        const int64_t c2 = c + w2;
-        SF_CUDA(gemm_sub<T>(w2, m - w2, w, RL, ldd, 0, RU + w2 * ldd, ldd, 1, src + c + c2 * lds, lds,
-                            LU + c + c2 * ldd, ldd, kMaskNone, fail, st));
+      // flush, part 1: columns [c, c+w2) (all rows >= c) and rows [c, c+w2) right of them —
+      // fp64: the two blocks of the L-shaped region in ONE grouped launch
+      bool done1 = false;
+      if constexpr (std::is_same<T, double>::value) {
+        if (lu_part1_grouped()) {
+          GemmGroup g[2] = {};
+          int ng = 0;
+          g[ng].M = m; g[ng].N = w2; g[ng].off = 0; g[ng].A = RL; g[ng].B = RU;
+          g[ng].Cin = src + c + c * lds; g[ng].C = LU + c + c * ldd; ++ng;
+          if (m > w2) {
+            const int64_t c2 = c + w2;
+            g[ng].M = w2; g[ng].N = m - w2; g[ng].off = 0; g[ng].A = RL; g[ng].B = RU + w2 * ldd;
+            g[ng].Cin = src + c + c2 * lds; g[ng].C = LU + c + c2 * ldd; ++ng;
+          }
+          GemmF64 p64{0, 0, w, nullptr, ldd, nullptr, ldd, nullptr, lds, nullptr, ldd, -1.0, 1, 1, nullptr, fail};
+          SF_CUDA(gemm_f64_grouped(p64, g, ng, 0, 1, kMaskNone, st));
+          done1 = true;
+        }
+      }
+      if (!done1) {
+        SF_CUDA(gemm_sub<T>(m, w2, w, RL, ldd, 0, RU, ldd, 1, src + c + c * lds, lds, LU + c + c * ldd, ldd, kMaskNone,
+                            fail, st));
+        if (m > w2) {
+          const int64_t c2 = c + w2;
+          SF_CUDA(gemm_sub<T>(w2, m - w2, w, RL, ldd, 0, RU + w2 * ldd, ldd, 1, src + c + c2 * lds, lds,
+                              LU + c + c2 * ldd, ldd, kMaskNone, fail, st));
+        }
       }
       SF_CUDA(fork_join(*sd, st, pst));
     } else {
