@@ -206,6 +206,14 @@ int sf_set_strassen(int levels, int64_t min_dim);
 
 /* Number of flushes the c = z+s schedule performs: floor((n-1)/s). */
 int64_t sf_flush_count(int64_t n, int64_t s);
+/* The schedule the drivers run (row a1; PAPER.md:36-52, 87-104, 139-157 and, for a step
+ * sequence, PAPER.md:194 / reading R11): writes the 0-based columns c at which the flushes
+ * fire (c = z + s_p, then z := c; never at c = n) to flush_cols[0 .. min(count, cap)) and
+ * returns the count.  nsteps == 1: the fixed step steps[0] (the chol/lu/qr_factor schedule);
+ * nsteps > 1: the *_factor_steps schedule, the last step repeating.  Host only, no GPU.
+ * Returns -1 if n < 1, nsteps < 1, steps is NULL or a step is < 1; flush_cols may be NULL
+ * when cap == 0. */
+int64_t sf_schedule(int64_t n, int64_t nsteps, const int64_t* steps, int64_t* flush_cols, int64_t cap);
 /* Cumulative number of kernel launches this library has enqueued in this process
  * (launch accounting for benchmarks: read it before and after a timed region). */
 int64_t sf_launch_counter(void);

@@ -59,6 +59,9 @@ def _load():
         lib.orc_flush_count.argtypes = [i64, i64]
         lib.orc_frobenius.restype = dbl
         lib.orc_frobenius.argtypes = [i64, p, i64]
+        lib.orc_trace_flushes.restype = None
+        lib.orc_trace_flushes.argtypes = [p, i64]
+        lib.orc_trace_count.restype = i64
         lib.orc_set_threads.argtypes = [ctypes.c_int]
         lib.orc_max_threads.restype = ctypes.c_int
         _lib = lib
@@ -149,6 +152,22 @@ def qr(A, s, kcols=None, tol=0.0):
         info = _load().orc_qr_steps(n, len(st), st, K, A.ctypes.data, n, Q.ctypes.data, n, R.ctypes.data, n,
                                     float(tol), ctypes.byref(mass))
     return Q, R, int(info), float(mass.value)
+
+
+def flush_positions(kind, A, s, kcols=None):
+    """Run Algorithm 1/2/3 (kind 'chol' / 'lu' / 'qr') on A with step s (or a step sequence)
+    and return the 0-based columns c at which its flushes fired —
+    recorded inside the algorithm by the oracle's flush trace hook."""
+    lib = _load()
+    buf = np.zeros(4096, dtype=np.int64)
+    lib.orc_trace_flushes(buf.ctypes.data, len(buf))
+    try:
+        {"chol": chol, "lu": lu, "qr": qr}[kind](A, s, kcols=kcols)
+        cnt = int(lib.orc_trace_count())
+    finally:
+        lib.orc_trace_flushes(None, 0)
+    assert cnt <= len(buf), "trace buffer too small"
+    return [int(x) for x in buf[:cnt]]
 
 
 def frobenius(A):

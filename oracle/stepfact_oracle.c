@@ -93,6 +93,18 @@ static int64_t step_max(const Steps* st) {
   return m;
 }
 
+/* Flush trace (test hook, tests/test_oracle.py): while armed, every flush of Algorithms 1-3
+ * records the 0-based column c at which it fires (the `if c = z+s` of PAPER.md:41, 91, 143),
+ * so the schedule each algorithm actually runs can be pinned against hand-worked lists. */
+static int64_t* g_trace = NULL;
+static int64_t g_trace_cap = 0, g_trace_n = 0;
+void orc_trace_flushes(int64_t* buf, int64_t cap) { g_trace = buf; g_trace_cap = cap; g_trace_n = 0; }
+int64_t orc_trace_count(void) { return g_trace_n; }
+static void trace_flush(int64_t c) {
+  if (g_trace && g_trace_n < g_trace_cap) g_trace[g_trace_n] = c;
+  g_trace_n++;
+}
+
 /* Number of flushes the schedule of Algorithms 1-3 performs (R1). */
 int64_t orc_flush_count(int64_t n, int64_t s) {
   int64_t z = 0, flushes = 0;
@@ -123,6 +135,7 @@ static int64_t chol_core(int64_t n, Steps sp, int64_t kcols, const double* A, in
   int64_t z = 0;                                             /* z := 1            (:37) */
   for (int64_t c = 0; c < K; ++c) {                          /* for c from 1 to n (:39) */
     if (c == z + step_now(&sp)) {                            /* if c = z+s        (:41) */
+      trace_flush(c);
       /* R := L[c..n, z..c-1] (:42); S := R R^T (:43); A_ij := A_ij - S (:44-50).
          Columns j >= K of W are never read again in a restricted run. */
 #pragma omp parallel for schedule(dynamic, 16)
@@ -184,6 +197,7 @@ static int64_t lu_core(int64_t n, Steps sp, int64_t kcols, const double* A, int6
   int64_t z = 0;
   for (int64_t c = 0; c < K; ++c) {
     if (c == z + step_now(&sp)) {                            /* (:91) */
+      trace_flush(c);
       /* R_L := L[c..n, z..c-1], R_U := U[z..c-1, c..n], S := R_L R_U, A -= S (:92-103).
          A restricted run only ever reads W[i][j] with j < K (L columns) or i < K (U rows). */
 #pragma omp parallel for schedule(dynamic, 16)
@@ -252,6 +266,7 @@ static int64_t qr_core(int64_t n, Steps sp, int64_t kcols, const double* A, int6
   int64_t z = 0;
   for (int64_t c = 0; c < K; ++c) {
     if (c == z + step_now(&sp)) {                            /* (:143) */
+      trace_flush(c);
       const int64_t w = c - z;
       const int64_t jend = K;  /* a restricted run never reads M columns >= K */
       /* B_Q := Q[1..n, z..c-1], B_M := M[1..n, c..n] (:145-146); C := B_Q^T B_M (:147) */

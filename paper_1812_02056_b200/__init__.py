@@ -91,6 +91,8 @@ def lib():
     L.sf_local_cols.restype = i64
     L.sf_flush_count.argtypes = [i64, i64]
     L.sf_flush_count.restype = i64
+    L.sf_schedule.argtypes = [i64, i64, ctypes.POINTER(ctypes.c_int64), p, i64]
+    L.sf_schedule.restype = i64
     L.sf_launch_counter.argtypes = []
     L.sf_launch_counter.restype = i64
     L.sf_set_strassen.argtypes = [i32, i64]
@@ -114,7 +116,7 @@ EXPORTS = ("chol_factor", "lu_factor", "qr_factor", "chol_factor_host", "lu_fact
            "sf_profile_collect", "sf_get_unique_id", "sf_comm_init", "sf_comm_init_loopback", "sf_comm_destroy",
            "sf_comm_size", "sf_comm_local_ranks", "sf_local_cols", "chol_factor_dist", "lu_factor_dist",
            "qr_factor_dist", "chol_factor_steps", "lu_factor_steps", "qr_factor_steps", "chol_solve", "lu_solve",
-           "qr_solve", "sf_set_strassen")
+           "qr_solve", "sf_set_strassen", "sf_schedule")
 
 
 def _check(rc):
@@ -145,6 +147,19 @@ def _need_cuda(*ts):
 
 def flush_count(n, s):
     return int(lib().sf_flush_count(n, s))
+
+
+def schedule(n, s):
+    """0-based columns at which the library's drivers flush (sf_schedule): s an int (fixed
+    step) or a step sequence."""
+    seq = [int(s)] if not isinstance(s, (list, tuple)) else [int(x) for x in s]
+    arr = (ctypes.c_int64 * len(seq))(*seq)
+    cnt = lib().sf_schedule(n, len(seq), arr, None, 0)
+    if cnt < 0:
+        raise StepfactError(1, "bad schedule arguments")
+    out = (ctypes.c_int64 * max(cnt, 1))()
+    lib().sf_schedule(n, len(seq), arr, ctypes.addressof(out), cnt)
+    return [int(out[i]) for i in range(cnt)]
 
 
 def launch_counter():

@@ -940,6 +940,16 @@ int64_t sf_flush_count(int64_t n, int64_t s) {
   return f;
 }
 
+int64_t sf_schedule(int64_t n, int64_t nsteps, const int64_t* steps, int64_t* flush_cols, int64_t cap) {
+  if (n < 1 || nsteps < 1 || !steps) return -1;
+  for (int64_t i = 0; i < nsteps; ++i)
+    if (steps[i] < 1) return -1;
+  const Sched S = nsteps == 1 ? Sched(n, steps[0]) : Sched(n, steps, nsteps);
+  const int64_t count = S.P() - 1;   // a flush follows every panel but the last
+  for (int64_t p = 0; p < count && p < cap; ++p) flush_cols[p] = S.z(p + 1);
+  return count;
+}
+
 int64_t sf_launch_counter(void) { return g_launches.load(); }
 
 int sf_set_strassen(int levels, int64_t min_dim) {

@@ -268,6 +268,255 @@ __device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vec
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// v2 tile (DESIGN.md §5 K1): BM x 64 CTA tile, 4 warps as 2 x 2 (warp tile BM/2 x 32),
+// MINB CTAs per SM.  Differences from gemm_f64_body:
+//  * paired fragment loads: for an idx-contiguous operand the two atoms 2b, 2b+1 of a warp
+//    tile interleave their rows (atom 2b row r = logical row 16b + 2r, atom 2b+1 = 16b+2r+1),
+//    so ONE 16-byte shared load feeds both DMMA operands — half the LDS instructions per DMMA;
+//  * BM = 96 with 3 CTAs per SM (12 warps, 3 per SM sub-partition): while one CTA is in its
+//    prologue / epilogue the other two still keep two warps per sub-partition issuing DMMA;
+//  * in-place epilogue by bulk reduction: the tile (alpha * acc, -0.0 where masked) is
+//    parked in shared memory and added to C in L2 by `cp.reduce.async.bulk .add.f64`, one
+//    column per lane — no C load on the CTA's critical path.  fl(C + alpha*acc) is the same
+//    IEEE operation as the load/add/store epilogue; x + (-0.0) == x for every x, so masked
+//    entries are unchanged bit for bit.
+namespace g64v2 {
+using g64::BK;
+using g64::PAD_KI;
+template <int NIDX, bool KC> constexpr int slice_elems() { return KC ? NIDX * PAD_KI : BK * (NIDX + 4); }
+template <int BM, bool AK, bool BKC> constexpr int stage_elems() { return slice_elems<BM, AK>() + slice_elems<64, BKC>(); }
+template <int BM, bool AK, bool BKC> constexpr size_t smem_bytes() {
+  const size_t pipe = sizeof(double) * (size_t)stage_elems<BM, AK, BKC>() * g64::STAGES;
+  const size_t epi = sizeof(double) * (size_t)64 * (BM + 2);
+  return pipe > epi ? pipe : epi;
+}
+}  // namespace g64v2
+
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_reduce_add_f64(double* gdst, const double* ssrc, int bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n" ::"l"(gdst), "r"(s),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+
+template <int BM, bool PAIR, bool AK, bool BKC, bool V16, int MASK>
+__device__ __forceinline__ void gemm_f64_body2(const GemmF64& p, int bid, int vecC, int bulk) {
+  using namespace g64;
+  constexpr int NT = 128, WTM = BM / 2, ATM = WTM / 8;
+  static_assert(ATM % 2 == 0, "paired atoms");
+  constexpr bool PA_ = PAIR && !AK, PB_ = PAIR && !BKC;   // paired fragment loads per operand
+  constexpr int SA = g64v2::slice_elems<BM, AK>(), SB = g64v2::slice_elems<64, BKC>();
+  constexpr int PA = BM + 4, PB = 64 + 4;   // idx-contiguous row strides (== 4 mod 16 doubles)
+  constexpr int CP = BM + 2;
+  using TT = Tiles<BM, 64>;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * SA;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int TM = (int)((p.M + BM - 1) / BM), TN = (int)((p.N + 63) / 64);
+  int ti, tj;
+  if (p.rs.ngroups > 0) TT::tile_of_raster(MASK, bid, TM, p.off, p.rs, ti, tj);
+  else TT::tile_of(MASK, bid, TM, TN, p.off, ti, tj);
+  const int64_t i0 = (int64_t)ti * BM, j0 = (int64_t)tj * 64;
+
+  const int sp = blockIdx.y;
+  int64_t kchunk = (p.K + p.splits - 1) / p.splits;
+  kchunk = (kchunk + BK - 1) / BK * BK;
+  const int64_t kbeg = (int64_t)sp * kchunk;
+  const int64_t kend = (kbeg + kchunk < p.K) ? kbeg + kchunk : p.K;
+  const int nk = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+
+  if (p.beta && p.splits == 1) {
+#pragma unroll
+    for (int r = 0; r < 64 * 8 / NT; ++r) {
+      const int id = tid + r * NT;
+      const int64_t jj = j0 + (id >> 3), ii = i0 + (id & 7) * 16;
+      if (jj < p.N && ii < p.M) prefetch_l2(p.Cin + ii + jj * p.ldcin);
+    }
+  }
+
+  double acc[ATM][4][2];
+#pragma unroll
+  for (int a = 0; a < ATM; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  auto issue = [&](int kb) {
+    if (kb < nk) {
+      const int slot = kb % STAGES;
+      const int64_t k0 = kbeg + (int64_t)kb * BK;
+      load_slice<BM, AK, V16, NT>(As + slot * SA, p.A, p.lda, i0, p.M, k0, kend, tid);
+      load_slice<64, BKC, V16, NT>(Bs + slot * SB, p.B, p.ldb, j0, p.N, k0, kend, tid);
+    }
+    cp_async_commit();
+  };
+  // fragments of step kk: A atoms (i), B atoms (j)
+  auto load_frags = [&](const double* as, const double* bs, int kk, double (&fa)[ATM], double (&fb)[4]) {
+    if (PA_) {
+#pragma unroll
+      for (int b2 = 0; b2 < ATM / 2; ++b2) {
+        const double2 v = *reinterpret_cast<const double2*>(as + (kk * 4 + (lane & 3)) * PA + wm * WTM + 16 * b2 +
+                                                            2 * (lane >> 2));
+        fa[2 * b2] = v.x; fa[2 * b2 + 1] = v.y;
+      }
+    } else if (AK) {
+#pragma unroll
+      for (int a = 0; a < ATM; ++a) fa[a] = as[(wm * WTM + a * 8 + (lane >> 2)) * PAD_KI + kk * 4 + (lane & 3)];
+    } else {
+#pragma unroll
+      for (int a = 0; a < ATM; ++a) fa[a] = as[(kk * 4 + (lane & 3)) * PA + wm * WTM + a * 8 + (lane >> 2)];
+    }
+    if (PB_) {
+#pragma unroll
+      for (int b2 = 0; b2 < 2; ++b2) {
+        const double2 v = *reinterpret_cast<const double2*>(bs + (kk * 4 + (lane & 3)) * PB + wn * 32 + 16 * b2 +
+                                                            2 * (lane >> 2));
+        fb[2 * b2] = v.x; fb[2 * b2 + 1] = v.y;
+      }
+    } else if (BKC) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) fb[b] = bs[(wn * 32 + b * 8 + (lane >> 2)) * PAD_KI + kk * 4 + (lane & 3)];
+    } else {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) fb[b] = bs[(kk * 4 + (lane & 3)) * PB + wn * 32 + b * 8 + (lane >> 2)];
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) issue(s);
+
+  for (int kb = 0; kb < nk; ++kb) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    issue(kb + STAGES - 1);
+    const double* as = As + (kb % STAGES) * SA;
+    const double* bs = Bs + (kb % STAGES) * SB;
+    double fa[2][ATM], fb[2][4];
+    load_frags(as, bs, 0, fa[0], fb[0]);
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      const int cur = kk & 1, nxt = cur ^ 1;
+      if (kk + 1 < BK / 4) load_frags(as, bs, kk + 1, fa[nxt], fb[nxt]);
+#pragma unroll
+      for (int a = 0; a < ATM; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], fb[cur][b], fa[cur][a]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // ---- park the tile in shared memory, Cs[j*CP + i] (logical tile coordinates)
+  double* Cs = smem;
+  const int64_t rows = (p.M - i0 < BM) ? p.M - i0 : BM;
+  const bool use_bulk = bulk && p.splits == 1 && (rows & 1) == 0;
+  const double alpha = p.alpha;
+  // logical i of atom a, MMA column c (0..7); logical j of atom b, MMA row r
+  auto li = [&](int a, int c) { return !PA_ ? wm * WTM + 8 * a + c : wm * WTM + 16 * (a >> 1) + 2 * c + (a & 1); };
+  auto lj = [&](int b, int r) { return !PB_ ? wn * 32 + 8 * b + r : wn * 32 + 16 * (b >> 1) + 2 * r + (b & 1); };
+#pragma unroll
+  for (int a = 0; a < ATM; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int jl = lj(b, lane >> 2);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int il = li(a, 2 * (lane & 3) + e);
+        double v = acc[a][b][e];
+        if (use_bulk) {
+          const int64_t i = i0 + il, jd = j0 + jl + p.off;
+          const bool in = MASK == kMaskNone || (MASK == kMaskLower ? i >= jd : i <= jd);
+          v = in ? alpha * v : -0.0;
+        }
+        Cs[jl * CP + il] = v;
+      }
+    }
+  if (use_bulk) {
+    fence_proxy_async_smem();
+    __syncthreads();
+    // one 16-byte-multiple column segment per lane: rows [i0, i0+rows) of column j
+    if (tid < 64) {
+      const int64_t j = j0 + tid;
+      if (j < p.N) bulk_reduce_add_f64(p.C + i0 + j * p.ldc, Cs + tid * CP, (int)(rows * 8));
+      bulk_commit();
+      bulk_wait_read0();
+    }
+    return;
+  }
+  __syncthreads();
+
+  constexpr int COLS = 64 / 4;
+  if (p.splits > 1) {
+    double* W = p.work + (int64_t)sp * p.M * p.N;
+    for (int q = 0; q < COLS; ++q) {
+      const int jl = warp * COLS + q;
+      const int64_t j = j0 + jl;
+      if (j >= p.N) break;
+      for (int il = lane; il < BM; il += 32)
+        if (i0 + il < p.M) W[j * p.M + i0 + il] = Cs[jl * CP + il];
+    }
+    return;
+  }
+  // load/add/store epilogue: lane owns rows 2*lane+{0,1} (+64 for BM = 128) of each column
+  constexpr int H = (BM + 63) / 64;
+  double cin[COLS][H][2];
+  if (p.beta) {
+#pragma unroll
+    for (int q = 0; q < COLS; ++q) {
+      const int64_t j = j0 + warp * COLS + q;
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const int il = 64 * h + 2 * lane;
+        const int64_t i = i0 + il;
+        const double* src = p.Cin + i + j * p.ldcin;
+        if (il < BM && vecC && j < p.N && i + 1 < p.M) {
+          const double2 v = __ldcg(reinterpret_cast<const double2*>(src));
+          cin[q][h][0] = v.x; cin[q][h][1] = v.y;
+        } else {
+          cin[q][h][0] = (il < BM && j < p.N && i < p.M) ? __ldcg(src) : 0.0;
+          cin[q][h][1] = (il < BM && j < p.N && i + 1 < p.M) ? __ldcg(src + 1) : 0.0;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < COLS; ++q) {
+    const int jl = warp * COLS + q;
+    const int64_t j = j0 + jl;
+    if (j >= p.N) break;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int il = 64 * h + 2 * lane;
+      if (il >= BM) continue;
+      const int64_t i = i0 + il;
+      const double2 d = *reinterpret_cast<const double2*>(Cs + jl * CP + il);
+      double v0 = alpha * d.x, v1 = alpha * d.y;
+      if (p.beta) { v0 += cin[q][h][0]; v1 += cin[q][h][1]; }
+      double* dst = p.C + i + j * p.ldc;
+      const int64_t jd = j + p.off;
+      const bool pair_in = (i + 1 < p.M) && (MASK == kMaskNone || (MASK == kMaskLower ? i >= jd : i + 1 <= jd));
+      if (pair_in && vecC) {
+        __stcg(reinterpret_cast<double2*>(dst), make_double2(v0, v1));
+      } else {
+        if (i < p.M && (MASK == kMaskNone || (MASK == kMaskLower ? i >= jd : i <= jd))) dst[0] = v0;
+        if (i + 1 < p.M && (MASK == kMaskNone || (MASK == kMaskLower ? i + 1 >= jd : i + 1 <= jd))) dst[1] = v1;
+      }
+    }
+  }
+}
+
+template <int BM, int MINB, bool PAIR, bool AK, bool BKC, bool V16, int MASK>
+__global__ void __launch_bounds__(128, MINB) gemm_f64v2_kernel(GemmF64 p, int vecC, int bulk) {
+  if (p.fail && failed(p.fail)) return;
+  gemm_f64_body2<BM, PAIR, AK, BKC, V16, MASK>(p, blockIdx.x, vecC, bulk);
+}
+
 template <bool AK, bool BKC, bool V16, int MASK, int NT = g64::THREADS>
 __global__ void __launch_bounds__(NT, 2) gemm_f64_kernel(GemmF64 p, int vecC) {
   if (p.fail && failed(p.fail)) return;
@@ -380,6 +629,74 @@ static cudaError_t launch_key(const GemmF64& p, const GemmGroups* gs, int a_kcon
   }
 }
 
+// Tile variant per K (DESIGN.md §5 K1, measured: profiles/r02_dmma_variants.txt):
+//   K <= 64        gemm_f64_kernel, 8 warps (the 128x64 short-K tile)
+//   64 < K <= 128  v2, 64x64 tiles, 4 CTAs/SM, plain fragment loads
+//   K > 128        v2, 64x64 tiles, 4 CTAs/SM, paired fragment loads
+// SF_DMMA / SF_DMMA_SHORTK override (0 = gemm_f64_kernel, 1 = v2 128x64 paired 2/SM, 2 = 96x64
+// paired 3/SM, 3 = 96x64 3/SM, 4 = 128x64 2/SM, 5 = 64x64 4/SM, 6 = 64x64 paired 4/SM) for
+// the long- (K > 256) and short-K (K <= 256) products; SF_DMMA_BULK=0 disables the
+// bulk-reduce epilogue.
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+static int dmma_variant_for(int64_t K) {
+  static const int lk = env_int("SF_DMMA", -1), sk = env_int("SF_DMMA_SHORTK", -1);
+  if (K > 256) return lk >= 0 ? lk : 6;
+  if (sk >= 0) return sk;
+  return K <= 64 ? 0 : (K <= 128 ? 5 : 6);
+}
+static bool dmma_bulk() {
+  static const int v = env_int("SF_DMMA_BULK", 1);
+  return v != 0;
+}
+
+template <int BM, int MINB, bool PAIR, bool AK, bool BKC, bool V16, int MASK>
+static cudaError_t launch_v2_t(const GemmF64& p, int ntiles, int vecC, int bulk, cudaStream_t st) {
+  constexpr size_t SM = g64v2::smem_bytes<BM, AK, BKC>();
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_f64v2_kernel<BM, MINB, PAIR, AK, BKC, V16, MASK>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid(ntiles, p.splits);
+  gemm_f64v2_kernel<BM, MINB, PAIR, AK, BKC, V16, MASK><<<grid, 128, SM, st>>>(p, vecC, bulk);
+  count_launch();
+  return cudaGetLastError();
+}
+template <int BM, int MINB, bool PAIR, bool AK, bool BKC, bool V16>
+static cudaError_t launch_v2_mask(const GemmF64& p, int mask, int ntiles, int vecC, int bulk, cudaStream_t st) {
+  switch (mask) {
+    case kMaskLower: return launch_v2_t<BM, MINB, PAIR, AK, BKC, V16, kMaskLower>(p, ntiles, vecC, bulk, st);
+    case kMaskUpper: return launch_v2_t<BM, MINB, PAIR, AK, BKC, V16, kMaskUpper>(p, ntiles, vecC, bulk, st);
+    default: return launch_v2_t<BM, MINB, PAIR, AK, BKC, V16, kMaskNone>(p, ntiles, vecC, bulk, st);
+  }
+}
+template <int BM, int MINB, bool PAIR>
+static cudaError_t launch_v2(GemmF64 p, int a_kcontig, int b_kcontig, bool v16, int mask, int vecC, int bulk,
+                             cudaStream_t st) {
+  using TT = Tiles<BM, 64>;
+  const int TM = (int)((p.M + BM - 1) / BM), TN = (int)((p.N + 63) / 64);
+  const int ntiles = (int)TT::count(mask, TM, TN, p.off);
+  if (ntiles == 0) return cudaSuccess;
+  TT::make_raster(mask, TM, TN, p.off, kGroupCols, p.rs);
+  p.ntiles = ntiles;
+  const int key = (a_kcontig ? 1 : 0) | (b_kcontig ? 2 : 0) | (v16 ? 4 : 0);
+  switch (key) {
+    case 0: return launch_v2_mask<BM, MINB, PAIR, false, false, false>(p, mask, ntiles, vecC, bulk, st);
+    case 1: return launch_v2_mask<BM, MINB, PAIR, true, false, false>(p, mask, ntiles, vecC, bulk, st);
+    case 2: return launch_v2_mask<BM, MINB, PAIR, false, true, false>(p, mask, ntiles, vecC, bulk, st);
+    case 3: return launch_v2_mask<BM, MINB, PAIR, true, true, false>(p, mask, ntiles, vecC, bulk, st);
+    case 4: return launch_v2_mask<BM, MINB, PAIR, false, false, true>(p, mask, ntiles, vecC, bulk, st);
+    case 5: return launch_v2_mask<BM, MINB, PAIR, true, false, true>(p, mask, ntiles, vecC, bulk, st);
+    case 6: return launch_v2_mask<BM, MINB, PAIR, false, true, true>(p, mask, ntiles, vecC, bulk, st);
+    default: return launch_v2_mask<BM, MINB, PAIR, true, true, true>(p, mask, ntiles, vecC, bulk, st);
+  }
+}
+
 cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStream_t st) {
   if (p.M <= 0 || p.N <= 0) return cudaSuccess;
   if (p.K <= 0) {
@@ -388,6 +705,22 @@ cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStre
     p.K = 0;
   }
   if (p.splits < 1) p.splits = 1;
+  {
+    const int var = dmma_variant_for(p.K);
+    if (var > 0 && p.max_ctas == 0 && p.splits == 1 && p.K > 0) {
+      const bool v16 = aligned16(p.A, p.lda) && aligned16(p.B, p.ldb);
+      const int vecC = aligned16(p.C, p.ldc) && (!p.beta || aligned16(p.Cin, p.ldcin));
+      const int bulk = dmma_bulk() && p.beta && vecC && p.Cin == p.C && p.ldcin == p.ldc;
+      switch (var) {
+        case 1: return launch_v2<128, 2, true>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st);
+        case 2: return launch_v2<96, 3, true>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st);
+        case 3: return launch_v2<96, 3, false>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st);
+        case 5: return launch_v2<64, 4, false>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st);
+        case 6: return launch_v2<64, 4, true>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st);
+        default: return launch_v2<128, 2, false>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st);
+      }
+    }
+  }
   const int TM = (int)((p.M + g64::BM - 1) / g64::BM), TN = (int)((p.N + g64::BN - 1) / g64::BN);
   const int ntiles = masked_tiles(mask, TM, TN, p.off);
   if (ntiles == 0) return cudaSuccess;

@@ -34,8 +34,18 @@ def test_header_symbols_exported(L):
 
 
 def test_no_torch_in_abi():
+    """No torch / ATen / c10 type crosses the boundary: the header includes only <stdint.h>
+    and every parameter type is a C scalar, a plain pointer or an opaque sf_* handle."""
     txt = open(os.path.join(ROOT, "include", "stepfact.h")).read()
-    assert "torch" not in txt.lower().replace("pytorch", "") or "at::" not in txt
+    code = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    assert re.findall(r"#include\s*[<\"]([^>\"]+)", code) == ["stdint.h"]
+    for bad in ("torch", "at::", "c10", "Tensor", "std::"):
+        assert bad not in code, bad
+    allowed = {"int", "int64_t", "uint8_t", "double", "void", "const", "char", "sf_comm_t", "float"}
+    for m in re.finditer(r"^\s*(?:const\s+)?\w+\**\s+\**\w+\s*\(([^)]*)\)\s*;", code, flags=re.M | re.S):
+        for arg in filter(None, (a.strip() for a in m.group(1).split(","))):
+            words = re.findall(r"[A-Za-z_]\w*", arg)
+            assert words and set(words[:-1] if len(words) > 1 else words) <= allowed, arg
 
 
 def test_strerror(L):
@@ -77,6 +87,32 @@ def test_flush_count_matches_paper_schedule(L):
     # BASELINE.json configs
     assert L.sf_flush_count(256, 16) == 15 and L.sf_flush_count(4096, 64) == 63
     assert L.sf_flush_count(16384, 168) == 97 and L.sf_flush_count(65536, 512) == 127
+
+
+def test_schedule_matches_oracle_and_hand_lists(L):
+    """The drivers' schedule (sf_schedule: the Sched the GPU drivers run, row a1) equals the
+    flush positions recorded inside the oracle's Algorithms 1-3 and hand-worked lists
+    (readings R1, R11)."""
+    import numpy as np
+    import oracle
+    import synth
+    assert sf.schedule(37, [9, 3, 1, 12, 5, 7]) == [9, 12, 13, 25, 30]
+    assert sf.schedule(37, [2, 3])[:4] == [2, 5, 8, 11]
+    assert sf.schedule(4, 1) == [1, 2, 3] and sf.schedule(4, 4) == [] and sf.schedule(1, 1) == []
+    assert sf.schedule(16384, 168)[-1] == 97 * 168 and len(sf.schedule(16384, 168)) == 97
+    rng = np.random.default_rng(0)
+    A = synth.gen_numpy("paper_spd", 61, seed=1)
+    for _ in range(40):
+        seq = [int(x) for x in rng.integers(1, 20, size=rng.integers(1, 6))]
+        s = seq if len(seq) > 1 else seq[0]
+        if isinstance(s, int) and s > 61:
+            continue
+        assert sf.schedule(61, s) == oracle.flush_positions("chol", A, s), seq
+    for n in range(1, 40):
+        for s in range(1, n + 1):
+            assert len(sf.schedule(n, s)) == L.sf_flush_count(n, s)
+    bad = (ctypes.c_int64 * 2)(3, 0)
+    assert L.sf_schedule(10, 2, bad, None, 0) == -1 and L.sf_schedule(0, 1, bad, None, 0) == -1
 
 
 def test_sass_is_sm100a_tensor_core():

@@ -161,7 +161,7 @@ def test_nccl_comm_single_rank():
 def test_chol_dist_cfg5_shape_sampled():
     """cfg5's layout (s=512, G=8 ranks) at n=8192 on one GPU: the distributed factor equals
     the single-GPU factor bit for bit and its first columns match the oracle."""
-    n, s, G, K = 8192, 512, 8, 512
+    n, s, G, K = 8192, 512, 8, 1536   # K = 3s: flushed columns of ranks 1 and 2 compared
     A = synth.gen_torch("spd_scaled", n, seed=0)
     An = A.cpu().numpy()
     (Lg,), info = run_dist("chol", An, s, G)

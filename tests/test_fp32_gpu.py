@@ -98,7 +98,7 @@ def test_chol32_cfg5_shape_sampled():
     """cfg5's fp32 setting (s = 512, A = G G^T/n + I rounded to fp32) at n = 16384: the first
     K columns against the restricted fp64 oracle, plus a Freivalds residual of the whole
     factor (torch fp64, an independent checker)."""
-    n, s, K = 16384, 512, 512
+    n, s, K = 16384, 512, 1536      # K = 3s: entries of both lookahead flush parts compared
     A64 = synth.gen_torch("spd_scaled", n, seed=0)
     A32 = A64.float()
     info = torch.zeros(1, dtype=torch.int64, device="cuda")

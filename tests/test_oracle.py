@@ -67,8 +67,16 @@ def test_golden_qr_all_s(ex):
 @pytest.mark.parametrize("ex", GOLD["errors"], ids=lambda e: e["kind"])
 def test_golden_error_paths(ex):
     A = np.array(ex["A"], float); n = len(A)
+    if ex["kind"] == "chol":       # the stated failure is a property of A, not of the oracle
+        assert np.linalg.eigvalsh(A).min() <= 1e-12
+    elif ex["kind"] == "qr":
+        assert np.linalg.matrix_rank(A[:, :ex["info"]]) < ex["info"]
+    else:
+        k = ex["info"]
+        assert abs(np.linalg.det(A[:k, :k])) <= 1e-12 and abs(np.linalg.det(A[:k - 1, :k - 1])) > 0.5
     for s in range(1, n + 1):
-        info = oracle.chol(A, s)[1] if ex["kind"] == "chol" else oracle.lu(A, s)[2]
+        info = {"chol": lambda: oracle.chol(A, s)[1], "lu": lambda: oracle.lu(A, s)[2],
+                "qr": lambda: oracle.qr(A, s)[2]}[ex["kind"]]()
         assert info == ex["info"], (s, info)
 
 
@@ -217,6 +225,44 @@ def test_restricted_columns_bitwise(K):
     C = synth.gen_numpy("gaussian", n, seed=5)
     Q, R, _, _ = oracle.qr(C, s); Qk, Rk, _, _ = oracle.qr(C, s, kcols=K)
     assert np.array_equal(Qk[:, :K], Q[:, :K]) and np.array_equal(Rk[:K, :], R[:K, :])
+
+
+def test_flush_positions_hand_worked():
+    """The schedule each algorithm runs (reading R1; flush iff c = z+s,
+    then z := c; R11 for a sequence), recorded inside the oracle's loops, against
+    positions worked out by hand.  [9,3,1,12,5,7] at n = 37: z = 0 -> c = 9 -> 12 -> 13 -> 25 ->
+    30, and 30 + 7 = 37 = n never fires."""
+    n = 37
+    mats = {"chol": synth.gen_numpy("paper_spd", n, seed=4), "lu": synth.gen_numpy("diag_dominant", n, seed=4),
+            "qr": synth.gen_numpy("gaussian", n, seed=4)}
+    cases = [([9, 3, 1, 12, 5, 7], None, [9, 12, 13, 25, 30]),
+             ([9, 3, 1, 12, 5, 7], 20, [9, 12, 13]),          # restricted run: flushes at c < K only
+             ([2, 3], None, [2, 5, 8, 11, 14, 17, 20, 23, 26, 29, 32, 35]),   # the last step repeats
+             ([36], None, [36]), ([37], None, []), ([40], None, []),
+             (5, None, [5, 10, 15, 20, 25, 30, 35]), (37, None, []), (1, 6, [1, 2, 3, 4, 5]),
+             (12, None, [12, 24, 36])]
+    for kind, A in mats.items():
+        for s, K, want in cases:
+            assert oracle.flush_positions(kind, A, s, kcols=K) == want, (kind, s, K)
+
+
+def test_frobenius_and_threshold_pins():
+    """orc_frobenius (the R3 threshold's norm) against closed forms and LAPACK; the R3
+    thresholds tol = 1e-12 ||A||_F / n pinned from both sides (a wrong power of n, a missing
+    factor or the wrong norm moves the boundary past one of the two probes)."""
+    for n in (1, 3, 8, 31):
+        assert oracle.frobenius(np.ones((n, n))) == float(n)            # sqrt(n^2)
+        Hd = np.array(scipy.linalg.hadamard(8), float)
+        assert oracle.frobenius(Hd) == 8.0
+        A = synth.gen_numpy("gaussian", n, seed=n)
+        assert abs(oracle.frobenius(A) - np.linalg.norm(A)) <= 4 * EPS * np.linalg.norm(A)
+    # diag(1, 1, 1, d): ||A||_F = sqrt(3) to within 1e-25, tol = 1e-12 * sqrt(3) / 4 = 4.330e-13
+    tol = 1e-12 * np.sqrt(3.0) / 4
+    for d, fails in ((0.99 * tol, True), (1.01 * tol, False)):
+        A = np.diag([1.0, 1.0, 1.0, d])
+        for s in (1, 2, 4):
+            assert oracle.lu(A, s)[2] == (4 if fails else 0), (d, s)
+            assert oracle.qr(A, s)[2] == (4 if fails else 0), (d, s)
 
 
 def test_thread_count_does_not_change_bits():

@@ -69,6 +69,13 @@ def run_qr(A, s):
     return host(Q), host(R), int(info.item())
 
 
+def flushed_cols(K, s):
+    """How many of the first K columns are produced AFTER at least one flush (c >= s) and
+    how many after the lookahead's part-2 update (columns beyond the panel that follows a
+    flush: c >= 2s) — what a restricted-oracle comparison of K columns exercises."""
+    return max(0, K - s), max(0, K - 2 * s)
+
+
 def svals(n):
     return sorted({1, 2, 3, 7, 16, 32, 64, 100, 128, 130, 200, n // 2, n} & set(range(1, n + 1)))
 
@@ -133,10 +140,15 @@ def test_chol_deterministic():
 
 @pytest.mark.parametrize("s", [64, 168, 512, 1024])
 def test_chol_cfg3_sampled(s):
-    """BASELINE.json configs[2] at full size n=16384: the first K columns of L against the
-    restricted oracle (bitwise the full oracle's first K columns), plus a Freivalds residual
-    of the whole factor computed with torch (an independent checker)."""
-    n, K = 16384, 384
+    """BASELINE.json configs[2] at full size n=16384: the first K = max(384, 3s) columns of L
+    against the restricted oracle (bitwise the full oracle's first K columns) — so entries
+    updated by flush part 1 (the next panel's columns) AND part 2 (the rest, concurrent with
+    the lookahead panel) are compared elementwise — plus a Freivalds residual of the whole
+    factor computed with torch (an independent checker)."""
+    n = 16384
+    K = max(384, 3 * s)
+    f1, f2 = flushed_cols(K, s)
+    assert f1 >= 2 * s and f2 >= s
     A = synth.gen_torch("spd_scaled", n, seed=0)
     B = A.clone()                                   # symmetric: column-major buffer == A
     info = torch.zeros(1, dtype=torch.int64, device="cuda")
@@ -192,6 +204,22 @@ def test_lu_zero_pivot_info():
         assert run_lu(A, s)[2] == 1
 
 
+@pytest.mark.parametrize("n,s,bad", [(300, 64, 200), (1000, 128, 777), (2048, 64, 1500)])
+def test_lu_interior_failure_info(n, s, bad):
+    """R3 at an interior column beyond the first panel: planted integer
+    factors with L_bad,bad = 0 exactly, so |L_cc| < tol at column bad+1 on both sides."""
+    Lx, Ux = synth.planted_lu(n, seed=n + bad)
+    Lx[bad, bad] = 0.0
+    A = Lx @ Ux
+    io = oracle.lu(A, s)[2]
+    assert io == bad + 1
+    for inplace in (True, False):
+        assert run_lu(A, s, inplace)[2] == io
+    # columns before the failure are still the exact factor (columns >= info are unspecified)
+    Lg, Ug, _ = run_lu(A, s)
+    assert np.array_equal(Lg[:, :bad], Lx[:, :bad]) and np.array_equal(Ug[:bad, :bad], Ux[:bad, :bad])
+
+
 # ============================================================ QR
 
 def check_qr(A, s, Qg, Rg, Qo, Ro):
@@ -217,6 +245,43 @@ def test_qr_small_grid(n):
         Qg, Rg, ig = run_qr(A, s)
         assert io == ig == 0
         check_qr(A, s, Qg, Rg, Qo, Ro)
+
+
+@pytest.mark.timeout(600, method="thread")
+@pytest.mark.parametrize("n,s,bad", [(300, 64, 150), (3, 1, 1), (2000, 96, 1500), (8192, 128, 4000),
+                                     (16384, 128, 9000)])
+def test_qr_rank_deficient_info(n, s, bad):
+    """R3 for QR (PAPER.md:158-164 needs full rank): column `bad` repeats column 0, so after
+    projection ||v|| is round-off (~u ||a_0||), far below 1e-12 ||A||_F / n, on both sides;
+    info = bad + 1.  At n = 8192 / 16384 the column is zero (||v|| = 0 exactly: at that size
+    ||a_0|| ~ sqrt(n) puts round-off within a decade of the threshold); these run the
+    persistent multi-cluster MGS grid, whose CTAs must all leave together once the failure
+    is flagged (no hang: the test has a timeout)."""
+    A = synth.gen_numpy("gaussian", n, seed=n + bad)
+    A[:, bad] = A[:, 0] if n <= 2000 else 0.0
+    if n <= 2000:
+        io = oracle.qr(A, s)[2]
+        assert io == bad + 1
+    Qg, Rg, ig = run_qr(A, s)
+    assert ig == bad + 1
+    if n <= 2000:   # columns before the failure still match the oracle's
+        Qo = oracle.qr(A, s, kcols=bad)[0]
+        assert synth.r2_error(Qg[:, :bad], Qo[:, :bad]) <= TOL64
+
+
+def test_qr_wide_panels_chunked():
+    """Reading R12: a panel wider than one MGS launch holds (w_max = 216 columns
+    at n = 2048: 16 CTAs of 128 rows, (220 KiB/8 - 64)/(128 + 2)) is factored in chunks, each
+    chunk block-projected against the earlier chunks of its panel before its own MGS.  With
+    s = 512 every panel takes that path (chunks 216 + 216 + 80); the head columns [0, n-2s) —
+    two whole chunked panels and the flush between them — meet the R2 <= 1e-10 bar."""
+    n, s = 2048, 512
+    A = synth.gen_numpy("gaussian", n, seed=11)
+    Qo, Ro, io, _ = oracle.qr(A, s)
+    Qg, Rg, ig = run_qr(A, s)
+    assert io == ig == 0
+    assert n - 2 * s >= 2 * 216
+    check_qr(A, s, Qg, Rg, Qo, Ro)
 
 
 @pytest.mark.parametrize("n,s", [(256, 1), (256, 64), (1024, 128), (4096, 128)])
@@ -443,12 +508,17 @@ def test_variable_steps_invalid():
 @pytest.mark.parametrize("dtype", [0, 1])
 def test_chol_cfg5_full_size_sampled(dtype):
     """BASELINE.json configs[4] at its full size, n = 65536, s = 512, in bench.py's launch
-    configuration (single GPU, out of place): the first K columns of L against the restricted
-    oracle (bitwise the full oracle's first K columns), a Freivalds residual of the whole
+    configuration (single GPU, out of place): the first K columns of L (K = 3s fp64, 2s fp32,
+    so flushed entries — incl. the first, out-of-place flush over 65024 rows — are compared
+    elementwise) against the restricted oracle (bitwise the full oracle's first K columns),
+    a Freivalds residual of the whole
     factor (torch fp64, an independent checker), info 0 and a positive diagonal.
     fp64 bar R2 <= 1e-10 / residual <= 1e-13 n; fp32 (3xTF32, the fp32-rounded input) 2e-4 /
     1e-5 n."""
-    n, s, K = 65536, 512, 256
+    n, s = 65536, 512
+    K = 1536 if dtype == 0 else 1024            # >= 3s (fp64) / 2s (fp32): flushed columns compared
+    f1, f2 = flushed_cols(K, s)
+    assert f1 >= s and (dtype == 1 or f2 >= s), (f1, f2)
     A = synth.gen_torch("spd_scaled", n, seed=0)
     if dtype == 1:
         A = A.float()
