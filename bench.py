@@ -41,6 +41,8 @@ WORKLOADS = {
     "chol_f64_n65536_s512": ("chol", 65536, 512, "spd_scaled", "f64", "configs[4]"),
     "chol_f32_n65536_s512": ("chol", 65536, 512, "spd_scaled", "f32", "configs[4]"),
     "chol_f32_n16384_s512": ("chol", 16384, 512, "spd_scaled", "f32", "configs[2] in fp32"),
+    "lu_f32_n4096_s64": ("lu", 4096, 64, "diag_dominant", "f32", "configs[1] in fp32 (f4)"),
+    "qr_f32_n8192_s128": ("qr", 8192, 128, "gaussian", "f32", "configs[3] in fp32 (f4)"),
 }
 DEFAULT = "chol_f64_n65536_s512"
 CALIB = os.path.join(ROOT, "calib", "peaks_fp64_tf32.json")

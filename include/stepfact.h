@@ -19,8 +19,9 @@
  *     cudaStream_t; NULL = the legacy default stream).  They never synchronize.
  *   - Numerical failure is NOT a return code: it is written, stream-ordered, to the device
  *     int64 *d_info: 0 = success, k >= 1 = the first (1-based) column
- *     at which the algorithm could not continue (see each function).  Columns >= k of the
- *     outputs are then unspecified (LAPACK/cuSOLVER devInfo semantics).
+ *     at which the algorithm could not continue (see each function).  The outputs are then
+ *     unspecified from the first column of the panel (step) containing column k on; the
+ *     panels before it hold their final values (cf. LAPACK/cuSOLVER devInfo semantics).
  *   - Return codes (sf_status) report argument / resource / launch errors, synchronously;
  *     on SF_EINVAL nothing has been enqueued.  sf_last_error() gives a one-line detail.
  *   - dtype: SF_F64 (double storage and arithmetic; the update runs on the FP64 tensor

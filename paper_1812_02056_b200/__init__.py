@@ -184,59 +184,74 @@ def profile_collect():
 
 # ----------------------------------------------------------------------- raw column-major API
 
-def chol_colmajor(n, s, dA, lda, dL, ldl, d_info, dtype=SF_F64, stream=None):
-    """chol_factor on raw column-major device buffers (torch tensors or int pointers)."""
-    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
-    _check(lib().chol_factor(n, s, dtype, ptr(dA), lda, ptr(dL), ldl, ptr(d_info), _stream(stream)))
+def _ptr(x):
+    return x.data_ptr() if hasattr(x, "data_ptr") else int(x)
 
 
-def lu_colmajor(n, s, dA, lda, dLU, ldlu, d_info, dtype=SF_F64, stream=None):
-    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
-    _check(lib().lu_factor(n, s, dtype, ptr(dA), lda, ptr(dLU), ldlu, ptr(d_info), _stream(stream)))
+def _dt(dtype, *bufs):
+    """The SF_* dtype code: inferred from the (torch) buffers when not given; every tensor
+    buffer must then agree with it (a mismatch would make the library read and write past
+    a buffer of the other element size)."""
+    import torch
+    codes = {torch.float64: SF_F64, torch.float32: SF_F32}
+    seen = {codes.get(b.dtype, -1) for b in bufs if hasattr(b, "dtype")}
+    if dtype is None:
+        if len(seen) != 1 or -1 in seen:
+            raise TypeError("buffers must all be float64 or all float32 tensors (or pass dtype=)")
+        return seen.pop()
+    if seen - {dtype}:
+        raise TypeError(f"dtype={dtype} does not match the buffers' element type")
+    return dtype
 
 
-def qr_colmajor(n, s, dA, lda, dQ, ldq, dR, ldr, d_info, dtype=SF_F64, stream=None):
-    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
-    _check(lib().qr_factor(n, s, dtype, ptr(dA), lda, ptr(dQ), ldq, ptr(dR), ldr, ptr(d_info), _stream(stream)))
+def chol_colmajor(n, s, dA, lda, dL, ldl, d_info, dtype=None, stream=None):
+    """chol_factor on raw column-major device buffers (torch tensors or int pointers; with raw
+    pointers pass dtype)."""
+    dt = _dt(dtype, dA, dL)
+    _check(lib().chol_factor(n, s, dt, _ptr(dA), lda, _ptr(dL), ldl, _ptr(d_info), _stream(stream)))
+
+
+def lu_colmajor(n, s, dA, lda, dLU, ldlu, d_info, dtype=None, stream=None):
+    _check(lib().lu_factor(n, s, _dt(dtype, dA, dLU), _ptr(dA), lda, _ptr(dLU), ldlu, _ptr(d_info), _stream(stream)))
+
+
+def qr_colmajor(n, s, dA, lda, dQ, ldq, dR, ldr, d_info, dtype=None, stream=None):
+    _check(lib().qr_factor(n, s, _dt(dtype, dA, dQ, dR), _ptr(dA), lda, _ptr(dQ), ldq, _ptr(dR), ldr, _ptr(d_info),
+                           _stream(stream)))
 
 
 def _steps_arr(steps):
     return (ctypes.c_int64 * len(steps))(*[int(x) for x in steps])
 
 
-def chol_steps_colmajor(n, steps, dA, lda, dL, ldl, d_info, dtype=SF_F64, stream=None):
+def chol_steps_colmajor(n, steps, dA, lda, dL, ldl, d_info, dtype=None, stream=None):
     """chol_factor_steps: variable step sequence."""
-    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
-    _check(lib().chol_factor_steps(n, len(steps), _steps_arr(steps), dtype, ptr(dA), lda, ptr(dL), ldl, ptr(d_info),
-                                   _stream(stream)))
+    _check(lib().chol_factor_steps(n, len(steps), _steps_arr(steps), _dt(dtype, dA, dL), _ptr(dA), lda, _ptr(dL), ldl,
+                                   _ptr(d_info), _stream(stream)))
 
 
-def lu_steps_colmajor(n, steps, dA, lda, dLU, ldlu, d_info, dtype=SF_F64, stream=None):
-    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
-    _check(lib().lu_factor_steps(n, len(steps), _steps_arr(steps), dtype, ptr(dA), lda, ptr(dLU), ldlu, ptr(d_info),
-                                 _stream(stream)))
+def lu_steps_colmajor(n, steps, dA, lda, dLU, ldlu, d_info, dtype=None, stream=None):
+    _check(lib().lu_factor_steps(n, len(steps), _steps_arr(steps), _dt(dtype, dA, dLU), _ptr(dA), lda, _ptr(dLU), ldlu,
+                                 _ptr(d_info), _stream(stream)))
 
 
-def qr_steps_colmajor(n, steps, dA, lda, dQ, ldq, dR, ldr, d_info, dtype=SF_F64, stream=None):
-    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
-    _check(lib().qr_factor_steps(n, len(steps), _steps_arr(steps), dtype, ptr(dA), lda, ptr(dQ), ldq, ptr(dR), ldr,
-                                 ptr(d_info), _stream(stream)))
+def qr_steps_colmajor(n, steps, dA, lda, dQ, ldq, dR, ldr, d_info, dtype=None, stream=None):
+    _check(lib().qr_factor_steps(n, len(steps), _steps_arr(steps), _dt(dtype, dA, dQ, dR), _ptr(dA), lda, _ptr(dQ), ldq,
+                                 _ptr(dR), ldr, _ptr(d_info), _stream(stream)))
 
 
-def chol_solve_colmajor(n, nrhs, dL, ldl, dB, ldb, dtype=SF_F64, stream=None):
+def chol_solve_colmajor(n, nrhs, dL, ldl, dB, ldb, dtype=None, stream=None):
     """chol_solve: B := A^-1 B with A = L L^T (column-major device buffers)."""
-    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
-    _check(lib().chol_solve(n, nrhs, dtype, ptr(dL), ldl, ptr(dB), ldb, _stream(stream)))
+    _check(lib().chol_solve(n, nrhs, _dt(dtype, dL, dB), _ptr(dL), ldl, _ptr(dB), ldb, _stream(stream)))
 
 
-def lu_solve_colmajor(n, nrhs, dLU, ldlu, dB, ldb, dtype=SF_F64, stream=None):
-    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
-    _check(lib().lu_solve(n, nrhs, dtype, ptr(dLU), ldlu, ptr(dB), ldb, _stream(stream)))
+def lu_solve_colmajor(n, nrhs, dLU, ldlu, dB, ldb, dtype=None, stream=None):
+    _check(lib().lu_solve(n, nrhs, _dt(dtype, dLU, dB), _ptr(dLU), ldlu, _ptr(dB), ldb, _stream(stream)))
 
 
-def qr_solve_colmajor(n, nrhs, dQ, ldq, dR, ldr, dB, ldb, dtype=SF_F64, stream=None):
-    ptr = lambda x: x.data_ptr() if hasattr(x, "data_ptr") else int(x)
-    _check(lib().qr_solve(n, nrhs, dtype, ptr(dQ), ldq, ptr(dR), ldr, ptr(dB), ldb, _stream(stream)))
+def qr_solve_colmajor(n, nrhs, dQ, ldq, dR, ldr, dB, ldb, dtype=None, stream=None):
+    _check(lib().qr_solve(n, nrhs, _dt(dtype, dQ, dR, dB), _ptr(dQ), ldq, _ptr(dR), ldr, _ptr(dB), ldb,
+                          _stream(stream)))
 
 
 # ----------------------------------------------------------------------- torch convenience API
@@ -287,36 +302,60 @@ def qr(A, s, stream=None):
 
 # ----------------------------------------------------------------------- host (end-to-end) API
 
-def _host_ptr(x):
+def _host_buf(x, n, dtype=None):
+    """(pointer, SF_* dtype) of an n x n column-major HOST buffer, validated: a numpy array in
+    Fortran order (logical matrix X, X[i, j] at column-major offset i + j*n) or a contiguous
+    CPU torch tensor holding the column-major buffer (row j = column j, i.e. the tensor is
+    X^T).  The element type must be float64 or float32 and agree with `dtype` if given."""
     if hasattr(x, "data_ptr"):
-        assert not x.is_cuda
-        return x.data_ptr()
-    assert isinstance(x, np.ndarray) and x.flags["F_CONTIGUOUS"] or x.flags["C_CONTIGUOUS"]
-    return x.ctypes.data
+        import torch
+        if x.is_cuda or not x.is_contiguous() or tuple(x.shape) != (n, n):
+            raise ValueError("host buffers must be contiguous CPU tensors of shape (n, n)")
+        code = {torch.float64: SF_F64, torch.float32: SF_F32}.get(x.dtype)
+        ptr = x.data_ptr()
+    else:
+        if not isinstance(x, np.ndarray) or x.shape != (n, n) or not x.flags["F_CONTIGUOUS"]:
+            raise ValueError("host buffers must be Fortran-ordered (column-major) numpy arrays of shape (n, n)")
+        if not x.flags["WRITEABLE"]:
+            raise ValueError("host buffers must be writeable")
+        code = {np.dtype(np.float64): SF_F64, np.dtype(np.float32): SF_F32}.get(x.dtype)
+        ptr = x.ctypes.data
+    if code is None:
+        raise TypeError("host buffers must be float64 or float32")
+    if dtype is not None and dtype != code:
+        raise TypeError(f"dtype={dtype} does not match the host buffer's element type")
+    return ptr, code
 
 
-def chol_host(hA, s, hL=None, dtype=SF_F64):
-    """chol_factor_host on column-major host buffers (pinned torch tensors or numpy)."""
+def chol_host(hA, s, hL=None, dtype=None):
+    """chol_factor_host on column-major host buffers (pinned torch tensors or numpy); dtype is
+    inferred from hA and every buffer must match it."""
     n = hA.shape[0]
+    pa, dt = _host_buf(hA, n, dtype)
     out = hA if hL is None else hL
+    po, _ = _host_buf(out, n, dt)
     info = ctypes.c_int64(0)
-    _check(lib().chol_factor_host(n, s, dtype, _host_ptr(hA), n, _host_ptr(out), n, ctypes.addressof(info)))
+    _check(lib().chol_factor_host(n, s, dt, pa, n, po, n, ctypes.addressof(info)))
     return out, info.value
 
 
-def lu_host(hA, s, hLU=None, dtype=SF_F64):
+def lu_host(hA, s, hLU=None, dtype=None):
     n = hA.shape[0]
+    pa, dt = _host_buf(hA, n, dtype)
     out = hA if hLU is None else hLU
+    po, _ = _host_buf(out, n, dt)
     info = ctypes.c_int64(0)
-    _check(lib().lu_factor_host(n, s, dtype, _host_ptr(hA), n, _host_ptr(out), n, ctypes.addressof(info)))
+    _check(lib().lu_factor_host(n, s, dt, pa, n, po, n, ctypes.addressof(info)))
     return out, info.value
 
 
-def qr_host(hA, s, hQ, hR, dtype=SF_F64):
+def qr_host(hA, s, hQ, hR, dtype=None):
     n = hA.shape[0]
+    pa, dt = _host_buf(hA, n, dtype)
+    pq, _ = _host_buf(hQ, n, dt)
+    pr, _ = _host_buf(hR, n, dt)
     info = ctypes.c_int64(0)
-    _check(lib().qr_factor_host(n, s, dtype, _host_ptr(hA), n, _host_ptr(hQ), n, _host_ptr(hR), n,
-                                ctypes.addressof(info)))
+    _check(lib().qr_factor_host(n, s, dt, pa, n, pq, n, pr, n, ctypes.addressof(info)))
     return hQ, hR, info.value
 
 
@@ -375,18 +414,21 @@ def _ptr_array(xs):
     return arr
 
 
-def chol_dist(comm, n, s, dA, dL, ld, d_info, dtype=SF_F64, stream=None):
+def chol_dist(comm, n, s, dA, dL, ld, d_info, dtype=None, stream=None):
     """chol_factor_dist: lists (one entry per local rank) of column-major local buffers."""
+    dtype = _dt(dtype, *dA, *dL)
     _check(lib().chol_factor_dist(comm.handle, n, s, dtype, _ptr_array(dA), _ptr_array(dL), ld, _ptr_array(d_info),
                                   _stream(stream)))
 
 
-def lu_dist(comm, n, s, dA, dLU, ld, d_info, dtype=SF_F64, stream=None):
+def lu_dist(comm, n, s, dA, dLU, ld, d_info, dtype=None, stream=None):
+    dtype = _dt(dtype, *dA, *dLU)
     _check(lib().lu_factor_dist(comm.handle, n, s, dtype, _ptr_array(dA), _ptr_array(dLU), ld, _ptr_array(d_info),
                                 _stream(stream)))
 
 
-def qr_dist(comm, n, s, dA, dQ, dR, ld, d_info, dtype=SF_F64, stream=None):
+def qr_dist(comm, n, s, dA, dQ, dR, ld, d_info, dtype=None, stream=None):
+    dtype = _dt(dtype, *dA, *dQ, *dR)
     _check(lib().qr_factor_dist(comm.handle, n, s, dtype, _ptr_array(dA), _ptr_array(dQ), _ptr_array(dR), ld,
                                 _ptr_array(d_info), _stream(stream)))
 

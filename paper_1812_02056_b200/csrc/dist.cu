@@ -283,6 +283,7 @@ static int setup_ranks(sf_comm_t comm, std::vector<Rank<T>>& rk, const Cyclic& c
     x.d_info = d_info[i];
     SF_CUDA(rank_streams(comm->device, i, x.st));
     SF_CUDA(x.ws.init(sizeof(T) * (2 * buf_elems + qfull_elems + extra_elems) + 64 * 1024, caller));
+    x.ws.join(x.st.mn); x.ws.join(x.st.pan); x.ws.join(x.st.com);
     x.fail = x.ws.template take<long long>(2);
     x.tol = x.ws.template take<T>(1);
     x.sumsq = x.ws.template take<double>(1);

@@ -67,7 +67,7 @@ static int chol_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* L, in
   SF_CUDA(init_fail(fail, st));
   Side* sd = nullptr;
   const bool la = lookahead_on() && S.P() > 1;
-  if (la) SF_CUDA(side_stream(sd));
+  if (la) { SF_CUDA(side_stream(sd)); ws.join(sd->st); }
   {
     ProfScope ps(1, 0.0, st);
     const int64_t w0 = S.w(0);
@@ -133,7 +133,7 @@ static int chol_run_f32(int64_t n, const Sched& S, const float* A, int64_t lda, 
   SF_CUDA(init_fail(fail, st));
   Side* sd = nullptr;
   const bool la = lookahead_on() && S.P() > 1;
-  if (la) SF_CUDA(side_stream(sd));
+  if (la) { SF_CUDA(side_stream(sd)); ws.join(sd->st); }
   {
     ProfScope ps(1, 0.0, st);
     const int64_t w0 = S.w(0);
@@ -205,7 +205,7 @@ static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int
   SF_CUDA(frob_norm_tol<T>(n, A, lda, tol, part, st));
   Side* sd = nullptr;
   const bool la = lookahead_on() && S.P() > 1;
-  if (la) SF_CUDA(side_stream(sd));
+  if (la) { SF_CUDA(side_stream(sd)); ws.join(sd->st); }
   {
     ProfScope ps(1, 0.0, st);
     const int64_t w0 = S.w(0);
@@ -325,7 +325,7 @@ static int qr_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* Q, int6
   SF_CUDA(frob_norm_tol<T>(n, A, lda, tol, part, st));
   Side* sd = nullptr;
   const bool la = lookahead_on() && S.P() > 1;
-  if (la) SF_CUDA(side_stream(sd));
+  if (la) { SF_CUDA(side_stream(sd)); ws.join(sd->st); }
   // R := Q^T A by row blocks as soon as their Q columns are final: the
   // rows [z, z+w) of R need only Q[:, z:z+w) (later flushes never touch it), so each block
   // runs on a low-priority stream in the SM slots the short-K flushes leave idle, instead
@@ -335,6 +335,7 @@ static int qr_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* Q, int6
   const bool early_r = qr_early_r_on();
   if (early_r) {
     SF_CUDA(low_stream(rs));
+    ws.join(rs->st);
     SF_CUDA(fork_join(*rs, st, rs->st));
     SF_CUDA(zero_strict_lower<T>(n, R, ldr, rs->st));
   }
@@ -488,7 +489,9 @@ static int run_graph(const GraphKey& key, cudaStream_t st, F&& body) {
     if (ei != cudaSuccess) { e->exec = nullptr; return fail_with(SF_ECUDA, "graph instantiate: %s", cudaGetErrorString(ei)); }
     e->launches = nl;
   }
+  if (key.kind == 2) mgs_order_before(st);   // QR: persistent MGS grids never overlap
   SF_CUDA(cudaGraphLaunch(e->exec, st));
+  if (key.kind == 2) mgs_order_after(st);
   count_launch((int)e->launches);
   return SF_OK;
 }
@@ -659,52 +662,48 @@ int qr_solve(int64_t n, int64_t nrhs, int dtype, const void* dQ, int64_t ldq, co
 }
 
 // ------------------------------------------------------------------ host-buffer variants
-static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hO1, int64_t ld1,
-                     void* hO2, int64_t ld2, int64_t* info) {
-  SF_API_LOCK;
-  if (n < 1 || !hA || !hO1 || !info || (kind == 2 && !hO2)) return fail_with(SF_EINVAL, "bad host arguments");
-  if (lda < n || ld1 < n || (kind == 2 && ld2 < n)) return fail_with(SF_EINVAL, "leading dimension < n");
-  if (s < 1 || s > n) return fail_with(SF_EINVAL, "step s=%lld outside [1, n=%lld]", (long long)s, (long long)n);
-  if (dtype != SF_F64 && dtype != SF_F32) return fail_with(SF_EINVAL, "unknown dtype %d", dtype);
+// Host buffers the caller did not pin are registered (page-locked) for the duration of the
+// call: the per-panel device->host copies must be asynchronous, or enqueueing would stall
+// at every panel until that panel is factored and the lookahead overlap would be lost.
+struct HostPin {
+  void* ptr[3] = {nullptr, nullptr, nullptr};
+  int n = 0;
+  cudaError_t pin(const void* p, size_t bytes) {
+    for (int i = 0; i < n; ++i)
+      if (ptr[i] == p) return cudaSuccess;
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) cudaGetLastError();
+    if (e == cudaSuccess && at.type != cudaMemoryTypeUnregistered) return cudaSuccess;   // pinned / managed already
+    e = cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterDefault);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) { cudaGetLastError(); return cudaSuccess; }
+    if (e != cudaSuccess) return e;
+    ptr[n++] = const_cast<void*>(p);
+    return cudaSuccess;
+  }
+  ~HostPin() {
+    for (int i = 0; i < n; ++i) cudaHostUnregister(ptr[i]);
+  }
+};
+
+static int host_body(int kind, int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hO1, int64_t ld1,
+                     void* hO2, int64_t ld2, int64_t* info, char* d, int64_t* dinfo, cudaStream_t st,
+                     cudaStream_t cs, cudaEvent_t ev) {
   const size_t elt = dtype == SF_F64 ? 8 : 4;
   const size_t bytes = elt * (size_t)n * (size_t)n;
-  static cudaStream_t streams[16] = {};
-  int devh = 0;
-  SF_CUDA(cudaGetDevice(&devh));
-  if (!streams[devh & 15]) SF_CUDA(cudaStreamCreateWithFlags(&streams[devh & 15], cudaStreamNonBlocking));
-  cudaStream_t st = streams[devh & 15];
-  {
-    // keep freed device blocks in the stream-ordered pool so repeated calls do not pay
-    // for fresh allocations
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
-  char* d = nullptr;
-  const int nbuf = kind == 2 ? 3 : 1;
-  cudaError_t e = cudaMallocAsync((void**)&d, nbuf * bytes + 256, st);
-  if (e != cudaSuccess) return fail_with(SF_ENOMEM, "device allocation failed");
-  int64_t* dinfo = (int64_t*)(d + nbuf * bytes);
+  // the copy stream must not run ahead of the previous call
+  SF_CUDA(cudaEventRecord(ev, st));
+  SF_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+  const Sched S(n, s);
   int rc = SF_OK;
   if (kind == 0) {
     // Cholesky reads and writes only the lower triangle: copy it panel by panel (half the
-    // bytes), and return each panel of L as soon as it is final, on a copy stream, while the
-    // later flushes run (the device->host copy hides behind the factorization).
-    static cudaStream_t cstreams[16] = {};
-    static cudaEvent_t cevents[16] = {};
-    if (!cstreams[devh & 15]) {
-      SF_CUDA(cudaStreamCreateWithFlags(&cstreams[devh & 15], cudaStreamNonBlocking));
-      SF_CUDA(cudaEventCreateWithFlags(&cevents[devh & 15], cudaEventDisableTiming));
-    }
-    cudaStream_t cs = cstreams[devh & 15];
-    cudaEvent_t ev = cevents[devh & 15];
-    for (int64_t z = 0; z < n && e == cudaSuccess; z += s) {
+    // bytes), and return each panel of L as soon as it is final, on the copy stream, while
+    // the later flushes run (the device->host copy hides behind the factorization).
+    for (int64_t z = 0; z < n; z += s) {
       const int64_t w = (s < n - z) ? s : n - z;
-      e = cudaMemcpy2DAsync(d + elt * (z + z * n), n * elt, (const char*)hA + elt * (z + z * lda), lda * elt,
-                            (n - z) * elt, w, cudaMemcpyHostToDevice, st);
+      SF_CUDA(cudaMemcpy2DAsync(d + elt * (z + z * n), n * elt, (const char*)hA + elt * (z + z * lda), lda * elt,
+                                (n - z) * elt, w, cudaMemcpyHostToDevice, st));
     }
     struct D2H : PanelHook {
       int64_t n, ldh; size_t elt; const char* dev; char* host; cudaStream_t cs; cudaEvent_t ev;
@@ -718,105 +717,100 @@ static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, 
       }
     } hook;
     hook.n = n; hook.ldh = ld1; hook.elt = elt; hook.dev = d; hook.host = (char*)hO1; hook.cs = cs; hook.ev = ev;
-    if (e == cudaSuccess) {
-      SF_CUDA(cudaEventRecord(ev, st));      // the copy stream must not run ahead of the previous call
-      SF_CUDA(cudaStreamWaitEvent(cs, ev, 0));
-      const Sched S(n, s);
-      rc = dtype == SF_F64 ? chol_run<double>(n, S, (const double*)d, n, (double*)d, n, dinfo, st, &hook)
-                           : chol_run_f32(n, S, (const float*)d, n, (float*)d, n, dinfo, st, &hook);
-      // join the copy stream even on failure: the device buffer is freed on st below
-      cudaError_t ej = cudaEventRecord(ev, cs);
-      if (ej == cudaSuccess) ej = cudaStreamWaitEvent(st, ev, 0);
-      if (!rc) {
-        e = ej;
-        if (e == cudaSuccess) e = cudaMemcpyAsync(info, dinfo, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    rc = dtype == SF_F64 ? chol_run<double>(n, S, (const double*)d, n, (double*)d, n, dinfo, st, &hook)
+                         : chol_run_f32(n, S, (const float*)d, n, (float*)d, n, dinfo, st, &hook);
+  } else if (kind == 1) {
+    SF_CUDA(cudaMemcpy2DAsync(d, n * elt, hA, lda * elt, n * elt, n, cudaMemcpyHostToDevice, st));
+    // LU: each panel's L columns [z, z+w) (rows >= z) and U rows [z, z+w) (columns >= z+w)
+    // are final once the panel is factored; returned on the copy stream as for Cholesky.
+    struct LuD2H : PanelHook {
+      int64_t n, ldh; size_t elt; const char* dev; char* host; cudaStream_t cs; cudaEvent_t ev;
+      cudaError_t done(int64_t z, int64_t w, cudaStream_t pst) override {
+        cudaError_t r = cudaEventRecord(ev, pst);
+        if (r == cudaSuccess) r = cudaStreamWaitEvent(cs, ev, 0);
+        if (r == cudaSuccess)   // L columns (incl. the diagonal block's U part)
+          r = cudaMemcpy2DAsync(host + elt * (z + z * ldh), ldh * elt, dev + elt * (z + z * n), n * elt,
+                                (n - z) * elt, w, cudaMemcpyDeviceToHost, cs);
+        if (r == cudaSuccess && z + w < n)   // U rows right of the panel
+          r = cudaMemcpy2DAsync(host + elt * (z + (z + w) * ldh), ldh * elt, dev + elt * (z + (z + w) * n), n * elt,
+                                w * elt, n - z - w, cudaMemcpyDeviceToHost, cs);
+        return r;
       }
-    }
+    } hook;
+    hook.n = n; hook.ldh = ld1; hook.elt = elt; hook.dev = d; hook.host = (char*)hO1; hook.cs = cs; hook.ev = ev;
+    rc = dtype == SF_F64 ? lu_run<double>(n, S, (const double*)d, n, (double*)d, n, dinfo, st, &hook)
+                         : lu_run<float>(n, S, (const float*)d, n, (float*)d, n, dinfo, st, &hook);
   } else {
-  e = cudaMemcpy2DAsync(d, n * elt, hA, lda * elt, n * elt, n, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) {
-    if (kind == 1) {
-      // LU: each panel's L columns [z, z+w) (rows >= z) and U rows [z, z+w) (columns >= z+w)
-      // are final once the panel is factored; return them on a copy stream while the later
-      // flushes run, as for Cholesky.
-      static cudaStream_t lstreams[16] = {};
-      static cudaEvent_t levents[16] = {};
-      if (!lstreams[devh & 15]) {
-        SF_CUDA(cudaStreamCreateWithFlags(&lstreams[devh & 15], cudaStreamNonBlocking));
-        SF_CUDA(cudaEventCreateWithFlags(&levents[devh & 15], cudaEventDisableTiming));
+    SF_CUDA(cudaMemcpy2DAsync(d, n * elt, hA, lda * elt, n * elt, n, cudaMemcpyHostToDevice, st));
+    // QR: Q[:, z:z+w) is final once panel p's MGS is done (later flushes touch columns >= z+w
+    // only): returned on the copy stream while the factorization continues; R (one product
+    // at the end) follows.
+    struct QD2H : PanelHook {
+      int64_t n, ldh; size_t elt; const char* dev; char* host; cudaStream_t cs; cudaEvent_t ev;
+      cudaError_t done(int64_t z, int64_t w, cudaStream_t pst) override {
+        cudaError_t r = cudaEventRecord(ev, pst);
+        if (r == cudaSuccess) r = cudaStreamWaitEvent(cs, ev, 0);
+        if (r == cudaSuccess)
+          r = cudaMemcpy2DAsync(host + elt * (z * ldh), ldh * elt, dev + elt * (z * n), n * elt, n * elt, w,
+                                cudaMemcpyDeviceToHost, cs);
+        return r;
       }
-      struct LuD2H : PanelHook {
-        int64_t n, ldh; size_t elt; const char* dev; char* host; cudaStream_t cs; cudaEvent_t ev;
-        cudaError_t done(int64_t z, int64_t w, cudaStream_t pst) override {
-          cudaError_t r = cudaEventRecord(ev, pst);
-          if (r == cudaSuccess) r = cudaStreamWaitEvent(cs, ev, 0);
-          if (r == cudaSuccess)   // L columns (incl. the diagonal block's U part)
-            r = cudaMemcpy2DAsync(host + elt * (z + z * ldh), ldh * elt, dev + elt * (z + z * n), n * elt,
-                                  (n - z) * elt, w, cudaMemcpyDeviceToHost, cs);
-          if (r == cudaSuccess && z + w < n)   // U rows right of the panel
-            r = cudaMemcpy2DAsync(host + elt * (z + (z + w) * ldh), ldh * elt, dev + elt * (z + (z + w) * n), n * elt,
-                                  w * elt, n - z - w, cudaMemcpyDeviceToHost, cs);
-          return r;
-        }
-      } hook;
-      hook.n = n; hook.ldh = ld1; hook.elt = elt; hook.dev = d; hook.host = (char*)hO1;
-      hook.cs = lstreams[devh & 15]; hook.ev = levents[devh & 15];
-      SF_CUDA(cudaEventRecord(hook.ev, st));   // the copy stream must not run ahead of the previous call
-      SF_CUDA(cudaStreamWaitEvent(hook.cs, hook.ev, 0));
-      const Sched S(n, s);
-      rc = dtype == SF_F64 ? lu_run<double>(n, S, (const double*)d, n, (double*)d, n, dinfo, st, &hook)
-                           : lu_run<float>(n, S, (const float*)d, n, (float*)d, n, dinfo, st, &hook);
-      {   // join the copy stream even on failure: the device buffer is freed on st below
-        cudaError_t ej = cudaEventRecord(hook.ev, hook.cs);
-        if (ej == cudaSuccess) ej = cudaStreamWaitEvent(st, hook.ev, 0);
-        if (!rc) e = ej;
-      }
-    } else {
-      // QR: Q[:, z:z+w) is final once panel p's MGS is done (later flushes touch columns
-      // >= z+w only): return it on a copy stream while the factorization continues; R
-      // (one product at the end) follows.
-      static cudaStream_t qstreams[16] = {};
-      static cudaEvent_t qevents[16] = {};
-      if (!qstreams[devh & 15]) {
-        SF_CUDA(cudaStreamCreateWithFlags(&qstreams[devh & 15], cudaStreamNonBlocking));
-        SF_CUDA(cudaEventCreateWithFlags(&qevents[devh & 15], cudaEventDisableTiming));
-      }
-      struct QD2H : PanelHook {
-        int64_t n, ldh; size_t elt; const char* dev; char* host; cudaStream_t cs; cudaEvent_t ev;
-        cudaError_t done(int64_t z, int64_t w, cudaStream_t pst) override {
-          cudaError_t r = cudaEventRecord(ev, pst);
-          if (r == cudaSuccess) r = cudaStreamWaitEvent(cs, ev, 0);
-          if (r == cudaSuccess)
-            r = cudaMemcpy2DAsync(host + elt * (z * ldh), ldh * elt, dev + elt * (z * n), n * elt, n * elt, w,
-                                  cudaMemcpyDeviceToHost, cs);
-          return r;
-        }
-      } hook;
-      hook.n = n; hook.ldh = ld1; hook.elt = elt; hook.dev = d + bytes; hook.host = (char*)hO1;
-      hook.cs = qstreams[devh & 15]; hook.ev = qevents[devh & 15];
-      SF_CUDA(cudaEventRecord(hook.ev, st));
-      SF_CUDA(cudaStreamWaitEvent(hook.cs, hook.ev, 0));
-      const Sched S(n, s);
-      rc = dtype == SF_F64
-               ? qr_run<double>(n, S, (const double*)d, n, (double*)(d + bytes), n, (double*)(d + 2 * bytes), n, dinfo,
-                                st, &hook)
-               : qr_run<float>(n, S, (const float*)d, n, (float*)(d + bytes), n, (float*)(d + 2 * bytes), n, dinfo,
-                               st, &hook);
-      if (!rc) e = cudaMemcpy2DAsync(hO2, ld2 * elt, d + 2 * bytes, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st);
-      {   // join the copy stream even on failure: the device buffer is freed on st below
-        cudaError_t ej = cudaEventRecord(hook.ev, hook.cs);
-        if (ej == cudaSuccess) ej = cudaStreamWaitEvent(st, hook.ev, 0);
-        if (!rc && e == cudaSuccess) e = ej;
-      }
-    }
-    if (!rc && e == cudaSuccess) e = cudaMemcpyAsync(info, dinfo, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+    } hook;
+    hook.n = n; hook.ldh = ld1; hook.elt = elt; hook.dev = d + bytes; hook.host = (char*)hO1; hook.cs = cs; hook.ev = ev;
+    rc = dtype == SF_F64 ? qr_run<double>(n, S, (const double*)d, n, (double*)(d + bytes), n,
+                                          (double*)(d + 2 * bytes), n, dinfo, st, &hook)
+                         : qr_run<float>(n, S, (const float*)d, n, (float*)(d + bytes), n, (float*)(d + 2 * bytes), n,
+                                         dinfo, st, &hook);
+    if (!rc)
+      SF_CUDA(cudaMemcpy2DAsync(hO2, ld2 * elt, d + 2 * bytes, n * elt, n * elt, n, cudaMemcpyDeviceToHost, st));
   }
-  }
-  cudaFreeAsync(d, st);
-  cudaError_t e2 = cudaStreamSynchronize(st);
   if (rc) return rc;
-  if (e != cudaSuccess) return fail_with(SF_ECUDA, "host copy: %s", cudaGetErrorString(e));
-  if (e2 != cudaSuccess) return fail_with(SF_ECUDA, "stream sync: %s", cudaGetErrorString(e2));
+  SF_CUDA(cudaMemcpyAsync(info, dinfo, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  return SF_OK;
+}
+
+static int host_call(int kind, int64_t n, int64_t s, int dtype, const void* hA, int64_t lda, void* hO1, int64_t ld1,
+                     void* hO2, int64_t ld2, int64_t* info) {
+  SF_API_LOCK;
+  if (n < 1 || !hA || !hO1 || !info || (kind == 2 && !hO2)) return fail_with(SF_EINVAL, "bad host arguments");
+  if (lda < n || ld1 < n || (kind == 2 && ld2 < n)) return fail_with(SF_EINVAL, "leading dimension < n");
+  if (s < 1 || s > n) return fail_with(SF_EINVAL, "step s=%lld outside [1, n=%lld]", (long long)s, (long long)n);
+  if (dtype != SF_F64 && dtype != SF_F32) return fail_with(SF_EINVAL, "unknown dtype %d", dtype);
+  const size_t elt = dtype == SF_F64 ? 8 : 4;
+  const size_t bytes = elt * (size_t)n * (size_t)n;
+  int devh = 0;
+  SF_CUDA(cudaGetDevice(&devh));
+  // per-device internal compute stream + copy stream / event (created once)
+  static cudaStream_t streams[16] = {}, cstreams[16] = {};
+  static cudaEvent_t cevents[16] = {};
+  if (!streams[devh & 15]) {
+    SF_CUDA(cudaStreamCreateWithFlags(&streams[devh & 15], cudaStreamNonBlocking));
+    SF_CUDA(cudaStreamCreateWithFlags(&cstreams[devh & 15], cudaStreamNonBlocking));
+    SF_CUDA(cudaEventCreateWithFlags(&cevents[devh & 15], cudaEventDisableTiming));
+  }
+  cudaStream_t st = streams[devh & 15], cs = cstreams[devh & 15];
+  cudaEvent_t ev = cevents[devh & 15];
+  Workspace::keep_pool();   // repeated calls reuse the device block from the stream-ordered pool
+  HostPin pins;
+  SF_CUDA(pins.pin(hA, elt * ((size_t)lda * (n - 1) + n)));
+  SF_CUDA(pins.pin(hO1, elt * ((size_t)ld1 * (n - 1) + n)));
+  if (kind == 2) SF_CUDA(pins.pin(hO2, elt * ((size_t)ld2 * (n - 1) + n)));
+  char* d = nullptr;
+  const int nbuf = kind == 2 ? 3 : 1;
+  if (cudaMallocAsync((void**)&d, nbuf * bytes + 256, st) != cudaSuccess) {
+    cudaGetLastError();
+    return fail_with(SF_ENOMEM, "device allocation of %zu bytes failed", nbuf * bytes + 256);
+  }
+  int64_t* dinfo = (int64_t*)(d + nbuf * bytes);
+  const int rc = host_body(kind, n, s, dtype, hA, lda, hO1, ld1, hO2, ld2, info, d, dinfo, st, cs, ev);
+  // on every path: join the copy stream (it reads d), free d, wait for the call's work
+  cudaError_t ej = cudaEventRecord(ev, cs);
+  if (ej == cudaSuccess) ej = cudaStreamWaitEvent(st, ev, 0);
+  cudaFreeAsync(d, st);
+  const cudaError_t es = cudaStreamSynchronize(st);
+  if (rc) return rc;
+  if (ej != cudaSuccess) return fail_with(SF_ECUDA, "copy stream join: %s", cudaGetErrorString(ej));
+  if (es != cudaSuccess) return fail_with(SF_ECUDA, "stream sync: %s", cudaGetErrorString(es));
   return SF_OK;
 }
 

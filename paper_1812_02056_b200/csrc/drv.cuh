@@ -75,6 +75,19 @@ inline int chol_leaf_width() {
   return w;
 }
 
+// One-launch 64-wide panels (panel64.cu).  LU: on by default (SF_LU_P64=0 -> the 32-wide
+// leaf recursion).  Cholesky: for panels whose height m is at most SF_CHOL_P64_MAXM (the
+// fused leaf doubles the SIMT flops of the rows below — the 32-wide recursion moves half of
+// them to the tensor cores — so it pays only where launch latency dominates).
+inline bool lu_p64_on() {
+  static const int on = [] { const char* e = getenv("SF_LU_P64"); return e ? atoi(e) : 1; }();
+  return on != 0;
+}
+inline int64_t chol_p64_maxm() {
+  static const int64_t v = [] { const char* e = getenv("SF_CHOL_P64_MAXM"); return e ? (int64_t)atoll(e) : (int64_t)0; }();
+  return v;
+}
+
 inline int64_t half_of(int64_t w, int leaf) {
   int64_t h = (w / 2 + leaf - 1) / leaf * leaf;
   if (h >= w) h = w - leaf;
@@ -83,15 +96,24 @@ inline int64_t half_of(int64_t w, int leaf) {
 }
 
 // ------------------------------------------------------------------ workspace
+// Stream-ordered scratch, freed on `st` when the driver returns — on every path, including
+// an error return in the middle of the factorization: streams registered with join() (the
+// lookahead side stream, the QR early-R stream) are joined into `st` first, so no kernel
+// still queued there can touch the freed block.
 struct Workspace {
   char* base = nullptr;
   size_t off = 0, cap = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t joins[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaError_t init(size_t bytes, cudaStream_t s) {
     st = s;
     cap = bytes;
     keep_pool();
     return cudaMallocAsync((void**)&base, bytes, s);
+  }
+  void join(cudaStream_t s) {
+    for (auto& j : joins)
+      if (!j || j == s) { j = s; return; }
   }
   // keep freed workspace in the device's stream-ordered pool (the default release
   // threshold of 0 would unmap it at every synchronization and remap it next call)
@@ -114,7 +136,17 @@ struct Workspace {
     return p;
   }
   ~Workspace() {
-    if (base) cudaFreeAsync(base, st);
+    if (!base) return;
+    for (cudaStream_t j : joins) {
+      if (!j || j == st) continue;
+      cudaEvent_t e;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) {
+        cudaEventRecord(e, j);
+        cudaStreamWaitEvent(st, e, 0);
+        cudaEventDestroy(e);
+      }
+    }
+    cudaFreeAsync(base, st);
   }
 };
 
@@ -408,8 +440,11 @@ inline int flush_ctas_for_panel(double flush_flops) {
 template <typename T>
 inline cudaError_t chol_panel_rec(int64_t m, int64_t w, const T* src, int64_t lds, T* dst, int64_t ldd,
                                   int64_t col0, long long* fail, cudaStream_t st) {
-  const int leaf = chol_leaf_width();
-  if (w <= leaf) return chol_leaf<T>(m, (int)w, src, lds, dst, ldd, col0, fail, st);
+  const bool p64 = m <= chol_p64_maxm();
+  const int leaf = p64 ? 64 : chol_leaf_width();
+  if (w <= leaf)
+    return p64 ? chol_panel64<T>(m, (int)w, src, lds, dst, ldd, col0, fail, st)
+               : chol_leaf<T>(m, (int)w, src, lds, dst, ldd, col0, fail, st);
   const int64_t h = half_of(w, leaf);
   cudaError_t e = chol_panel_rec<T>(m, h, src, lds, dst, ldd, col0, fail, st);
   if (e != cudaSuccess) return e;
@@ -440,8 +475,11 @@ inline cudaError_t syrk_tf32(int64_t M, int64_t N, int64_t K, const SplitBuf& a,
 // for the flush.
 inline cudaError_t chol_panel_rec_f32(int64_t m, int64_t w, const float* src, int64_t lds, float* dst, int64_t ldd,
                                       int64_t col0, SplitBuf sb, long long* fail, cudaStream_t st) {
-  const int leaf = chol_leaf_width();
-  if (w <= leaf) return chol_leaf<float>(m, (int)w, src, lds, dst, ldd, col0, fail, st);
+  const bool p64 = m <= chol_p64_maxm();
+  const int leaf = p64 ? 64 : chol_leaf_width();
+  if (w <= leaf)
+    return p64 ? chol_panel64<float>(m, (int)w, src, lds, dst, ldd, col0, fail, st)
+               : chol_leaf<float>(m, (int)w, src, lds, dst, ldd, col0, fail, st);
   const int64_t h = half_of(w, leaf);
   cudaError_t e = chol_panel_rec_f32(m, h, src, lds, dst, ldd, col0, sb, fail, st);
   if (e != cudaSuccess) return e;
@@ -458,8 +496,11 @@ inline cudaError_t chol_panel_rec_f32(int64_t m, int64_t w, const float* src, in
 template <typename T>
 inline cudaError_t lu_panel_rec(int64_t m, int64_t w, int64_t ncr, const T* src, int64_t lds, T* dst, int64_t ldd,
                                 int64_t col0, const T* tol, long long* fail, cudaStream_t st) {
-  const int leaf = leaf_width();
-  if (w <= leaf) return lu_leaf<T>(m, ncr, (int)w, src, lds, dst, ldd, col0, tol, fail, st);
+  const bool p64 = lu_p64_on();
+  const int leaf = p64 ? 64 : leaf_width();
+  if (w <= leaf)
+    return p64 ? lu_panel64<T>(m, ncr, (int)w, src, lds, dst, ldd, col0, tol, fail, st)
+               : lu_leaf<T>(m, ncr, (int)w, src, lds, dst, ldd, col0, tol, fail, st);
   const int64_t h = half_of(w, leaf);
   cudaError_t e = lu_panel_rec<T>(m, h, ncr + (w - h), src, lds, dst, ldd, col0, tol, fail, st);
   if (e != cudaSuccess) return e;

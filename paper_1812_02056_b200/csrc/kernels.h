@@ -89,6 +89,21 @@ template <typename T>
 cudaError_t lu_leaf(int64_t m, int64_t ncols_right, int w, const T* src, int64_t lds, T* dst,
                     int64_t ldd, int64_t col0, const T* tol, long long* fail, cudaStream_t st);
 
+// Per-device chaining of persistent MGS grids across streams (panels.cu MgsOrder), for
+// whole replayed QR graphs: wait before the launch, record after it.
+void mgs_order_before(cudaStream_t st);
+void mgs_order_after(cudaStream_t st);
+
+// A whole panel of width w <= 64 in one launch (panel64.cu): LU — the diagonal block, the L
+// rows below it and the U columns right of it (ncr columns); Cholesky — the diagonal block
+// and the L rows below it.  Same arguments as lu_leaf / chol_leaf.
+template <typename T>
+cudaError_t lu_panel64(int64_t m, int64_t ncr, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
+                       const T* tol, long long* fail, cudaStream_t st);
+template <typename T>
+cudaError_t chol_panel64(int64_t m, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
+                         long long* fail, cudaStream_t st);
+
 // LU U rows only, against an already factored diagonal block L11 (ldl): the U part of
 // lu_leaf for ncols columns (block-cyclic distributed LU).
 template <typename T>
