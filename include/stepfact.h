@@ -179,6 +179,11 @@ int sf_comm_init(sf_comm_t* comm, int nranks, int rank, const uint8_t id[128]); 
 int sf_comm_init_loopback(sf_comm_t* comm, int nranks);
 int sf_comm_destroy(sf_comm_t comm);
 int sf_comm_size(sf_comm_t comm);
+/* Payload bytes of every panel message this communicator has broadcast so far (cumulative):
+ * panel p of a Cholesky / LU run sends rows [p*s, n) of its w columns, packed ((n - p*s) * w
+ * elements; the last panel, never flushed, is not sent); QR sends whole Q panels (n * w).
+ * -1 for a NULL comm. */
+int64_t sf_comm_bcast_bytes(sf_comm_t comm);
 int sf_comm_local_ranks(sf_comm_t comm);
 int64_t sf_local_cols(int64_t n, int64_t s, int nranks, int rank);
 
@@ -221,11 +226,12 @@ int64_t sf_launch_counter(void);
 
 /* Profiling hook.  sf_profile_enable(1) makes the drivers record a CUDA event pair on the
  * factorization stream around every flush (kind 0: the trailing-update kernel launches),
- * every panel (kind 1) and QR's R := Q^T A (kind 2).  sf_profile_collect synchronizes on
- * the recorded events and returns, per kind, total device milliseconds, number of
+ * every panel (kind 1), QR's R := Q^T A (kind 2) and, in the distributed drivers, every
+ * NCCL panel broadcast on the rank's comm stream (kind 3).  sf_profile_collect synchronizes
+ * on the recorded events and returns, per kind, total device milliseconds, number of
  * bracketed regions and the algorithmic flops they performed (SURVEY.md §8(d) formulas:
- * Cholesky flush s*m*(m+1), LU flush 2*s*m^2, QR flush 4*n*s*m, R n^2*(n+1));
- * arrays of length 3; then it clears the record.  Not for use during graph capture. */
+ * Cholesky flush s*m*(m+1), LU flush 2*s*m^2, QR flush 4*n*s*m, R n^2*(n+1); kind 3:
+ * bytes); arrays of length 4; then it clears the record.  Not for use during graph capture. */
 void sf_profile_enable(int on);
 int sf_profile_collect(double* ms, int64_t* count, double* flops);
 

@@ -87,6 +87,8 @@ def lib():
         f = getattr(L, name)
         f.argtypes = args
         f.restype = i32
+    L.sf_comm_bcast_bytes.argtypes = [p]
+    L.sf_comm_bcast_bytes.restype = i64
     L.sf_local_cols.argtypes = [i64, i64, i32, i32]
     L.sf_local_cols.restype = i64
     L.sf_flush_count.argtypes = [i64, i64]
@@ -116,7 +118,7 @@ EXPORTS = ("chol_factor", "lu_factor", "qr_factor", "chol_factor_host", "lu_fact
            "sf_profile_collect", "sf_get_unique_id", "sf_comm_init", "sf_comm_init_loopback", "sf_comm_destroy",
            "sf_comm_size", "sf_comm_local_ranks", "sf_local_cols", "chol_factor_dist", "lu_factor_dist",
            "qr_factor_dist", "chol_factor_steps", "lu_factor_steps", "qr_factor_steps", "chol_solve", "lu_solve",
-           "qr_solve", "sf_set_strassen", "sf_schedule")
+           "qr_solve", "sf_set_strassen", "sf_schedule", "sf_comm_bcast_bytes")
 
 
 def _check(rc):
@@ -176,10 +178,11 @@ def profile_enable(on=True):
 
 
 def profile_collect():
-    """{kind: (ms, count, flops)} for kinds 'update', 'panel', 'qr_r' since the last collect."""
-    ms = (ctypes.c_double * 3)(); cnt = (ctypes.c_int64 * 3)(); fl = (ctypes.c_double * 3)()
+    """{kind: (ms, count, flops)} for kinds 'update', 'panel', 'qr_r', 'bcast' (flops = bytes)
+    since the last collect."""
+    ms = (ctypes.c_double * 4)(); cnt = (ctypes.c_int64 * 4)(); fl = (ctypes.c_double * 4)()
     _check(lib().sf_profile_collect(ctypes.addressof(ms), ctypes.addressof(cnt), ctypes.addressof(fl)))
-    return {k: (ms[i], cnt[i], fl[i]) for i, k in enumerate(("update", "panel", "qr_r"))}
+    return {k: (ms[i], cnt[i], fl[i]) for i, k in enumerate(("update", "panel", "qr_r", "bcast"))}
 
 
 # ----------------------------------------------------------------------- raw column-major API
@@ -394,6 +397,10 @@ class Comm:
         h = ctypes.c_void_p()
         _check(lib().sf_comm_init_loopback(ctypes.byref(h), nranks))
         return cls(h, nranks, list(range(nranks)))
+
+    def bcast_bytes(self):
+        """Payload bytes of the panel messages this communicator has broadcast so far."""
+        return int(lib().sf_comm_bcast_bytes(self.handle))
 
     def destroy(self):
         if self.handle is not None:

@@ -41,6 +41,7 @@ struct sf_comm_ {
   int rank = 0;        // ignored for loopback
   int device = 0;
   ncclComm_t nccl = nullptr;
+  int64_t bcast_bytes = 0;   // payload of every panel message sent so far (sf_comm_bcast_bytes)
   bool loopback() const { return nccl == nullptr; }
   int nlocal() const { return loopback() ? nranks : 1; }
   int local_rank(int i) const { return loopback() ? i : rank; }
@@ -200,6 +201,7 @@ static cudaError_t wait_on(cudaStream_t waiter, cudaEvent_t ev) { return cudaStr
 template <typename T, typename DstF, typename FreeF>
 static int exchange(sf_comm_t comm, std::vector<Rank<T>>& rk, int64_t p, int owner, size_t count, DstF dst,
                     FreeF free_ev) {
+  comm->bcast_bytes += (int64_t)(count * sizeof(T));
   if (!comm->loopback()) {
     Rank<T>& me = rk[0];
     if (me.r == owner) SF_CUDA(wait_on(me.st.com, me.ready[p]));
@@ -207,6 +209,7 @@ static int exchange(sf_comm_t comm, std::vector<Rank<T>>& rk, int64_t p, int own
     static const bool skip1 = getenv("SF_DIST_SKIP1") && atoi(getenv("SF_DIST_SKIP1"));
     if (!(skip1 && comm->nranks == 1)) {
       T* b = dst(me);
+      ProfScope pb(3, (double)(count * sizeof(T)), me.st.com);
       SF_NCCL(ncclBroadcast(b, b, count, nccl_type<T>(), owner, comm->nccl, me.st.com));
       count_launch();
     }
@@ -362,16 +365,27 @@ static cudaError_t chol_panel_any(Rank<float>& x, int64_t m, int64_t w, const fl
   return chol_panel_rec_f32(m, w, src, lds, dst, ldd, col0, x.sb_pan, x.fail, st);
 }
 
-// Panel p as broadcast: the contiguous span of the owner's local storage from (ps, first
-// column of the panel) to (n-1, last column) — the panel's rows [ps, n) with ld = ld_local,
-// plus rows [0, ps) of its later columns (strict upper: never written, harmless).  No pack:
-// the owner broadcasts in place from its factor, receivers get the same layout (ld = ld).
+// Panel p as broadcast: rows [ps, n) of its w columns, packed (ld = n - ps) into the rank's
+// receive buffer buf[p & 1] — on the owner by one strided device copy right after the panel
+// is factored, on the others by the broadcast.  Rows [0, ps) are never sent: an in-place
+// broadcast of the owner's storage would move the contiguous span from (ps, first column)
+// to (n-1, last column), about twice the bytes (n*w instead of (n - ps)*w).  Every rank,
+// the owner included, then flushes from the packed copy (same operations, only the operand
+// leading dimension differs: results bitwise equal).
 template <typename T>
 struct Span {
   const Cyclic& cy; int64_t ld;
-  T* owner_ptr(Rank<T>& x, int64_t p) const { return x.X + p * cy.s + cy.slot(p) * cy.s * ld; }
-  size_t count(int64_t p) const { return (size_t)((cy.width(p) - 1) * ld + (cy.n - p * cy.s)); }
-  T* at(Rank<T>& x, int64_t p) const { return x.r == cy.owner(p) ? owner_ptr(x, p) : x.buf[p & 1]; }
+  int64_t ldp(int64_t p) const { return cy.n - p * cy.s; }
+  size_t count(int64_t p) const { return (size_t)ldp(p) * (size_t)cy.width(p); }
+  T* at(Rank<T>& x, int64_t p) const { return x.buf[p & 1]; }
+  // owner: copy the factored panel into its packed buffer; `prev` = the buffer's last reader
+  int pack(Rank<T>& x, int64_t p, cudaEvent_t prev, cudaStream_t st) const {
+    if (prev) SF_CUDA(cudaStreamWaitEvent(st, prev, 0));
+    const T* src = x.X + p * cy.s + cy.slot(p) * cy.s * ld;
+    SF_CUDA(cudaMemcpy2DAsync(at(x, p), sizeof(T) * ldp(p), src, sizeof(T) * ld, sizeof(T) * ldp(p), cy.width(p),
+                              cudaMemcpyDeviceToDevice, st));
+    return SF_OK;
+  }
 };
 
 template <typename T>
@@ -395,20 +409,23 @@ static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, 
   // prologue: panel 0 on its owner, out of place from A
   for (auto& o : rk) {
     if (o.r != 0) continue;
-    ProfScope ps(1, 0.0, o.st.pan);
-    SF_CUDA(chol_panel_any(o, n, cy.width(0), o.A, ld, o.X, ld, 0, o.st.pan));
+    {
+      ProfScope ps(1, 0.0, o.st.pan);
+      SF_CUDA(chol_panel_any(o, n, cy.width(0), o.A, ld, o.X, ld, 0, o.st.pan));
+    }
+    if (cy.P > 1) { rc = sp.pack(o, 0, nullptr, o.st.pan); if (rc) return rc; }
     SF_CUDA(cudaEventRecord(o.ready[0], o.st.pan));
   }
-  for (int64_t p = 0; p < cy.P; ++p) {
+  for (int64_t p = 0; p + 1 < cy.P; ++p) {   // the last panel is never flushed: not sent
     rc = exchange<T>(comm, rk, p, cy.owner(p), sp.count(p), [&](Rank<T>& x) { return sp.at(x, p); },
                      [&](Rank<T>& x) -> cudaEvent_t { return p >= 2 ? x.done[p - 2] : nullptr; });
     if (rc) return rc;
-    if (p + 1 == cy.P) break;   // the last panel is never flushed
     for (auto& x : rk) {
       SF_CUDA(wait_on(x.st.mn, x.recv[p]));
       const T* Lp = sp.at(x, p);
+      const int64_t ldp = sp.ldp(p);
       const int64_t nslots = (cy.local_cols(x.r) + s - 1) / s;
-      SF_CUDA(chol_split_panel(cy, x, p, Lp, ld, x.st.mn));
+      SF_CUDA(chol_split_panel(cy, x, p, Lp, ldp, x.st.mn));
       int64_t j0 = cy.first_slot_after(p, x.r);
       if (cy.owner(p + 1) == x.r) {
         // lookahead: flush into panel p+1 first, factor it while the rest of the flush runs
@@ -416,7 +433,7 @@ static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, 
         {
           double fl = 0.0;
           ProfScope pf(0, 0.0, x.st.mn);
-          SF_CUDA(chol_update_slots(cy, x, p, j, j + 1, Lp, ld, ld, &fl, x.st.mn));
+          SF_CUDA(chol_update_slots(cy, x, p, j, j + 1, Lp, ldp, ld, &fl, x.st.mn));
           pf.r.flops = fl;
         }
         j0 = j + 1;
@@ -427,12 +444,13 @@ static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, 
           T* P0 = x.X + qs + j * s * ld;
           SF_CUDA(chol_panel_any(x, n - qs, wq, P0, ld, P0, ld, qs, x.st.pan));
         }
+        if (q + 1 < cy.P) { rc = sp.pack(x, q, q >= 2 ? x.done[q - 2] : nullptr, x.st.pan); if (rc) return rc; }
         SF_CUDA(cudaEventRecord(x.ready[q], x.st.pan));
       }
       {
         double fl = 0.0;
         ProfScope pf(0, 0.0, x.st.mn);
-        SF_CUDA(chol_update_slots(cy, x, p, j0, nslots, Lp, ld, ld, &fl, x.st.mn));
+        SF_CUDA(chol_update_slots(cy, x, p, j0, nslots, Lp, ldp, ld, &fl, x.st.mn));
         pf.r.flops = fl;
       }
       SF_CUDA(cudaEventRecord(x.done[p], x.st.mn));
@@ -478,18 +496,21 @@ static int lu_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, vo
   const Span<T> sp{cy, ld};   // the L panel incl. U11 in its diagonal block
   for (auto& o : rk) {
     if (o.r != 0) continue;
-    ProfScope ps(1, 0.0, o.st.pan);
-    SF_CUDA(lu_panel_rec<T>(n, cy.width(0), 0, o.X, ld, o.X, ld, 0, o.tol, o.fail, o.st.pan));
+    {
+      ProfScope ps(1, 0.0, o.st.pan);
+      SF_CUDA(lu_panel_rec<T>(n, cy.width(0), 0, o.X, ld, o.X, ld, 0, o.tol, o.fail, o.st.pan));
+    }
+    if (cy.P > 1) { rc = sp.pack(o, 0, nullptr, o.st.pan); if (rc) return rc; }
     SF_CUDA(cudaEventRecord(o.ready[0], o.st.pan));
   }
-  for (int64_t p = 0; p < cy.P; ++p) {
+  for (int64_t p = 0; p + 1 < cy.P; ++p) {   // the last panel is never flushed: not sent
     rc = exchange<T>(comm, rk, p, cy.owner(p), sp.count(p), [&](Rank<T>& x) { return sp.at(x, p); },
                      [&](Rank<T>& x) -> cudaEvent_t { return p >= 2 ? x.done[p - 2] : nullptr; });
     if (rc) return rc;
-    if (p + 1 == cy.P) break;
     for (auto& x : rk) {
       SF_CUDA(wait_on(x.st.mn, x.recv[p]));
       const T* Lp = sp.at(x, p);
+      const int64_t ldp = sp.ldp(p);
       const int64_t nloc = cy.local_cols(x.r);
       int64_t c0 = cy.first_slot_after(p, x.r) * s;
       if (cy.owner(p + 1) == x.r) {
@@ -497,7 +518,7 @@ static int lu_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, vo
         {
           double fl = 0.0;
           ProfScope pf(0, 0.0, x.st.mn);
-          SF_CUDA(lu_update_cols<T>(cy, x, p, j * s, j * s + wq, Lp, ld, ld, &fl, x.st.mn));
+          SF_CUDA(lu_update_cols<T>(cy, x, p, j * s, j * s + wq, Lp, ldp, ld, &fl, x.st.mn));
           pf.r.flops = fl;
         }
         c0 = j * s + wq;
@@ -508,12 +529,13 @@ static int lu_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, vo
           T* P0 = x.X + qs + j * s * ld;
           SF_CUDA(lu_panel_rec<T>(n - qs, wq, 0, P0, ld, P0, ld, qs, x.tol, x.fail, x.st.pan));
         }
+        if (q + 1 < cy.P) { rc = sp.pack(x, q, q >= 2 ? x.done[q - 2] : nullptr, x.st.pan); if (rc) return rc; }
         SF_CUDA(cudaEventRecord(x.ready[q], x.st.pan));
       }
       {
         double fl = 0.0;
         ProfScope pf(0, 0.0, x.st.mn);
-        SF_CUDA(lu_update_cols<T>(cy, x, p, c0, nloc, Lp, ld, ld, &fl, x.st.mn));
+        SF_CUDA(lu_update_cols<T>(cy, x, p, c0, nloc, Lp, ldp, ld, &fl, x.st.mn));
         pf.r.flops = fl;
       }
       SF_CUDA(cudaEventRecord(x.done[p], x.st.mn));
@@ -703,6 +725,7 @@ int sf_comm_destroy(sf_comm_t comm) {
 }
 
 int sf_comm_size(sf_comm_t comm) { return comm ? comm->nranks : 0; }
+int64_t sf_comm_bcast_bytes(sf_comm_t comm) { return comm ? comm->bcast_bytes : -1; }
 int sf_comm_local_ranks(sf_comm_t comm) { return comm ? comm->nlocal() : 0; }
 
 int64_t sf_local_cols(int64_t n, int64_t s, int nranks, int rank) {

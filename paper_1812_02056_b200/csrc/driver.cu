@@ -964,9 +964,10 @@ void sf_profile_enable(int on) {
 
 int sf_profile_collect(double* ms, int64_t* count, double* flops) {
   SF_API_LOCK;
-  for (int k = 0; k < 3; ++k) { ms[k] = 0.0; count[k] = 0; flops[k] = 0.0; }
+  for (int k = 0; k < 4; ++k) { ms[k] = 0.0; count[k] = 0; flops[k] = 0.0; }
   int rc = SF_OK;
   for (auto& r : g_prof_recs) {
+    if (r.kind < 0 || r.kind > 3) continue;
     float t = 0.f;
     cudaError_t e = cudaEventSynchronize(r.b);
     if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);

@@ -62,14 +62,12 @@ inline int leaf_width() {
   return w;
 }
 
-// Cholesky leaf width: 32 (default) or 64 (chol_leaf_warp_kernel<T, 64>: one launch instead
-// of two 32-wide leaves and the GEMM between them — measured slower: its 64-step diagonal
-// Crout and 168-register substitution cost more than they save).  SF_CHOL_LEAF = 16/32/64.
+// Cholesky leaf width of the recursive panel: 32 (default) or 16 (SF_CHOL_LEAF).
 inline int chol_leaf_width() {
   static int w = [] {
     const char* e = getenv("SF_CHOL_LEAF");
     int v = e ? atoi(e) : 32;
-    if (v != 16 && v != 32 && v != 64) v = 32;
+    if (v != 16 && v != 32) v = 32;
     return v;
   }();
   return w;
@@ -557,8 +555,9 @@ inline cudaError_t trsm_upper_rec(int64_t w, int64_t ncols, const T* t, int64_t 
 
 // ------------------------------------------------------------------ QR
 inline int splitk_for(int64_t M, int64_t N, int64_t K) {
-  const int64_t tiles = ((M + 127) / 128) * ((N + 63) / 64);   // gemm_f64 CTA tile 128 x 64, 2 CTAs/SM
-  int64_t sp = (4 * 148 + tiles - 1) / tiles;
+  // long-K products run on the 64 x 64 DMMA tiles, 4 CTAs per SM: aim at two waves
+  const int64_t tiles = ((M + 63) / 64) * ((N + 63) / 64);
+  int64_t sp = (8 * 148 + tiles - 1) / tiles;
   const int64_t maxsp = K / 256 > 1 ? K / 256 : 1;
   if (sp > maxsp) sp = maxsp;
   if (sp > 16) sp = 16;
@@ -591,7 +590,7 @@ inline cudaError_t qr_panel(int64_t n, int64_t w, const T* src, int64_t lds, T* 
   const int64_t wmax = qr_mgs_max_width(n, (int)sizeof(T));
   if (w <= wmax) return qr_mgs_panel<T>(n, (int)w, src, lds, dst, ldd, col0, tol, mgswork, fail, st);
   // panel wider than one cooperative MGS launch holds: chunks, projected against the
-  // finished chunks of the same panel ("wide QR panels")
+  // finished chunks of the same panel (DESIGN.md §3 reading R12)
   for (int64_t z0 = 0; z0 < w; z0 += wmax) {
     const int64_t wc = (wmax < w - z0) ? wmax : w - z0;
     const T* vin = src + z0 * lds;

@@ -560,6 +560,15 @@ __global__ void splitk_reduce_f64(GemmF64 p) {
   }
 }
 
+static cudaError_t splitk_reduce(const GemmF64& p, cudaStream_t st) {
+  const int64_t total = p.M * p.N;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  splitk_reduce_f64<<<blocks, 256, 0, st>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
 static bool short_k_wide() {
   static const int on = [] { const char* e = getenv("SF_GEMM_SHORTK8"); return e ? atoi(e) : 1; }();
   return on != 0;
@@ -707,18 +716,21 @@ cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStre
   if (p.splits < 1) p.splits = 1;
   {
     const int var = dmma_variant_for(p.K);
-    if (var > 0 && p.max_ctas == 0 && p.splits == 1 && p.K > 0) {
+    if (var > 0 && p.max_ctas == 0 && p.K > 0) {
       const bool v16 = aligned16(p.A, p.lda) && aligned16(p.B, p.ldb);
       const int vecC = aligned16(p.C, p.ldc) && (!p.beta || aligned16(p.Cin, p.ldcin));
-      const int bulk = dmma_bulk() && p.beta && vecC && p.Cin == p.C && p.ldcin == p.ldc;
+      const int bulk = dmma_bulk() && p.splits == 1 && p.beta && vecC && p.Cin == p.C && p.ldcin == p.ldc;
+      cudaError_t e;
       switch (var) {
-        case 1: return launch_v2<128, 2, true>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st);
-        case 2: return launch_v2<96, 3, true>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st);
-        case 3: return launch_v2<96, 3, false>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st);
-        case 5: return launch_v2<64, 4, false>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st);
-        case 6: return launch_v2<64, 4, true>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st);
-        default: return launch_v2<128, 2, false>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st);
+        case 1: e = launch_v2<128, 2, true>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st); break;
+        case 2: e = launch_v2<96, 3, true>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st); break;
+        case 3: e = launch_v2<96, 3, false>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st); break;
+        case 5: e = launch_v2<64, 4, false>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st); break;
+        case 6: e = launch_v2<64, 4, true>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st); break;
+        default: e = launch_v2<128, 2, false>(p, a_kcontig, b_kcontig, v16, mask, vecC, bulk, st); break;
       }
+      if (e != cudaSuccess || p.splits == 1) return e;
+      return splitk_reduce(p, st);
     }
   }
   const int TM = (int)((p.M + g64::BM - 1) / g64::BM), TN = (int)((p.N + g64::BN - 1) / g64::BN);
@@ -730,12 +742,7 @@ cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStre
   const int vecC = aligned16(p.C, p.ldc) && (!p.beta || aligned16(p.Cin, p.ldcin));
   cudaError_t e = launch_key(p, nullptr, a_kcontig, b_kcontig, v16, mask, ntiles, vecC, st);
   if (e != cudaSuccess || p.splits == 1) return e;
-  const int64_t total = p.M * p.N;
-  int blocks = (int)((total + 255) / 256);
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  splitk_reduce_f64<<<blocks, 256, 0, st>>>(p);
-  count_launch();
-  return cudaGetLastError();
+  return splitk_reduce(p, st);
 }
 
 cudaError_t gemm_f64_grouped(GemmF64 p, const GemmGroup* groups, int count, int a_kcontig, int b_kcontig, int mask,

@@ -54,177 +54,7 @@ __device__ __forceinline__ bool last_reader(long long* counter) {
 }
 
 // ------------------------------------------------------------------ Cholesky
-template <typename T, int W>
-__global__ void __launch_bounds__(kLeafT) chol_leaf_kernel(int64_t m, int w, const T* __restrict__ src, int64_t lds,
-                                                           T* __restrict__ dst, int64_t ldd, int64_t col0,
-                                                           long long* fail) {
-  if (failed(fail)) return;
-  __shared__ T Ls[W][W + 1];
-  __shared__ T inv[W];
-  __shared__ int bad;
-  const int tid = threadIdx.x, lane = tid & 31;
-  // Diagonal block: Crout in shared memory, all threads, rolled loops (small code: the
-  // kernel runs once per CTA, so instruction fetch dominates any fully unrolled variant).
-  // Column c: thread (row i = c + tid/4, part = tid%4) sums k = part, part+4, ... < c.
-  for (int idx = tid; idx < W * W; idx += kLeafT) {
-    const int i = idx % W, k = idx / W;
-    Ls[i][k] = (i < w && k <= i) ? __ldcg(src + i + (int64_t)k * lds) : T(0);
-  }
-  if (tid == 0) bad = 0;
-  __syncthreads();
-  {
-    const int part = tid & 3;
-    for (int c = 0; c < w; ++c) {
-      const int i = c + (tid >> 2);
-      T s = T(0);
-      if (i < w)
-        for (int k = part; k < c; k += 4) s = fma(Ls[i][k], Ls[c][k], s);
-      s += __shfl_xor_sync(kFull, s, 1);
-      s += __shfl_xor_sync(kFull, s, 2);
-      const T t = (i < w) ? Ls[i][c] - s : T(0);
-      if (i == c && part == 0) {
-        if (!(t > T(0))) {
-          bad = 1;
-          if (blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
-        } else {
-          const T Lcc = leaf_sqrt(t);
-          Ls[c][c] = Lcc;
-          inv[c] = T(1) / Lcc;
-        }
-      }
-      __syncthreads();
-      if (bad) return;
-      if (i > c && i < w && part == 0) Ls[i][c] = t / Ls[c][c];
-      __syncthreads();
-    }
-  }
-  // The diagonal block is read by every CTA (redundant factorization) and may be
-  // overwritten in place: the LAST CTA to have read it writes the result out.
-  if (last_reader(fail + 1)) {
-    for (int idx = tid; idx < w * w; idx += kLeafT) {
-      const int i = idx % w, k = idx / w;
-      if (k <= i) dst[i + (int64_t)k * ldd] = Ls[i][k];
-    }
-  }
-  const int64_t r = w + (int64_t)blockIdx.x * kLeafT + tid;
-  if (r >= m) return;
-  T x[W];
-#pragma unroll
-  for (int k = 0; k < W; ++k) x[k] = (k < w) ? __ldcg(src + r + (int64_t)k * lds) : T(0);
-#pragma unroll
-  for (int c = 0; c < W; ++c) {
-    T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
-#pragma unroll
-    for (int k = 0; k < c; ++k) {
-      if ((k & 3) == 0) a0 = fma(-x[k], Ls[c][k], a0);
-      else if ((k & 3) == 1) a1 = fma(-x[k], Ls[c][k], a1);
-      else if ((k & 3) == 2) a2 = fma(-x[k], Ls[c][k], a2);
-      else a3 = fma(-x[k], Ls[c][k], a3);
-    }
-    x[c] = ((a0 + a1) + (a2 + a3)) * inv[c];
-  }
-#pragma unroll
-  for (int k = 0; k < W; ++k)
-    if (k < w) dst[r + (int64_t)k * ldd] = x[k];
-}
-
-// Variant: ONE warp factors the diagonal block (warp-synchronous Crout in shared memory,
-// lane i = row i, no block-wide barrier per column) while the other warps already load
-// their rows below from HBM; one __syncthreads, then the substitutions.  Same arithmetic per
-// element as chol_leaf_kernel (k-sums in four interleaved partial sums, then one
-// subtraction, sqrt, division by L_cc in the block, multiplication by 1/L_cc below).
-template <typename T, int W, int NT>
-__global__ void __launch_bounds__(NT) chol_leaf_warp_kernel(int64_t m, int w, const T* __restrict__ src,
-                                                                int64_t lds, T* __restrict__ dst, int64_t ldd,
-                                                                int64_t col0, long long* fail) {
-  if (failed(fail)) return;
-  __shared__ T Ls[W][W + 1];
-  __shared__ T inv[W];
-  __shared__ int bad;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t r = w + (int64_t)blockIdx.x * NT + tid;
-  T x[W];
-  if (warp == 0) {
-    constexpr int RPL = (W + 31) / 32;   // diagonal-block rows per lane: lane + 32*rr
-#pragma unroll
-    for (int rr = 0; rr < RPL; ++rr) {
-      const int i = lane + 32 * rr;
-      if (i < W)
-        for (int k = 0; k < W; ++k) Ls[i][k] = (i < w && k <= i && k < w) ? __ldcg(src + i + (int64_t)k * lds) : T(0);
-    }
-    __syncwarp();
-    int okc = 1;
-    for (int c = 0; c < w; ++c) {
-      T tv[RPL];
-#pragma unroll
-      for (int rr = 0; rr < RPL; ++rr) {
-        const int i = lane + 32 * rr;
-        T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
-        if (i >= c && i < w) {
-          int k = 0;
-          for (; k + 3 < c; k += 4) {
-            a0 = fma(Ls[i][k], Ls[c][k], a0);
-            a1 = fma(Ls[i][k + 1], Ls[c][k + 1], a1);
-            a2 = fma(Ls[i][k + 2], Ls[c][k + 2], a2);
-            a3 = fma(Ls[i][k + 3], Ls[c][k + 3], a3);
-          }
-          for (; k < c; ++k) a0 = fma(Ls[i][k], Ls[c][k], a0);
-        }
-        tv[rr] = (i < w) ? Ls[i][c] - ((a0 + a1) + (a2 + a3)) : T(0);
-      }
-      T tc = tv[0];
-#pragma unroll
-      for (int rr = 1; rr < RPL; ++rr)
-        if ((c >> 5) == rr) tc = tv[rr];
-      const T d = __shfl_sync(kFull, tc, c & 31);
-      if (!(d > T(0))) {
-        okc = 0;
-        if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
-        break;
-      }
-      const T Lcc = leaf_sqrt(d);
-#pragma unroll
-      for (int rr = 0; rr < RPL; ++rr) {
-        const int i = lane + 32 * rr;
-        if (i == c) { Ls[c][c] = Lcc; inv[c] = T(1) / Lcc; }
-        else if (i > c && i < w) Ls[i][c] = tv[rr] / Lcc;
-      }
-      __syncwarp();
-    }
-    if (lane == 0) bad = !okc;
-  }
-  // rows below (all warps; warp 0 after the block): loads in flight during the Crout
-  if (r < m) {
-#pragma unroll
-    for (int k = 0; k < W; ++k) x[k] = (k < w) ? __ldcg(src + r + (int64_t)k * lds) : T(0);
-  }
-  __syncthreads();
-  if (bad) return;
-  if (last_reader(fail + 1)) {
-    for (int idx = tid; idx < w * w; idx += NT) {
-      const int i = idx % w, k = idx / w;
-      if (k <= i) dst[i + (int64_t)k * ldd] = Ls[i][k];
-    }
-  }
-  if (r >= m) return;
-#pragma unroll
-  for (int c = 0; c < W; ++c) {
-    T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
-#pragma unroll
-    for (int k = 0; k < c; ++k) {
-      if ((k & 3) == 0) a0 = fma(-x[k], Ls[c][k], a0);
-      else if ((k & 3) == 1) a1 = fma(-x[k], Ls[c][k], a1);
-      else if ((k & 3) == 2) a2 = fma(-x[k], Ls[c][k], a2);
-      else a3 = fma(-x[k], Ls[c][k], a3);
-    }
-    x[c] = ((a0 + a1) + (a2 + a3)) * inv[c];
-  }
-#pragma unroll
-  for (int k = 0; k < W; ++k)
-    if (k < w) dst[r + (int64_t)k * ldd] = x[k];
-}
-
-// Variant (default for W <= 32): RIGHT-looking, the paper's per-element order.  Warp 0
+// RIGHT-looking, the paper's per-element order.  Warp 0
 // holds the diagonal block in registers (lane i = row i, a[k] = running A_ik); at column c
 // lane c's a[c] is final, L_cc = sqrt(a[c]) is broadcast, every lane scales its a[c] by
 // 1/L_cc, publishes L_ic to a shared vector, and subtracts L_ic L_jc from its a[j], j > c.
@@ -305,266 +135,31 @@ __global__ void __launch_bounds__(NT) chol_leaf_rl_kernel(int64_t m, int w, cons
     if (k < w) dst[r + (int64_t)k * ldd] = x[k];
 }
 
-// Same arithmetic as chol_leaf_rl_kernel with ROLLED column loops: the registers rotate
-// (a[0] is always the current column), so a column step is one small loop body (~100
-// instructions instead of ~2.7K unrolled) — the leaf's code is fetched cold at every
-// launch between GEMMs, and ncu attributes ~30% of its stalls to instruction fetch.
-// Lr[c][j] = L_{c+1+j, c} (0 past the block): the operands of column c, 16-byte aligned.
-template <typename T, int W, int NT>
-__global__ void __launch_bounds__(NT) chol_leaf_rot_kernel(int64_t m, int w, const T* __restrict__ src,
-                                                               int64_t lds, T* __restrict__ dst, int64_t ldd,
-                                                               int64_t col0, long long* fail) {
-  static_assert(W <= 32, "one row per lane");
-  if (failed(fail)) return;
-  __shared__ __align__(16) T Lr[W][W];
-  __shared__ T inv[W];
-  __shared__ T Ld[W][W + 1];
-  __shared__ int bad;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t r = w + (int64_t)blockIdx.x * NT + tid;
-  if (warp == 0) {
-    T a[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) a[k] = (lane < w && k <= lane && k < w) ? __ldcg(src + lane + (int64_t)k * lds) : T(0);
-    int okc = 1;
-#pragma unroll 1
-    for (int c = 0; c < w; ++c) {
-      const T d = __shfl_sync(kFull, a[0], c);     // a[0] = column c of my row
-      if (!(d > T(0))) {
-        okc = 0;
-        if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
-        break;
-      }
-      const T Lcc = leaf_sqrt(d);
-      const T ri = T(1) / Lcc;
-      const T l = (lane == c) ? Lcc : a[0] * ri;
-      if (lane < W) {
-        Ld[lane][c] = (lane >= c) ? l : T(0);
-        Lr[c][lane] = T(0);
-      }
-      __syncwarp();
-      if (lane > c && lane < W) Lr[c][lane - c - 1] = l;
-      if (lane == c) inv[c] = ri;
-      __syncwarp();
-      const T* v = &Lr[c][0];
-#pragma unroll
-      for (int j = 1; j < W; ++j) a[j - 1] = fma(-l, v[j - 1], a[j]);
-      a[W - 1] = T(0);
-    }
-    if (lane == 0) bad = !okc;
-  }
-  T x[W];
-  if (r < m) {
-#pragma unroll
-    for (int k = 0; k < W; ++k) x[k] = (k < w) ? __ldcg(src + r + (int64_t)k * lds) : T(0);
-  }
-  __syncthreads();
-  if (bad) return;
-  if (last_reader(fail + 1)) {
-    for (int idx = tid; idx < w * w; idx += NT) {
-      const int i = idx % w, k = idx / w;
-      if (k <= i) dst[i + (int64_t)k * ldd] = Ld[i][k];
-    }
-  }
-  if (r >= m) return;
-#pragma unroll 1
-  for (int c = 0; c < w; ++c) {
-    const T xc = x[0] * inv[c];
-    dst[r + (int64_t)c * ldd] = xc;
-    const T* v = &Lr[c][0];
-#pragma unroll
-    for (int j = 1; j < W; ++j) x[j - 1] = fma(-xc, v[j - 1], x[j]);
-    x[W - 1] = T(0);
-  }
-}
-
-static bool leaf_rot_on() {
-  static int on = [] { const char* e = getenv("SF_LEAF_ROT"); return e ? atoi(e) : 0; }();
-  return on != 0;
-}
-
-static bool leaf_rl_on() {
-  static int on = [] { const char* e = getenv("SF_LEAF_RL"); return e ? atoi(e) : 1; }();
-  return on != 0;
-}
-
-static bool leaf_warp_on() {
-  static int on = [] { const char* e = getenv("SF_LEAF_WARP"); return e ? atoi(e) : 1; }();
-  return on != 0;
-}
-
 template <typename T>
 cudaError_t chol_leaf(int64_t m, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
                       long long* fail, cudaStream_t st) {
   if (w <= 0 || m <= 0) return cudaSuccess;
   const int64_t below = m - w;
   const int grid = below > 0 ? (int)((below + kLeafT - 1) / kLeafT) : 1;
-  if (leaf_rot_on() && w <= 32) {
-    if (w <= 16) chol_leaf_rot_kernel<T, 16, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-    else chol_leaf_rot_kernel<T, 32, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-    count_launch();
-    return cudaGetLastError();
-  }
-  if (leaf_rl_on() && w <= 32) {
-    if (w <= 16) chol_leaf_rl_kernel<T, 16, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-    else chol_leaf_rl_kernel<T, 32, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-    count_launch();
-    return cudaGetLastError();
-  }
-  if (leaf_warp_on()) {
-    // SF_LEAF_NT=64: 64-thread CTAs (~6.4K registers) fit on an SM next to two flush CTAs, so
-    // the lookahead panel's leaves need not wait for flush CTAs to retire — measured no
-    // faster (cfg3 61.4 vs 61.5 ms), default 128
-    static const int nt = [] { const char* e = getenv("SF_LEAF_NT"); return (e && atoi(e) == 64) ? 64 : 128; }();
-    if (nt == 64) {
-      const int g64 = below > 0 ? (int)((below + 63) / 64) : 1;
-      if (w <= 16) chol_leaf_warp_kernel<T, 16, 64><<<g64, 64, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-      else if (w <= 32) chol_leaf_warp_kernel<T, 32, 64><<<g64, 64, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-      else if (w <= 64) chol_leaf_warp_kernel<T, 64, 64><<<g64, 64, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-      else return cudaErrorInvalidValue;
-    } else {
-      if (w <= 16) chol_leaf_warp_kernel<T, 16, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-      else if (w <= 32) chol_leaf_warp_kernel<T, 32, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-      else if (w <= 64) chol_leaf_warp_kernel<T, 64, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-      else return cudaErrorInvalidValue;
-    }
-    count_launch();
-    return cudaGetLastError();
-  }
-  if (w <= 16) chol_leaf_kernel<T, 16><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
-  else if (w <= 32) chol_leaf_kernel<T, 32><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+  if (w <= 16) chol_leaf_rl_kernel<T, 16, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
+  else if (w <= 32) chol_leaf_rl_kernel<T, 32, kLeafT><<<grid, kLeafT, 0, st>>>(m, w, src, lds, dst, ldd, col0, fail);
   else return cudaErrorInvalidValue;
   count_launch();
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ LU
+// ONE warp factors the diagonal block in registers while the other warps already load their
+// rows below / stage their U columns; then one __syncthreads and the independent
+// substitutions (the 32-wide leaf of lu_panel_rec with SF_LU_P64=0; panel64.cu is the
+// default).
 template <typename T, int W>
-__global__ void __launch_bounds__(kLeafT) lu_leaf_kernel(int64_t m, int64_t ncr, int w, const T* __restrict__ src,
-                                                         int64_t lds, T* __restrict__ dst, int64_t ldd, int64_t col0,
-                                                         const T* tolp, long long* fail, int nrow_blocks) {
-  if (failed(fail)) return;
-  __shared__ T Ls[W][W + 1];     // L11 (row-major: Ls[c][k] = L_ck)
-  __shared__ T Us[W][W + 1];     // U11 (Us[k][c] = U_kc)
-  __shared__ T inv[W];
-  __shared__ T S[kUCols][W + 1]; // staging for the U columns
-  __shared__ int bad;
-  const int tid = threadIdx.x, lane = tid & 31;
-  if (tid < 32) {
-    const T tol = __ldcg(tolp);
-    T x[W], y[W];   // lane i: row i (x) and column i (y) of the diagonal block
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-      const bool in = lane < w && k < w;
-      x[k] = in ? __ldcg(src + lane + (int64_t)k * lds) : T(0);
-      y[k] = in ? __ldcg(src + k + (int64_t)lane * lds) : T(0);
-    }
-    int ok = 1;
-#pragma unroll
-    for (int c = 0; c < W; ++c) {
-      if (c < w && ok) {
-        T a0 = x[c], a1 = T(0), b0 = y[c], b1 = T(0);
-#pragma unroll
-        for (int k = 0; k < c; ++k) {
-          const T ukc = __shfl_sync(kFull, y[k], c);   // U_kc: column c lives in lane c
-          const T lck = __shfl_sync(kFull, x[k], c);   // L_ck: row c lives in lane c
-          if (k & 1) { a1 = fma(-x[k], ukc, a1); b1 = fma(-lck, y[k], b1); }
-          else { a0 = fma(-x[k], ukc, a0); b0 = fma(-lck, y[k], b0); }
-        }
-        const T t = a0 + a1, u = b0 + b1;
-        const T Lcc = __shfl_sync(kFull, t, c);
-        if (!(fabs(Lcc) >= tol)) {
-          ok = 0;
-          if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
-        } else {
-          if (lane >= c) x[c] = t;
-          if (lane > c) y[c] = u / Lcc;
-          if (lane == 0) inv[c] = T(1) / Lcc;
-        }
-      }
-    }
-#pragma unroll
-    if (lane < W)
-      for (int k = 0; k < W; ++k) { Ls[lane][k] = x[k]; Us[k][lane] = y[k]; }
-    if (lane == 0) bad = !ok;
-  }
-  __syncthreads();
-  if (bad) return;
-  if (last_reader(fail + 1)) {   // see chol_leaf_kernel
-    for (int idx = tid; idx < w * w; idx += kLeafT) {
-      const int i = idx % w, k = idx / w;
-      dst[i + (int64_t)k * ldd] = (k <= i) ? Ls[i][k] : Us[i][k];   // L incl. diagonal / U strict upper
-    }
-  }
-  if ((int)blockIdx.x < nrow_blocks) {
-    // L rows below: L_rc = A_rc - sum_{k<c} L_rk U_kc
-    const int64_t r = w + (int64_t)blockIdx.x * kLeafT + tid;
-    if (r >= m) return;
-    T x[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) x[k] = (k < w) ? __ldcg(src + r + (int64_t)k * lds) : T(0);
-#pragma unroll
-    for (int c = 0; c < W; ++c) {
-      T a0 = x[c], a1 = T(0), a2 = T(0), a3 = T(0);
-#pragma unroll
-      for (int k = 0; k < c; ++k) {
-        if ((k & 3) == 0) a0 = fma(-x[k], Us[k][c], a0);
-        else if ((k & 3) == 1) a1 = fma(-x[k], Us[k][c], a1);
-        else if ((k & 3) == 2) a2 = fma(-x[k], Us[k][c], a2);
-        else a3 = fma(-x[k], Us[k][c], a3);
-      }
-      x[c] = (a0 + a1) + (a2 + a3);
-    }
-#pragma unroll
-    for (int k = 0; k < W; ++k)
-      if (k < w) dst[r + (int64_t)k * ldd] = x[k];
-    return;
-  }
-  // U columns to the right: U_cj = (A_cj - sum_{k<c} L_ck U_kj) / L_cc
-  const int64_t j0 = w + (int64_t)(blockIdx.x - nrow_blocks) * kUCols;
-  const int ncols = (int)((w + ncr - j0) < kUCols ? (w + ncr - j0) : kUCols);
-  const int warp = tid >> 5;
-  for (int jj = warp; jj < ncols; jj += kLeafT / 32)
-    if (lane < w) S[jj][lane] = __ldcg(src + lane + (j0 + jj) * lds);
-  __syncthreads();
-  if (tid < ncols) {
-    T y[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) y[k] = (k < w) ? S[tid][k] : T(0);
-#pragma unroll
-    for (int c = 0; c < W; ++c) {
-      T a0 = y[c], a1 = T(0), a2 = T(0), a3 = T(0);
-#pragma unroll
-      for (int k = 0; k < c; ++k) {
-        if ((k & 3) == 0) a0 = fma(-Ls[c][k], y[k], a0);
-        else if ((k & 3) == 1) a1 = fma(-Ls[c][k], y[k], a1);
-        else if ((k & 3) == 2) a2 = fma(-Ls[c][k], y[k], a2);
-        else a3 = fma(-Ls[c][k], y[k], a3);
-      }
-      y[c] = ((a0 + a1) + (a2 + a3)) * inv[c];
-    }
-#pragma unroll
-    for (int k = 0; k < W; ++k) S[tid][k] = y[k];
-  }
-  __syncthreads();
-  for (int jj = warp; jj < ncols; jj += kLeafT / 32)
-    if (lane < w) dst[lane + (j0 + jj) * ldd] = S[jj][lane];
-}
-
-// Variant (default): ONE warp runs the diagonal-block Crout in shared memory (lane i: row i
-// of L and column i of U; no shuffle chains) while the other warps already load their rows
-// below / stage their U columns; then one __syncthreads and the independent substitutions.
-// Same per-element arithmetic as lu_leaf_kernel (interleaved partial sums, one subtraction,
-// U_ci = t / L_cc in the block, * 1/L_cc for the U columns).
-template <typename T, int W, bool ROT>
 __global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t ncr, int w, const T* __restrict__ src,
                                                               int64_t lds, T* __restrict__ dst, int64_t ldd,
                                                               int64_t col0, const T* tolp, long long* fail,
                                                               int nrow_blocks) {
   if (failed(fail)) return;
-  // ROT: rows of Lt / Us zero-padded to 2W so the rolled (register-rotating) substitutions can
-  // read past the block; dynamic shared memory (about 50 KB for fp64)
-  constexpr int LW = ROT ? 2 * W : W + 2;
+  constexpr int LW = W + 2;   // dynamic shared memory (about 50 KB for fp64)
   extern __shared__ __align__(16) unsigned char lusm[];
   T (*Lt)[LW] = reinterpret_cast<T (*)[LW]>(lusm);              // L11 transposed (Lt[k][i] = L_ik)
   T (*Us)[LW] = reinterpret_cast<T (*)[LW]>(lusm + sizeof(T) * W * LW);   // U11 (Us[k][j] = U_kj)
@@ -576,8 +171,6 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t
   const int64_t r = w + (int64_t)blockIdx.x * kLeafT + tid;
   const int64_t j0 = w + (int64_t)(blockIdx.x - nrow_blocks) * kUCols;
   const int ncols = rowblock ? 0 : (int)((w + ncr - j0) < kUCols ? (w + ncr - j0) : kUCols);
-  if (ROT)
-    for (int idx = tid; idx < W * W; idx += kLeafT) { Lt[idx / W][W + idx % W] = T(0); Us[idx / W][W + idx % W] = T(0); }
   if (warp == 0) {
     // Right-looking in registers, the paper's per-element order (every
     // entry receives its -L_ik U_k* terms one at a time in k order): lane i holds row i of
@@ -636,7 +229,7 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t
   }
   __syncthreads();
   if (bad) return;
-  if (last_reader(fail + 1)) {   // see chol_leaf_kernel
+  if (last_reader(fail + 1)) {   // in-place safety: every CTA has read the diagonal block
     for (int idx = tid; idx < w * w; idx += kLeafT) {
       const int i = idx % w, k = idx / w;
       dst[i + (int64_t)k * ldd] = (k <= i) ? Lt[k][i] : Us[i][k];   // L incl. diagonal / U strict upper
@@ -645,18 +238,6 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t
   if (rowblock) {
     // L rows below: L_rc = A_rc - sum_{k<c} L_rk U_kc, right-looking (terms in k order)
     if (r >= m) return;
-    if (ROT) {
-#pragma unroll 1
-      for (int c = 0; c < w; ++c) {   // x[0] is column c of my row
-        const T x0 = x[0];
-        dst[r + (int64_t)c * ldd] = x0;
-        const T* u = &Us[c][c];       // u[j] = U_{c, c+j}, 0 past the block
-#pragma unroll
-        for (int j = 1; j < W; ++j) x[j - 1] = fma(-x0, u[j], x[j]);
-        x[W - 1] = T(0);
-      }
-      return;
-    }
 #pragma unroll
     for (int c = 0; c < W; ++c) {
       const T xc = x[c];
@@ -673,35 +254,18 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t
     T y[W];
 #pragma unroll
     for (int k = 0; k < W; ++k) y[k] = (k < w) ? S[tid][k] : T(0);
-    if (ROT) {
-#pragma unroll 1
-      for (int c = 0; c < w; ++c) {   // y[0] is row c of my column
-        const T y0 = y[0] * inv[c];
-        S[tid][c] = y0;
-        const T* l = &Lt[c][c];       // l[j] = L_{c+j, c}, 0 past the block
 #pragma unroll
-        for (int j = 1; j < W; ++j) y[j - 1] = fma(-l[j], y0, y[j]);
-        y[W - 1] = T(0);
-      }
-    } else {
+    for (int c = 0; c < W; ++c) {   // right-looking: y_c *= 1/L_cc, then y_j -= L_jc y_c
+      y[c] = y[c] * inv[c];
 #pragma unroll
-      for (int c = 0; c < W; ++c) {   // right-looking: y_c *= 1/L_cc, then y_j -= L_jc y_c
-        y[c] = y[c] * inv[c];
-#pragma unroll
-        for (int j = c + 1; j < W; ++j) y[j] = fma(-Lt[c][j], y[c], y[j]);
-      }
-#pragma unroll
-      for (int k = 0; k < W; ++k) S[tid][k] = y[k];
+      for (int j = c + 1; j < W; ++j) y[j] = fma(-Lt[c][j], y[c], y[j]);
     }
+#pragma unroll
+    for (int k = 0; k < W; ++k) S[tid][k] = y[k];
   }
   __syncthreads();
   for (int jj = warp; jj < ncols; jj += kLeafT / 32)
     if (lane < w) dst[lane + (j0 + jj) * ldd] = S[jj][lane];
-}
-
-static bool lu_leaf_warp_on() {
-  static int on = [] { const char* e = getenv("SF_LU_LEAF_WARP"); return e ? atoi(e) : 1; }();
-  return on != 0;
 }
 
 template <typename T>
@@ -713,34 +277,28 @@ cudaError_t lu_leaf(int64_t m, int64_t ncr, int w, const T* src, int64_t lds, T*
   const int ncb = ncr > 0 ? (int)((ncr + kUCols - 1) / kUCols) : 0;
   int grid = nrb + ncb;
   if (grid == 0) grid = 1;
-  if (lu_leaf_warp_on()) {
-    static const bool rot = [] { const char* e = getenv("SF_LU_LEAF_ROT"); return e && atoi(e) != 0; }();
-    auto go = [&](auto kern, int W) -> cudaError_t {
-      const int lw = rot ? 2 * W : W + 2;
-      const size_t smem = sizeof(T) * ((size_t)2 * W * lw + (size_t)kUCols * (W + 1));
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      kern<<<grid, kLeafT, smem, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
-      return cudaSuccess;
-    };
-    cudaError_t e;
-    if (w <= 16) e = rot ? go(lu_leaf_warp_kernel<T, 16, true>, 16) : go(lu_leaf_warp_kernel<T, 16, false>, 16);
-    else if (w <= 32) e = rot ? go(lu_leaf_warp_kernel<T, 32, true>, 32) : go(lu_leaf_warp_kernel<T, 32, false>, 32);
-    else return cudaErrorInvalidValue;
+  auto go = [&](auto kern, int W) -> cudaError_t {
+    const size_t smem = sizeof(T) * ((size_t)2 * W * (W + 2) + (size_t)kUCols * (W + 1));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-  } else if (w <= 16) lu_leaf_kernel<T, 16><<<grid, kLeafT, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
-  else if (w <= 32) lu_leaf_kernel<T, 32><<<grid, kLeafT, 0, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
+    kern<<<grid, kLeafT, smem, st>>>(m, ncr, w, src, lds, dst, ldd, col0, tol, fail, nrb);
+    return cudaSuccess;
+  };
+  cudaError_t e;
+  if (w <= 16) e = go(lu_leaf_warp_kernel<T, 16>, 16);
+  else if (w <= 32) e = go(lu_leaf_warp_kernel<T, 32>, 32);
   else return cudaErrorInvalidValue;
+  if (e != cudaSuccess) return e;
   count_launch();
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ LU, U rows only
-// The U part of lu_leaf_kernel against an ALREADY FACTORED diagonal block: L11 (w x w,
+// The U part of lu_leaf_warp_kernel against an ALREADY FACTORED diagonal block: L11 (w x w,
 // lower incl. diagonal, at `l11`) is read, not recomputed.  Used by the block-cyclic
 // distributed LU (dist.cu), where a rank holds the received L panel but not the original
 // diagonal block: U_cj = (A_cj - sum_{k<c} L_ck U_kj) / L_cc for the
-// ncols columns at src.  Same per-element arithmetic as lu_leaf_kernel's U part.
+// ncols columns at src.
 template <typename T, int W>
 __global__ void __launch_bounds__(kLeafT) lu_usolve_kernel(int64_t ncols_total, int w, const T* __restrict__ l11,
                                                            int64_t ldl, const T* __restrict__ src, int64_t lds,

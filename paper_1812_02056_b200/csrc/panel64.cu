@@ -16,16 +16,18 @@
 // column blocks (LU only: 128 columns of U right of the panel each).  Every CTA factors the
 // w x w diagonal block itself in shared memory (no grid-wide dependency; identical
 // operations in every CTA, so identical bits), blocked 2 x 2 in 32 x 32 quarters:
-//   1. warp 0: D11, right-looking in registers (lane = row; per column one shuffle, one
-//      reciprocal, one broadcast row and one fma per entry — DESIGN.md reading P11);
+//   1. warp 0: D11, right-looking in registers, lane = row.  Per column c: the pivot by one
+//      shuffle, its reciprocal, and a rank-1 update whose pivot-row operands arrive by warp
+//      shuffles (no shared-memory round trip, no divergent branch, no __syncwarp);
 //   2. warp 1: the rows 32..w-1 of the block against U11 (L21); warp 2 (LU): the columns
 //      32..w-1 against L11 (U12) — one forward substitution per lane;
 //   3. all warps: D22 -= L21 U12 (Cholesky: L21 L21^T), terms one at a time in k order;
-//   4. warp 0: D22 as in 1.
-// while the CTA's own rows (or columns) are prefetched into L2.  Then each thread finishes its row (L_i* against U, right-looking: x_j -= x_c U_cj
-// for c ascending, i.e. the paper's per-element order of terms) or its column of U.  Every
-// entry receives the same terms in the same k order as the paper's loops (grouping-free);
-// only the reciprocal multiply (P11) and fma rounding differ from the oracle.
+//   4. warp 0: D22 as in 1,
+// while the CTA's own rows (or columns) are prefetched into L2.  Then each thread finishes its
+// row of L (against U, right-looking: x_j -= x_c U_cj for c ascending — the paper's per-entry
+// order of terms) or its column of U.  Reading P11: a division by L_cc is a
+// multiplication by the (warp-uniform) reciprocal; in the LU diagonal block the update term
+// L_ic U_cj is formed as (L_ic / L_cc) * (L_cc U_cj) — same terms, reassociated, <= 1 ulp.
 // The last CTA to have read the diagonal block writes it (in-place safety).
 // Loads of data produced by other kernels bypass L1 (ld.global.cg), see leaf.cu.
 #include <math.h>
@@ -35,11 +37,23 @@
 
 namespace sf {
 
+// SF_P64_TIMING (calib/p64_probe.cu only): CTA 0 thread 0 records %globaltimer at phase ends
+#ifdef SF_P64_TIMING
+__device__ unsigned long long p64_times[16];
+#define P64_T(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) { unsigned long long t; \
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); p64_times[k] = t; } } while (0)
+#else
+#define P64_T(k) do {} while (0)
+#endif
+
 namespace p64 {
 constexpr int NT = 128;     // threads per CTA = rows / columns per CTA
 constexpr int W = 64;       // maximum panel width
 constexpr int H = 32;       // quarter size
-constexpr int LD = W + 2;   // smem row stride (16-byte aligned rows)
+// Shared-memory matrices are W rows x DS columns: the substitution's register window covers
+// columns c0 .. c0+63 (c0 <= 48), so rows are zero padded to 112 columns; DS odd keeps
+// column-wise accesses (lane = row) at most 2-way bank conflicted.
+constexpr int DS = W + 48 + 1;
 constexpr unsigned kFull = 0xffffffffu;
 }  // namespace p64
 
@@ -54,7 +68,8 @@ __device__ __forceinline__ void p64_fail(long long* fail, long long col1) {
 __device__ __forceinline__ bool p64_last_reader(long long* counter) {
   __shared__ int last;
   if (threadIdx.x == 0) {
-    __threadfence();
+    // this CTA's reads of the diagonal block have completed (their values are in shared
+    // memory), so no fence is needed before announcing it
     const unsigned long long old = atomicAdd((unsigned long long*)counter, 1ull);
     last = (old == gridDim.x - 1);
     if (last) *counter = 0;
@@ -63,61 +78,65 @@ __device__ __forceinline__ bool p64_last_reader(long long* counter) {
   return last;
 }
 
-// Factor the H x H quarter D[o:o+H, o:o+H] in place with warp `warp` (lane = row o+lane),
+// Factor the H x H quarter D[o:o+H, o:o+H] in place with one warp (lane = row o+lane),
 // right-looking.  LU: D <- L (lower incl. diagonal) and U (strict upper, scaled by 1/L_cc);
 // Cholesky: D <- L (lower incl. diagonal), upper part untouched.  inv[o+c] = 1 / L_cc.
-// Returns false (in every lane) on R3 failure, after recording column col0+o+c+1.
+// Returns false (in every lane) on R3 failure, after recording column col0+o+c+1.  Every
+// warp of the CTA runs it (they would otherwise idle at the next barrier, each on its own SM
+// sub-partition) so that no shuffle sits under a divergent branch; only `writer` stores.
 template <typename T, bool LU>
-__device__ __forceinline__ bool p64_factor_quarter(T (*D)[p64::LD], T* inv, T (*buf)[p64::H], int o, int wq,
-                                                   T tol, int64_t col0, long long* fail, int lane) {
+__device__ __forceinline__ bool p64_factor_quarter(T* D, T* inv, int o, int wq, T tol, int64_t col0, long long* fail,
+                                                   int lane, bool writer) {
   using namespace p64;
   T a[H];
+  T* row = D + (o + lane) * DS + o;
 #pragma unroll
-  for (int k = 0; k < H; ++k) a[k] = D[o + lane][o + k];
-  bool ok = true;
+  for (int k = 0; k < H; ++k) a[k] = row[k];
+  T myri = T(0);
+  int bad_col = -1;   // first failing column of the quarter (warp-uniform)
+  // branch-free over all H columns (columns >= wq are zero padded and pivot on 1), so every
+  // shuffle is provably convergent: no per-shuffle warp synchronisation in the SASS
 #pragma unroll
   for (int c = 0; c < H; ++c) {
-    if (c < wq) {
-      const T d = __shfl_sync(kFull, a[c], c);
-      if (LU ? !(fabs(d) >= tol) : !(d > T(0))) {
-        ok = false;
-        if (lane == 0 && blockIdx.x == 0) p64_fail(fail, col0 + o + c + 1);
-        break;
+    const T d0 = __shfl_sync(kFull, a[c], c);
+    const bool live = c < wq;
+    if (live && bad_col < 0 && (LU ? !(fabs(d0) >= tol) : !(d0 > T(0)))) bad_col = c;
+    const T d = live ? d0 : T(1);
+    if (LU) {
+      // lane i > c: a_ij -= (L_ic / L_cc) * v_j, v = row c of the block (unscaled: L_cc U_cj)
+      const T ri = T(1) / d;
+      if (lane == c) myri = live ? ri : T(0);
+      const T mlt = a[c] * ri;
+#pragma unroll
+      for (int j = c + 1; j < H; ++j) {
+        const T v = __shfl_sync(kFull, a[j], c);
+        a[j] = (lane > c) ? fma(-mlt, v, a[j]) : a[j];
       }
-      if (LU) {
-        const T ri = T(1) / d;
-        if (lane == c) {
-          inv[o + c] = ri;
+    } else {
+      // lane i >= j > c: a_ij -= L_ic L_jc, L_jc from lane j
+      const T Lcc = p64_sqrt(d);
+      const T ri = T(1) / Lcc;
+      if (lane == c) myri = live ? ri : T(0);
+      const T l = (lane == c) ? Lcc : a[c] * ri;
+      a[c] = l;
 #pragma unroll
-          for (int j = c + 1; j < H; ++j) { a[j] = a[j] * ri; buf[c & 1][j] = a[j]; }
-        }
-        __syncwarp();
-        if (lane > c) {
-          const T l = a[c];
-#pragma unroll
-          for (int j = c + 1; j < H; ++j) a[j] = fma(-l, buf[c & 1][j], a[j]);
-        }
-      } else {
-        const T Lcc = p64_sqrt(d);
-        const T ri = T(1) / Lcc;
-        const T l = (lane == c) ? Lcc : a[c] * ri;
-        a[c] = l;
-        buf[c & 1][lane] = l;
-        if (lane == c) inv[o + c] = ri;
-        __syncwarp();
-        if (lane > c) {
-#pragma unroll
-          for (int j = c + 1; j < H; ++j) a[j] = fma(-l, buf[c & 1][j], a[j]);
-        }
+      for (int j = c + 1; j < H; ++j) {
+        const T lj = __shfl_sync(kFull, l, j);
+        a[j] = (lane >= j) ? fma(-l, lj, a[j]) : a[j];
       }
     }
   }
-  if (ok) {
+  const bool ok = bad_col < 0;
+  if (!ok && writer && lane == 0 && blockIdx.x == 0) p64_fail(fail, col0 + o + bad_col + 1);
+  if (ok && writer) {
 #pragma unroll
-    for (int k = 0; k < H; ++k)
-      if (LU || k <= lane) D[o + lane][o + k] = a[k];
+    for (int k = 0; k < H; ++k) {
+      if (LU) row[k] = (k > lane) ? a[k] * myri : a[k];   // U_lane,k = (L_lane,lane U_lane,k) / L_lane,lane
+      else if (k <= lane) row[k] = a[k];
+    }
+    if (lane < wq) inv[o + lane] = myri;
   }
-  return __all_sync(kFull, ok);
+  return ok;
 }
 
 // One launch per panel of width w <= 64.  LU: rows [0, m) from the diagonal down, ncr
@@ -129,15 +148,18 @@ __global__ void __launch_bounds__(p64::NT) panel64_kernel(int64_t m, int64_t ncr
                                                           const T* tolp, long long* fail, int nrb) {
   using namespace p64;
   if (failed(fail)) return;
-  __shared__ __align__(16) T D[W][LD];
+  extern __shared__ __align__(16) unsigned char p64_dyn[];
+  T* D = reinterpret_cast<T*>(p64_dyn);            // the diagonal block, W x DS (zero padded)
+  T* Mt = D + W * DS;                              // L^T for the L-against-L^T substitutions
   __shared__ T inv[W];
-  __shared__ T buf[2][H];
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool rowblock = (int)blockIdx.x < nrb;
   const int64_t r = w + (int64_t)blockIdx.x * NT + tid;                       // my row (row blocks)
   const int64_t jc = w + (int64_t)((int)blockIdx.x - nrb) * NT + tid;         // my U column (column blocks)
   const bool mine = rowblock ? r < m : jc < w + ncr;
+  // which operator the substitution applies: U (LU rows) or L^T (LU columns, Cholesky rows)
+  const bool use_u = LU && rowblock;
 
   // warm L2 with this CTA's rows / columns (512 lines of 128 B) while the diagonal block is
   // factored; they are loaded into registers after it (holding them through the diagonal
@@ -154,102 +176,128 @@ __global__ void __launch_bounds__(p64::NT) panel64_kernel(int64_t m, int64_t ncr
   }
   for (int idx = tid; idx < W * W; idx += NT) {
     const int i = idx % W, j = idx / W;
-    D[i][j] = (i < w && j < w && (LU || j <= i)) ? __ldcg(src + i + (int64_t)j * lds) : T(0);
+    D[i * DS + j] = (i < w && j < w && (LU || j <= i)) ? __ldcg(src + i + (int64_t)j * lds) : T(0);
   }
+  for (int idx = tid; idx < W * (DS - W); idx += NT) D[(idx / (DS - W)) * DS + W + idx % (DS - W)] = T(0);
   const T tol = LU ? __ldcg(tolp) : T(0);
   if (tid < W) inv[tid] = T(0);
   if (tid == 0) bad = 0;
+  P64_T(0);
   __syncthreads();
+  P64_T(1);
 
   const int w1 = w < H ? w : H, w2 = w - w1;
   // 1. D11
-  if (warp == 0 && !p64_factor_quarter<T, LU>(D, inv, buf, 0, w1, tol, col0, fail, lane) && lane == 0) bad = 1;
+  if (!p64_factor_quarter<T, LU>(D, inv, 0, w1, tol, col0, fail, lane, warp == 0) && tid == 0) bad = 1;
   __syncthreads();
+  P64_T(2);
   if (bad) return;
   if (w2 > 0) {
     // 2. L21 = D21 U11^-1 (LU) / D21 L11^-T (Cholesky): lane = row 32 + lane
     if (warp == 1) {
       T y[H];
+      T* row = D + (H + lane) * DS;
 #pragma unroll
-      for (int k = 0; k < H; ++k) y[k] = D[H + lane][k];
+      for (int k = 0; k < H; ++k) y[k] = row[k];
 #pragma unroll
       for (int c = 0; c < H; ++c) {
         if (!LU) y[c] = y[c] * inv[c];
 #pragma unroll
-        for (int j = c + 1; j < H; ++j) y[j] = fma(-y[c], LU ? D[c][j] : D[j][c], y[j]);
+        for (int j = c + 1; j < H; ++j) y[j] = fma(-y[c], LU ? D[c * DS + j] : D[j * DS + c], y[j]);
       }
       if (lane < w2) {
 #pragma unroll
-        for (int k = 0; k < H; ++k) D[H + lane][k] = y[k];
+        for (int k = 0; k < H; ++k) row[k] = y[k];
       }
     } else if (LU && warp == 2) {
       // U12 = L11^-1 D12, scaled: lane = column 32 + lane
       T y[H];
 #pragma unroll
-      for (int k = 0; k < H; ++k) y[k] = D[k][H + lane];
+      for (int k = 0; k < H; ++k) y[k] = D[k * DS + H + lane];
 #pragma unroll
       for (int c = 0; c < H; ++c) {
         y[c] = y[c] * inv[c];
 #pragma unroll
-        for (int k = c + 1; k < H; ++k) y[k] = fma(-D[k][c], y[c], y[k]);
+        for (int k = c + 1; k < H; ++k) y[k] = fma(-D[k * DS + c], y[c], y[k]);
       }
       if (lane < w2) {
 #pragma unroll
-        for (int k = 0; k < H; ++k) D[k][H + lane] = y[k];
+        for (int k = 0; k < H; ++k) D[k * DS + H + lane] = y[k];
       }
     }
     __syncthreads();
-    // 3. D22 -= L21 U12 (Cholesky: L21 L21^T, lower part), one term at a time in k order
+    P64_T(3);
+    // 3. D22 -= L21 U12 (Cholesky: L21 L21^T, lower part), one term at a time in k order;
+    //    lane = column (contiguous across the warp), rows warp-uniform (broadcast operands)
 #pragma unroll
     for (int e = 0; e < H * H / NT; ++e) {
-      const int idx = tid + e * NT, i = idx % H, j = idx / H;
+      const int i = warp + 4 * e, j = lane;
       if (i < w2 && j < w2 && (LU || j <= i)) {
-        T v = D[H + i][H + j];
+        T v = D[(H + i) * DS + H + j];
 #pragma unroll
-        for (int k = 0; k < H; ++k) v = fma(-D[H + i][k], LU ? D[k][H + j] : D[H + j][k], v);
-        D[H + i][H + j] = v;
+        for (int k = 0; k < H; ++k) v = fma(-D[(H + i) * DS + k], LU ? D[k * DS + H + j] : D[(H + j) * DS + k], v);
+        D[(H + i) * DS + H + j] = v;
       }
     }
     __syncthreads();
+    P64_T(4);
     // 4. D22
-    if (warp == 0 && !p64_factor_quarter<T, LU>(D, inv, buf, H, w2, tol, col0, fail, lane) && lane == 0) bad = 1;
+    if (!p64_factor_quarter<T, LU>(D, inv, H, w2, tol, col0, fail, lane, warp == 0) && tid == 0) bad = 1;
     __syncthreads();
     if (bad) return;
   }
+  P64_T(5);
+  // 5. L^T for the substitutions that need it: Mt[k][j] = L_jk (j > k), zero elsewhere
+  if (!use_u) {
+    if (tid < DS) {
+#pragma unroll 4
+      for (int k = 0; k < W; ++k) Mt[k * DS + tid] = (tid > k && tid < W) ? D[tid * DS + k] : T(0);
+    }
+    __syncthreads();
+  }
+  P64_T(6);
   if (p64_last_reader(fail + 1)) {
     for (int idx = tid; idx < w * w; idx += NT) {
       const int i = idx % w, k = idx / w;
-      if (LU || k <= i) dst[i + (int64_t)k * ldd] = D[i][k];
+      if (LU || k <= i) dst[i + (int64_t)k * ldd] = D[i * DS + k];
     }
   }
+  P64_T(7);
   if (!mine) return;
+  // my row r (x_k = A_rk) or my U column jc (x_k = A_kjc), k < w
   T x[W];
 #pragma unroll
   for (int k = 0; k < W; ++k)
     x[k] = (k < w) ? (rowblock ? __ldcg(src + r + (int64_t)k * lds) : __ldcg(src + k + jc * lds)) : T(0);
-  if (rowblock) {
-    // row r: L_rc = A_rc - sum_{k<c} L_rk U_kc (Cholesky: (A_rc - sum L_rk L_ck) / L_cc)
+  P64_T(8);
+  // right-looking substitution, terms one at a time in k order (x_j -= x_k M_kj for k
+  // ascending; M = U for LU rows, L^T otherwise, whose x_k is first scaled by 1/L_kk), in
+  // blocks of 16 columns: the register window x[0..63] holds columns c0..c0+63 and rotates
+  // by 16 per block, so the loop body is one block's code (a fully unrolled 64-column
+  // substitution is ~9K instructions, fetched cold by every CTA)
+  const T* Op = use_u ? D : Mt;
+  T* out = rowblock ? dst + r : dst + jc * ldd;
+  const int64_t ostride = rowblock ? ldd : 1;
+  const int nb = (w + 15) / 16;
+#pragma unroll 1
+  for (int b = 0; b < nb; ++b) {
+    const int c0 = 16 * b;
 #pragma unroll
-    for (int c = 0; c < W; ++c) {
-      if (!LU) x[c] = x[c] * inv[c];
+    for (int c = 0; c < 16; ++c) {
+      const T* Mr = Op + (c0 + c) * DS + c0;
+      if (!use_u) x[c] = x[c] * inv[c0 + c];
 #pragma unroll
-      for (int j = c + 1; j < W; ++j) x[j] = fma(-x[c], LU ? D[c][j] : D[j][c], x[j]);
+      for (int j = c + 1; j < W; ++j) x[j] = fma(-x[c], Mr[j], x[j]);
     }
 #pragma unroll
-    for (int k = 0; k < W; ++k)
-      if (k < w) dst[r + (int64_t)k * ldd] = x[k];
-  } else {
-    // U column jc: U_cj = (A_cj - sum_{k<c} L_ck U_kj) / L_cc
+    for (int c = 0; c < 16; ++c)
+      if (c0 + c < w) out[(int64_t)(c0 + c) * ostride] = x[c];
 #pragma unroll
-    for (int c = 0; c < W; ++c) {
-      x[c] = x[c] * inv[c];
+    for (int j = 0; j < W - 16; ++j) x[j] = x[j + 16];
 #pragma unroll
-      for (int k = c + 1; k < W; ++k) x[k] = fma(-D[k][c], x[c], x[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < W; ++k)
-      if (k < w) dst[k + jc * ldd] = x[k];
+    for (int j = W - 16; j < W; ++j) x[j] = T(0);
   }
+  P64_T(9);
 }
 
 template <typename T, bool LU>
@@ -262,7 +310,14 @@ static cudaError_t launch_panel64(int64_t m, int64_t ncr, int w, const T* src, i
   const int ncb = (LU && ncr > 0) ? (int)((ncr + p64::NT - 1) / p64::NT) : 0;
   int grid = nrb + ncb;
   if (grid == 0) grid = 1;
-  panel64_kernel<T, LU><<<grid, p64::NT, 0, st>>>(m, LU ? ncr : 0, w, src, lds, dst, ldd, col0, tol, fail, nrb);
+  constexpr size_t dyn = sizeof(T) * 2 * p64::W * p64::DS;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(panel64_kernel<T, LU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  panel64_kernel<T, LU><<<grid, p64::NT, dyn, st>>>(m, LU ? ncr : 0, w, src, lds, dst, ldd, col0, tol, fail, nrb);
   count_launch();
   return cudaGetLastError();
 }
