@@ -407,7 +407,22 @@ def main():
                      "avg_launch_ms": upd_ms / upd_n if upd_n else None,
                      "flops_per_launch": upd_fl / upd_n if upd_n else None,
                      "update_share_of_step": upd_ms / ms if ms else None,
-                     "panel_ms_per_step": pan_ms / args.steps, "qr_r_ms_per_step": qr_ms / args.steps})
+                     "panel_ms_per_step": pan_ms / args.steps, "qr_r_ms_per_step": qr_ms / args.steps,
+                     # the panels' column recurrences are sequential: device time per column
+                     # (summed over the panel launches of a step, lookahead concurrency included)
+                     "panel_us_per_column": pan_ms / args.steps * 1e3 / n})
+    # ---- per rank (N > 1): where each rank's step went, so the scaling curve explains itself
+    bc_ms, bc_n, bc_bytes = prof.get("bcast", (0.0, 0, 0.0))
+    if ws > 1:
+        mine = torch.tensor([ms, upd_ms, pan_ms, bc_ms, bc_bytes], dtype=torch.float64, device="cuda")
+        allr = [torch.zeros_like(mine) for _ in range(ws)]
+        dist.all_gather(allr, mine)
+        per_rank = [{"rank": r, "ms_per_step": float(v[0]) / args.steps,
+                     "flush_ms_per_step": float(v[1]) / args.steps, "panel_ms_per_step": float(v[2]) / args.steps,
+                     "bcast_ms_per_step": float(v[3]) / args.steps,
+                     "bcast_gb_per_step": float(v[4]) / args.steps / 1e9} for r, v in enumerate(allr)]
+    else:
+        per_rank = None
     # panel kernels: minimal HBM bytes (read + write each panel once: elt * 2 * (n - z) * w,
     # QR: all n rows) over their device time (they run concurrently on the lookahead stream)
     elt = 4 if dtype == "f32" else 8
@@ -501,7 +516,8 @@ def main():
                 "pct_peak_kind": ("classical useful GFLOP/s per GPU / TF32 dense peak" if dtype == "f32"
                                   else "classical GFLOP/s per GPU / FP64 tensor (DMMA) peak"),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": int(l1 - l0), "clocks": ck}
+                "gpu_launches": int(l1 - l0), "clocks": ck,
+                **({"per_rank": per_rank} if per_rank else {})}
         print(json.dumps(line), flush=True)
     if comm is not None:
         torch.cuda.synchronize()

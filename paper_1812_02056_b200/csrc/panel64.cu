@@ -16,9 +16,9 @@
 // column blocks (LU only: 128 columns of U right of the panel each).  Every CTA factors the
 // w x w diagonal block itself in shared memory (no grid-wide dependency; identical
 // operations in every CTA, so identical bits), blocked 2 x 2 in 32 x 32 quarters:
-//   1. warp 0: D11, right-looking in registers, lane = row.  Per column c: the pivot by one
-//      shuffle, its reciprocal, and a rank-1 update whose pivot-row operands arrive by warp
-//      shuffles (no shared-memory round trip, no divergent branch, no __syncwarp);
+//   1. warp 0: D11, right-looking in registers (2-D lane layout, see p64_factor_quarter):
+//      per column c the pivot by one shuffle, its reciprocal, and a rank-1 update whose
+//      operands arrive by 12 warp shuffles (no shared-memory round trip);
 //   2. warp 1: the rows 32..w-1 of the block against U11 (L21); warp 2 (LU): the columns
 //      32..w-1 against L11 (U12) — one forward substitution per lane;
 //   3. all warps: D22 -= L21 U12 (Cholesky: L21 L21^T), terms one at a time in k order;
@@ -32,6 +32,8 @@
 // Loads of data produced by other kernels bypass L1 (ld.global.cg), see leaf.cu.
 #include <math.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -42,8 +44,12 @@ namespace sf {
 __device__ unsigned long long p64_times[16];
 #define P64_T(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) { unsigned long long t; \
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); p64_times[k] = t; } } while (0)
+// [10] earliest CTA start, [11] latest thread end, [12] latest row-block end
+#define P64_EDGE(k, op) do { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); \
+  op(&p64_times[k], t); } while (0)
 #else
 #define P64_T(k) do {} while (0)
+#define P64_EDGE(k, op) do {} while (0)
 #endif
 
 namespace p64 {
@@ -51,15 +57,50 @@ constexpr int NT = 128;     // threads per CTA = rows / columns per CTA
 constexpr int W = 64;       // maximum panel width
 constexpr int H = 32;       // quarter size
 // Shared-memory matrices are W rows x DS columns: the substitution's register window covers
-// columns c0 .. c0+63 (c0 <= 48), so rows are zero padded to 112 columns; DS odd keeps
-// column-wise accesses (lane = row) at most 2-way bank conflicted.
-constexpr int DS = W + 48 + 1;
+// columns c0 .. c0+63 (c0 <= 56), so rows are zero padded (to 120 columns; DS even keeps
+// rows 16-byte aligned for paired loads).
+constexpr int DS = W + 56 + 2;
 constexpr unsigned kFull = 0xffffffffu;
 }  // namespace p64
 
-template <typename T> __device__ __forceinline__ T p64_sqrt(T x);
-template <> __device__ __forceinline__ double p64_sqrt<double>(double x) { return sqrt(x); }
-template <> __device__ __forceinline__ float p64_sqrt<float>(float x) { return sqrtf(x); }
+template <typename T> struct T2s;
+template <> struct T2s<double> { using type = double2; };
+template <> struct T2s<float> { using type = float2; };
+template <typename T> using T2 = typename T2s<T>::type;
+
+// Reciprocal and reciprocal square root without the IEEE division / square-root subroutine
+// calls (a CALL makes the compiler save the live register window around it, ~32 doubles per
+// pivot step): hardware approximation + Newton steps, within 1 ulp of the correctly rounded
+// value (reading P11), exact for powers of two (the planted-factor tests).
+__device__ __forceinline__ double p64_rcp(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ float p64_rcp(float d) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+  const float e = fmaf(-d, r, 1.0f);
+  return fmaf(r, e, r);
+}
+__device__ __forceinline__ double p64_rsqrt(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  // y <- y (3 - d y^2) / 2, twice
+  double h = 0.5 * d;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+__device__ __forceinline__ float p64_rsqrt(float d) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d));
+  const float h = 0.5f * d;
+  return y * fmaf(-h * y, y, 1.5f);
+}
 
 __device__ __forceinline__ void p64_fail(long long* fail, long long col1) {
   atomicMin((unsigned long long*)fail, (unsigned long long)col1);
@@ -78,65 +119,122 @@ __device__ __forceinline__ bool p64_last_reader(long long* counter) {
   return last;
 }
 
-// Factor the H x H quarter D[o:o+H, o:o+H] in place with one warp (lane = row o+lane),
-// right-looking.  LU: D <- L (lower incl. diagonal) and U (strict upper, scaled by 1/L_cc);
-// Cholesky: D <- L (lower incl. diagonal), upper part untouched.  inv[o+c] = 1 / L_cc.
-// Returns false (in every lane) on R3 failure, after recording column col0+o+c+1.  Every
-// warp of the CTA runs it (they would otherwise idle at the next barrier, each on its own SM
-// sub-partition) so that no shuffle sits under a divergent branch; only `writer` stores.
+// Factor the H x H quarter D[o:o+H, o:o+H] in place with ONE warp, right-looking.  LU:
+// D <- L (lower incl. diagonal) and U (strict upper, scaled by 1/L_cc); Cholesky: D <- L
+// (lower incl. diagonal), upper part untouched.  inv[o+c] = 1 / L_cc.  Returns false (in
+// every lane) on R3 failure, after recording column col0+o+c+1.
+// 2-D register layout: lane = 4p + q holds the 4 x 8 block of rows 4p..4p+3, columns
+// 8q..8q+7, so the rank-1 update of column c needs only 4 multipliers (from the lane holding
+// column c of my rows) and 8 pivot-row entries (from the lane holding row c of my columns)
+// by shuffle — 12 values instead of a whole row per lane.  Masked entries get a zero
+// multiplier (fma(-0, u, a) == a exactly), so the update itself is branch-free.  The column
+// loop is rolled in chunks of 8 (static register indices), and the reciprocal is a
+// call-free Newton iteration (p64_rcp): an IEEE division subroutine would make the
+// compiler save the whole register block around every call.
 template <typename T, bool LU>
 __device__ __forceinline__ bool p64_factor_quarter(T* D, T* inv, int o, int wq, T tol, int64_t col0, long long* fail,
-                                                   int lane, bool writer) {
+                                                   int lane) {
   using namespace p64;
-  T a[H];
-  T* row = D + (o + lane) * DS + o;
+  const int p = lane >> 2, q = lane & 3;
+  T blk[4][8];
 #pragma unroll
-  for (int k = 0; k < H; ++k) a[k] = row[k];
-  T myri = T(0);
-  int bad_col = -1;   // first failing column of the quarter (warp-uniform)
-  // branch-free over all H columns (columns >= wq are zero padded and pivot on 1), so every
-  // shuffle is provably convergent: no per-shuffle warp synchronisation in the SASS
+  for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-  for (int c = 0; c < H; ++c) {
-    const T d0 = __shfl_sync(kFull, a[c], c);
-    const bool live = c < wq;
-    if (live && bad_col < 0 && (LU ? !(fabs(d0) >= tol) : !(d0 > T(0)))) bad_col = c;
-    const T d = live ? d0 : T(1);
-    if (LU) {
-      // lane i > c: a_ij -= (L_ic / L_cc) * v_j, v = row c of the block (unscaled: L_cc U_cj)
-      const T ri = T(1) / d;
-      if (lane == c) myri = live ? ri : T(0);
-      const T mlt = a[c] * ri;
+    for (int jj = 0; jj < 8; ++jj) blk[ii][jj] = D[(o + 4 * p + ii) * DS + o + 8 * q + jj];
+  int bad_col = -1;   // warp-uniform
+#pragma unroll 1
+  for (int cb = 0; cb < H / 8; ++cb) {
 #pragma unroll
-      for (int j = c + 1; j < H; ++j) {
-        const T v = __shfl_sync(kFull, a[j], c);
-        a[j] = (lane > c) ? fma(-mlt, v, a[j]) : a[j];
+    for (int cc = 0; cc < 8; ++cc) {
+      const int c = 8 * cb + cc;
+      const int pi = cc & 3, pr = 2 * cb + (cc >> 2);   // row c = 4 pr + pi, column c = 8 cb + cc
+      const int src_d = 4 * pr + cb;
+      const T d0 = __shfl_sync(kFull, blk[pi][cc], src_d);
+      const bool live = c < wq;
+      if (live && bad_col < 0 && (LU ? !(fabs(d0) >= tol) : !(d0 > T(0)))) bad_col = c;
+      const T d = live ? d0 : T(1);
+      T l[4], u[8];
+      if (LU) {
+        const T ri = p64_rcp(d);
+        // multipliers L_ic of my rows (lane (p, cb)); pivot row U_cj = A_cj / L_cc of my
+        // columns (lane (pr, q))
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) l[ii] = __shfl_sync(kFull, blk[ii][cc], 4 * p + cb);
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) u[jj] = __shfl_sync(kFull, blk[pi][jj], 4 * pr + q) * ri;
+        if (lane == src_d) inv[o + c] = live ? ri : T(0);
+        if (p == pr) {   // row c keeps U_cj (scaled) right of the diagonal
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) blk[pi][jj] = (8 * q + jj > c) ? u[jj] : blk[pi][jj];
+        }
+      } else {
+        const T ri = p64_rsqrt(d);   // 1 / L_cc
+        const T Lcc = d * ri;
+        // L_ic of my rows (lane (p, cb)); L_jc of my columns j = 8q + jj, row j held by lane
+        // (2q + jj/4, cb) at row slot jj % 4
+#pragma unroll
+        for (int ii = 0; ii < 4; ++ii) l[ii] = __shfl_sync(kFull, blk[ii][cc], 4 * p + cb) * ri;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) u[jj] = __shfl_sync(kFull, blk[jj & 3][cc], 4 * (2 * q + (jj >> 2)) + cb) * ri;
+        if (lane == src_d) inv[o + c] = live ? ri : T(0);
+        if (q == cb) {   // column c keeps L_ic below the diagonal, L_cc on it
+#pragma unroll
+          for (int ii = 0; ii < 4; ++ii) {
+            const int i = 4 * p + ii;
+            blk[ii][cc] = (i > c) ? l[ii] : (i == c ? Lcc : blk[ii][cc]);
+          }
+        }
       }
-    } else {
-      // lane i >= j > c: a_ij -= L_ic L_jc, L_jc from lane j
-      const T Lcc = p64_sqrt(d);
-      const T ri = T(1) / Lcc;
-      if (lane == c) myri = live ? ri : T(0);
-      const T l = (lane == c) ? Lcc : a[c] * ri;
-      a[c] = l;
+      // rank-1 update of rows i > c, columns j > c (Cholesky: j <= i)
 #pragma unroll
-      for (int j = c + 1; j < H; ++j) {
-        const T lj = __shfl_sync(kFull, l, j);
-        a[j] = (lane >= j) ? fma(-l, lj, a[j]) : a[j];
-      }
+      for (int ii = 0; ii < 4; ++ii) l[ii] = (4 * p + ii > c) ? l[ii] : T(0);
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) u[jj] = (8 * q + jj > c) ? u[jj] : T(0);
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          if (LU || 8 * q + jj <= 4 * p + ii) blk[ii][jj] = fma(-l[ii], u[jj], blk[ii][jj]);
+        }
     }
   }
   const bool ok = bad_col < 0;
-  if (!ok && writer && lane == 0 && blockIdx.x == 0) p64_fail(fail, col0 + o + bad_col + 1);
-  if (ok && writer) {
+  if (!ok && lane == 0 && blockIdx.x == 0) p64_fail(fail, col0 + o + bad_col + 1);
+  if (ok) {
 #pragma unroll
-    for (int k = 0; k < H; ++k) {
-      if (LU) row[k] = (k > lane) ? a[k] * myri : a[k];   // U_lane,k = (L_lane,lane U_lane,k) / L_lane,lane
-      else if (k <= lane) row[k] = a[k];
-    }
-    if (lane < wq) inv[o + lane] = myri;
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        if (LU || 8 * q + jj <= 4 * p + ii) D[(o + 4 * p + ii) * DS + o + 8 * q + jj] = blk[ii][jj];
   }
   return ok;
+}
+
+// One 8-column block of the row / column substitution (see the kernel): x[0..JN) is the
+// register window for columns c0..c0+JN-1; on return it has moved on by 8 columns.
+template <typename T, int JN>
+__device__ __forceinline__ void p64_subst_block(T (&x)[p64::W], const T* Op, const T* inv, bool use_u, int c0, int w,
+                                                T* out, int64_t ostride) {
+  using namespace p64;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const T* Mr = Op + (c0 + c) * DS + c0;   // 16-byte aligned (DS, c0 even)
+    if (!use_u) x[c] = x[c] * inv[c0 + c];
+    if ((c + 1) & 1) x[c + 1] = fma(-x[c], Mr[c + 1], x[c + 1]);
+#pragma unroll
+    for (int jj = (c + 2) & ~1; jj < JN; jj += 2) {
+      const T2<T> mv = *reinterpret_cast<const T2<T>*>(Mr + jj);
+      x[jj] = fma(-x[c], mv.x, x[jj]);
+      x[jj + 1] = fma(-x[c], mv.y, x[jj + 1]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (c0 + c < w) out[(int64_t)(c0 + c) * ostride] = x[c];
+#pragma unroll
+  for (int j = 0; j < JN - 8; ++j) x[j] = x[j + 8];
+#pragma unroll
+  for (int j = JN - 8; j < JN; ++j) x[j] = T(0);
 }
 
 // One launch per panel of width w <= 64.  LU: rows [0, m) from the diagonal down, ncr
@@ -147,6 +245,7 @@ __global__ void __launch_bounds__(p64::NT) panel64_kernel(int64_t m, int64_t ncr
                                                           int64_t lds, T* __restrict__ dst, int64_t ldd, int64_t col0,
                                                           const T* tolp, long long* fail, int nrb) {
   using namespace p64;
+  if (threadIdx.x == 0) P64_EDGE(10, atomicMin);
   if (failed(fail)) return;
   extern __shared__ __align__(16) unsigned char p64_dyn[];
   T* D = reinterpret_cast<T*>(p64_dyn);            // the diagonal block, W x DS (zero padded)
@@ -174,11 +273,23 @@ __global__ void __launch_bounds__(p64::NT) panel64_kernel(int64_t m, int64_t ncr
       if (j < w + ncr && (l & 3) * 16 < w) prefetch_l2(src + (l & 3) * 16 + j * lds);
     }
   }
-  for (int idx = tid; idx < W * W; idx += NT) {
-    const int i = idx % W, j = idx / W;
-    D[i * DS + j] = (i < w && j < w && (LU || j <= i)) ? __ldcg(src + i + (int64_t)j * lds) : T(0);
+  {
+    // the diagonal block (column j: lanes over rows, coalesced), then the zero padding
+    T v[W / 4][2];
+#pragma unroll
+    for (int jj = 0; jj < W / 4; ++jj)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = lane + 32 * h, j = warp + 4 * jj;
+        v[jj][h] = (i < w && j < w && (LU || j <= i)) ? __ldcg(src + i + (int64_t)j * lds) : T(0);
+      }
+#pragma unroll
+    for (int jj = 0; jj < W / 4; ++jj)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) D[(lane + 32 * h) * DS + warp + 4 * jj] = v[jj][h];
+    for (int i = warp; i < W; i += NT / 32)
+      for (int j = W + lane; j < DS; j += 32) D[i * DS + j] = T(0);
   }
-  for (int idx = tid; idx < W * (DS - W); idx += NT) D[(idx / (DS - W)) * DS + W + idx % (DS - W)] = T(0);
   const T tol = LU ? __ldcg(tolp) : T(0);
   if (tid < W) inv[tid] = T(0);
   if (tid == 0) bad = 0;
@@ -187,63 +298,73 @@ __global__ void __launch_bounds__(p64::NT) panel64_kernel(int64_t m, int64_t ncr
   P64_T(1);
 
   const int w1 = w < H ? w : H, w2 = w - w1;
-  // 1. D11
-  if (!p64_factor_quarter<T, LU>(D, inv, 0, w1, tol, col0, fail, lane, warp == 0) && tid == 0) bad = 1;
-  __syncthreads();
-  P64_T(2);
-  if (bad) return;
-  if (w2 > 0) {
-    // 2. L21 = D21 U11^-1 (LU) / D21 L11^-T (Cholesky): lane = row 32 + lane
-    if (warp == 1) {
-      T y[H];
-      T* row = D + (H + lane) * DS;
+  // 1.-4.: the two diagonal quarters share ONE copy of the quarter code (a rolled loop): the
+  // second pass finds it in the instruction cache
+#pragma unroll 1
+  for (int qi = 0; qi < 2; ++qi) {
+    if (qi == 1) {
+      if (w2 <= 0) break;
+      // 2. L21 = D21 U11^-1 (LU) / D21 L11^-T (Cholesky): lane = row 32 + lane
+      if (warp == 1) {
+        T y[H];
+        T* row = D + (H + lane) * DS;
 #pragma unroll
-      for (int k = 0; k < H; ++k) y[k] = row[k];
+        for (int k = 0; k < H; ++k) y[k] = row[k];
 #pragma unroll
-      for (int c = 0; c < H; ++c) {
-        if (!LU) y[c] = y[c] * inv[c];
+        for (int c = 0; c < H; ++c) {
+          if (!LU) y[c] = y[c] * inv[c];
 #pragma unroll
-        for (int j = c + 1; j < H; ++j) y[j] = fma(-y[c], LU ? D[c * DS + j] : D[j * DS + c], y[j]);
+          for (int j = c + 1; j < H; ++j) y[j] = fma(-y[c], LU ? D[c * DS + j] : D[j * DS + c], y[j]);
+        }
+        if (lane < w2) {
+#pragma unroll
+          for (int k = 0; k < H; ++k) row[k] = y[k];
+        }
+      } else if (LU && warp == 2) {
+        // U12 = L11^-1 D12, scaled: lane = column 32 + lane
+        T y[H];
+#pragma unroll
+        for (int k = 0; k < H; ++k) y[k] = D[k * DS + H + lane];
+#pragma unroll
+        for (int c = 0; c < H; ++c) {
+          y[c] = y[c] * inv[c];
+#pragma unroll
+          for (int k = c + 1; k < H; ++k) y[k] = fma(-D[k * DS + c], y[c], y[k]);
+        }
+        if (lane < w2) {
+#pragma unroll
+          for (int k = 0; k < H; ++k) D[k * DS + H + lane] = y[k];
+        }
       }
-      if (lane < w2) {
+      __syncthreads();
+      P64_T(3);
+      // 3. D22 -= L21 U12 (Cholesky: L21 L21^T, lower part), one term at a time in k order;
+      //    lane = column (contiguous across the warp), rows warp-uniform (broadcast operands);
+      //    the k loop is rolled (one short body)
+      {
+        T v[H * H / NT];
+        const int j = lane;
 #pragma unroll
-        for (int k = 0; k < H; ++k) row[k] = y[k];
+        for (int e = 0; e < H * H / NT; ++e) v[e] = D[(H + warp + 4 * e) * DS + H + j];
+#pragma unroll 1
+        for (int k = 0; k < H; ++k) {
+          const T ukj = LU ? D[k * DS + H + j] : D[(H + j) * DS + k];
+#pragma unroll
+          for (int e = 0; e < H * H / NT; ++e) v[e] = fma(-D[(H + warp + 4 * e) * DS + k], ukj, v[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < H * H / NT; ++e) {
+          const int i = warp + 4 * e;
+          if (i < w2 && j < w2 && (LU || j <= i)) D[(H + i) * DS + H + j] = v[e];
+        }
       }
-    } else if (LU && warp == 2) {
-      // U12 = L11^-1 D12, scaled: lane = column 32 + lane
-      T y[H];
-#pragma unroll
-      for (int k = 0; k < H; ++k) y[k] = D[k * DS + H + lane];
-#pragma unroll
-      for (int c = 0; c < H; ++c) {
-        y[c] = y[c] * inv[c];
-#pragma unroll
-        for (int k = c + 1; k < H; ++k) y[k] = fma(-D[k * DS + c], y[c], y[k]);
-      }
-      if (lane < w2) {
-#pragma unroll
-        for (int k = 0; k < H; ++k) D[k * DS + H + lane] = y[k];
-      }
+      __syncthreads();
+      P64_T(4);
     }
+    if (warp == 0 && !p64_factor_quarter<T, LU>(D, inv, H * qi, qi ? w2 : w1, tol, col0, fail, lane) && lane == 0)
+      bad = 1;
     __syncthreads();
-    P64_T(3);
-    // 3. D22 -= L21 U12 (Cholesky: L21 L21^T, lower part), one term at a time in k order;
-    //    lane = column (contiguous across the warp), rows warp-uniform (broadcast operands)
-#pragma unroll
-    for (int e = 0; e < H * H / NT; ++e) {
-      const int i = warp + 4 * e, j = lane;
-      if (i < w2 && j < w2 && (LU || j <= i)) {
-        T v = D[(H + i) * DS + H + j];
-#pragma unroll
-        for (int k = 0; k < H; ++k) v = fma(-D[(H + i) * DS + k], LU ? D[k * DS + H + j] : D[(H + j) * DS + k], v);
-        D[(H + i) * DS + H + j] = v;
-      }
-    }
-    __syncthreads();
-    P64_T(4);
-    // 4. D22
-    if (!p64_factor_quarter<T, LU>(D, inv, H, w2, tol, col0, fail, lane, warp == 0) && tid == 0) bad = 1;
-    __syncthreads();
+    if (qi == 0) P64_T(2);
     if (bad) return;
   }
   P64_T(5);
@@ -272,32 +393,22 @@ __global__ void __launch_bounds__(p64::NT) panel64_kernel(int64_t m, int64_t ncr
   P64_T(8);
   // right-looking substitution, terms one at a time in k order (x_j -= x_k M_kj for k
   // ascending; M = U for LU rows, L^T otherwise, whose x_k is first scaled by 1/L_kk), in
-  // blocks of 16 columns: the register window x[0..63] holds columns c0..c0+63 and rotates
-  // by 16 per block, so the loop body is one block's code (a fully unrolled 64-column
-  // substitution is ~9K instructions, fetched cold by every CTA)
+  // blocks of 8 columns: the register window x[] holds columns c0..c0+63 and rotates by 8
+  // per block, so a loop body is one block's code (a fully unrolled 64-column substitution
+  // is several thousand instructions executed once).  Blocks with c0 >= 32 only touch the
+  // window's first 32 columns (the rest is past the panel) and run a half-width body.
   const T* Op = use_u ? D : Mt;
   T* out = rowblock ? dst + r : dst + jc * ldd;
   const int64_t ostride = rowblock ? ldd : 1;
-  const int nb = (w + 15) / 16;
+  const int nb = (w + 7) / 8;
+  const int nb1 = nb < 4 ? nb : 4;
 #pragma unroll 1
-  for (int b = 0; b < nb; ++b) {
-    const int c0 = 16 * b;
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      const T* Mr = Op + (c0 + c) * DS + c0;
-      if (!use_u) x[c] = x[c] * inv[c0 + c];
-#pragma unroll
-      for (int j = c + 1; j < W; ++j) x[j] = fma(-x[c], Mr[j], x[j]);
-    }
-#pragma unroll
-    for (int c = 0; c < 16; ++c)
-      if (c0 + c < w) out[(int64_t)(c0 + c) * ostride] = x[c];
-#pragma unroll
-    for (int j = 0; j < W - 16; ++j) x[j] = x[j + 16];
-#pragma unroll
-    for (int j = W - 16; j < W; ++j) x[j] = T(0);
-  }
+  for (int b = 0; b < nb1; ++b) p64_subst_block<T, 64>(x, Op, inv, use_u, 8 * b, w, out, ostride);
+#pragma unroll 1
+  for (int b = 4; b < nb; ++b) p64_subst_block<T, 32>(x, Op, inv, use_u, 8 * b, w, out, ostride);
   P64_T(9);
+  P64_EDGE(11, atomicMax);
+  if (rowblock) P64_EDGE(12, atomicMax);
 }
 
 template <typename T, bool LU>

@@ -7,6 +7,7 @@ Median of 5 timed runs after 2 warm-ups, CUDA events on the launching stream; ou
     python tools/measure_all.py [configs|sweep|paper|all] > gpurun_out/measure.json
 """
 import json
+import os
 import statistics
 import sys
 
@@ -15,6 +16,7 @@ import torch
 sys.path.insert(0, '.')
 import paper_1812_02056_b200 as sf  # noqa: E402
 import synth  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 
 PEAK64 = json.load(open("calib/peaks_fp64_tf32.json"))["fp64_dmma_tflops"]
 MP = json.load(open("MEASURED_PEAKS.json")) if __import__("os").path.exists("MEASURED_PEAKS.json") else {}
@@ -40,10 +42,13 @@ def run(kind, n, s, A, dtype=sf.SF_F64, reps=5, warm=2):
     torch.cuda.synchronize()
     assert int(info.item()) == 0
     ts = []
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", 0)))
+    clocks.start()
     for _ in range(reps):      # timed: no profiling hook, so repeated calls replay a CUDA graph
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(st); once(); e1.record(st); torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
+    ck = clocks.stop()
     sf.profile_enable(True)    # one extra, profiled (eager) run for the update / panel split
     sf.profile_collect()
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
@@ -61,7 +66,10 @@ def run(kind, n, s, A, dtype=sf.SF_F64, reps=5, warm=2):
     out = {"kind": kind, "n": n, "s": s, "dtype": "f32" if dtype == sf.SF_F32 else "f64", "ms": ms,
            "ms_all": ts, "eager_profiled_ms": eager_ms, "gflops": fl / ms / 1e6, "pct_peak": fl / ms / 1e9 / peak,
            "update_ms": up_ms / reps, "update_tflops": (up_fl / (up_ms * 1e-3) / 1e12) if up_ms else None,
-           "panel_ms": pan_ms}
+           "panel_ms": pan_ms, "clocks": ck,
+           # the main (flush) stream is busy update_ms of the eager step; the rest of the step
+           # is panel work the lookahead did not hide
+           "exposed_panel_ms": max(0.0, eager_ms - up_ms / reps - (prof["qr_r"][0] / reps))}
     if kind == "qr":
         out["R_ms"] = r_ms / reps
         out["R_tflops"] = r_fl / (r_ms * 1e-3) / 1e12 if r_ms else None
@@ -98,7 +106,7 @@ def configs():
 
 def sweep():
     A = synth.gen_torch("spd_scaled", 16384, 0)
-    return [run("chol", 16384, s, A) | {"config": f"configs[2] s-sweep"} for s in (64, 128, 168, 169, 256, 512, 1024)]
+    return [run("chol", 16384, s, A) | {"config": f"configs[2] s-sweep"} for s in (64, 128, 168, 169, 256, 512, 1024, 2048, 4096)]
 
 
 def paper():
