@@ -417,6 +417,7 @@ __device__ __forceinline__ void gemm_f64_body2(const GemmF64& p, int bid, int ve
   const int64_t rows = (p.M - i0 < BM) ? p.M - i0 : BM;
   const bool use_bulk = bulk && p.splits == 1 && (rows & 1) == 0;
   const double alpha = p.alpha;
+  const bool neg = alpha == -1.0;
   // logical i of atom a, MMA column c (0..7); logical j of atom b, MMA row r
   auto li = [&](int a, int c) { return !PA_ ? wm * WTM + 8 * a + c : wm * WTM + 16 * (a >> 1) + 2 * c + (a & 1); };
   auto lj = [&](int b, int r) { return !PB_ ? wn * 32 + 8 * b + r : wn * 32 + 16 * (b >> 1) + 2 * r + (b & 1); };
@@ -432,7 +433,10 @@ __device__ __forceinline__ void gemm_f64_body2(const GemmF64& p, int bid, int ve
         if (use_bulk) {
           const int64_t i = i0 + il, jd = j0 + jl + p.off;
           const bool in = MASK == kMaskNone || (MASK == kMaskLower ? i >= jd : i <= jd);
-          v = in ? alpha * v : -0.0;
+          // alpha = -1 (every flush): a sign flip on the integer pipe, not a DMUL on the FP64
+          // pipe the co-resident CTAs' DMMAs are using (bit-identical to alpha * v)
+          v = in ? (neg ? __longlong_as_double(__double_as_longlong(v) ^ (long long)0x8000000000000000ULL) : alpha * v)
+                 : -0.0;
         }
         Cs[jl * CP + il] = v;
       }

@@ -31,9 +31,6 @@ constexpr int kLeafT = 128;
 constexpr int kUCols = 64;   // U columns per CTA (static smem budget)
 constexpr unsigned kFull = 0xffffffffu;
 
-template <typename T> __device__ __forceinline__ T leaf_sqrt(T x);
-template <> __device__ __forceinline__ double leaf_sqrt<double>(double x) { return sqrt(x); }
-template <> __device__ __forceinline__ float leaf_sqrt<float>(float x) { return sqrtf(x); }
 
 __device__ __forceinline__ void leaf_fail(long long* fail, long long col1) {
   atomicMin((unsigned long long*)fail, (unsigned long long)col1);
@@ -94,8 +91,8 @@ __global__ void __launch_bounds__(NT) chol_leaf_rl_kernel(int64_t m, int w, cons
           if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
           break;
         }
-        const T Lcc = leaf_sqrt(d);
-        const T ri = T(1) / Lcc;                       // warp-uniform
+        const T ri = fast_rsqrt(d);                    // 1 / L_cc, warp-uniform (P11)
+        const T Lcc = d * ri;                          // sqrt(d)
         const T l = (lane == c) ? Lcc : a[c] * ri;     // lanes < c: unused (upper part)
         a[c] = l;
         if (lane < W) { lc[c & 1][lane] = l; Lt[c][lane] = (lane >= c) ? l : T(0); }
@@ -193,7 +190,7 @@ __global__ void __launch_bounds__(kLeafT) lu_leaf_warp_kernel(int64_t m, int64_t
           if (lane == 0 && blockIdx.x == 0) leaf_fail(fail, col0 + c + 1);
           break;
         }
-        const T ri = T(1) / Lcc;
+        const T ri = fast_rcp(Lcc);
         if (lane == c) {
           inv[c] = ri;
 #pragma unroll

@@ -68,40 +68,6 @@ template <> struct T2s<double> { using type = double2; };
 template <> struct T2s<float> { using type = float2; };
 template <typename T> using T2 = typename T2s<T>::type;
 
-// Reciprocal and reciprocal square root without the IEEE division / square-root subroutine
-// calls (a CALL makes the compiler save the live register window around it, ~32 doubles per
-// pivot step): hardware approximation + Newton steps, within 1 ulp of the correctly rounded
-// value (reading P11), exact for powers of two (the planted-factor tests).
-__device__ __forceinline__ double p64_rcp(double d) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-  double e = fma(-d, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-d, r, 1.0);
-  return fma(r, e, r);
-}
-__device__ __forceinline__ float p64_rcp(float d) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
-  const float e = fmaf(-d, r, 1.0f);
-  return fmaf(r, e, r);
-}
-__device__ __forceinline__ double p64_rsqrt(double d) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
-  // y <- y (3 - d y^2) / 2, twice
-  double h = 0.5 * d;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  return y;
-}
-__device__ __forceinline__ float p64_rsqrt(float d) {
-  float y;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(d));
-  const float h = 0.5f * d;
-  return y * fmaf(-h * y, y, 1.5f);
-}
-
 __device__ __forceinline__ void p64_fail(long long* fail, long long col1) {
   atomicMin((unsigned long long*)fail, (unsigned long long)col1);
 }
@@ -155,7 +121,7 @@ __device__ __forceinline__ bool p64_factor_quarter(T* D, T* inv, int o, int wq, 
       const T d = live ? d0 : T(1);
       T l[4], u[8];
       if (LU) {
-        const T ri = p64_rcp(d);
+        const T ri = fast_rcp(d);
         // multipliers L_ic of my rows (lane (p, cb)); pivot row U_cj = A_cj / L_cc of my
         // columns (lane (pr, q))
 #pragma unroll
@@ -168,7 +134,7 @@ __device__ __forceinline__ bool p64_factor_quarter(T* D, T* inv, int o, int wq, 
           for (int jj = 0; jj < 8; ++jj) blk[pi][jj] = (8 * q + jj > c) ? u[jj] : blk[pi][jj];
         }
       } else {
-        const T ri = p64_rsqrt(d);   // 1 / L_cc
+        const T ri = fast_rsqrt(d);   // 1 / L_cc
         const T Lcc = d * ri;
         // L_ic of my rows (lane (p, cb)); L_jc of my columns j = 8q + jj, row j held by lane
         // (2q + jj/4, cb) at row slot jj % 4
