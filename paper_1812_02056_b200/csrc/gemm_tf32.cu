@@ -504,6 +504,207 @@ gemm_tf32x3_pair_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_co
   }
 }
 
+// ------------------------------------------------------------------ persistent CTA-pair variant
+// One CTA pair per pair of SMs walks the tiles (static round-robin over the rasterized
+// order) with TWO TMEM accumulators (2 x 256 columns = all 512): the leader's MMAs for tile
+// t+1 run while both CTAs' epilogue warps drain tile t, so no tile pays its epilogue (or the
+// pipeline fill: the producer runs ahead into the next tile's slices) on the tensor pipe.
+// In-place tiles inside M, N (the flushes after the first) are added to C by bulk reduction
+// (cp.reduce.async.bulk .add.f32, one 512-byte column per lane from a double-buffered staging
+// chunk; masked entries add -0.0, which leaves every value bit-identical); other tiles take
+// the per-element load/add/store path.  fl(C + alpha*acc) is the same IEEE operation either way.
+// Barriers (leader-owned unless noted):
+//   full[s] / empty[s] (each CTA)   as in gemm_tf32x3_pair_kernel, slice counter across tiles
+//   tfull[a]  (each CTA)            the leader's commit after a tile's last MMA into accumulator a
+//   tempty[a] (leader)              8 arrivals: the 4 epilogue warps of each CTA, after reading a
+namespace t32q {
+constexpr int BM = 256, BN = 256, HALF = 128, BK = 16;
+constexpr int TILE = HALF * BK * 4;                 // one operand tile per CTA: 8 KB
+constexpr int STAGE_BYTES = 4 * TILE;               // 32 KB
+constexpr int STAGES = 5;
+constexpr int ECOLS = 32;                           // staging chunk: 128 rows x 32 columns = 16 KB
+constexpr int STG_BYTES = HALF * ECOLS * 4;
+constexpr int TMEM_COLS = 2 * BN;
+constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 2 * STG_BYTES + 1024 + 256;
+using TT = Tiles<BM, BN>;
+}  // namespace t32q
+
+__device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, const float* ssrc, int bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;\n" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(t32::THREADS, 1)
+gemm_tf32x3_pair_persist_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+                                const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
+                                Tf32Params p, int vecC, int ntiles, int tpc, const __grid_constant__ Raster rs) {
+  using namespace t32q;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  float* stg = (float*)(smem + STAGES * STAGE_BYTES);           // [2][ECOLS][HALF]
+  uint64_t* full = (uint64_t*)(smem + STAGES * STAGE_BYTES + 2 * STG_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;     // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  auto sAh = [&](int s) { return smem + s * STAGE_BYTES; };
+  auto sAl = [&](int s) { return smem + s * STAGE_BYTES + TILE; };
+  auto sBh = [&](int s) { return smem + s * STAGE_BYTES + 2 * TILE; };
+  auto sBl = [&](int s) { return smem + s * STAGE_BYTES + 3 * TILE; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  // tiles of this pair: tpc > 0 -> the contiguous run [pair*tpc, +tpc) of the rasterized order
+  // (pairs retire every tpc tiles, so the lookahead stream's panel kernels get SMs); tpc = 0
+  // -> every npairs-th tile (fully persistent)
+  const int t_first = tpc ? pair * tpc : pair, t_step = tpc ? 1 : npairs;
+  const int t_end = tpc ? min(ntiles, (pair + 1) * tpc) : ntiles;
+  const int TM = (int)((p.M + BM - 1) / BM), TN = (int)((p.N + BN - 1) / BN);
+  const int nkb = (int)((p.K + BK - 1) / BK);
+  const bool skip = p.fail && failed(p.fail);   // both CTAs still pass every barrier
+  auto tile_ij = [&](int t, int64_t& i0, int64_t& j0) {
+    int ti, tj;
+    if (rs.ngroups > 0) TT::tile_of_raster(p.mask, t, TM, p.off, rs, ti, tj);
+    else TT::tile_of(p.mask, t, TM, TN, p.off, ti, tj);
+    i0 = (int64_t)ti * BM; j0 = (int64_t)tj * BN;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tma_prefetch_desc(&mAh); tma_prefetch_desc(&mAl); tma_prefetch_desc(&mBh); tma_prefetch_desc(&mBl);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (each CTA: its halves of A and B), running ahead across tiles
+      const uint32_t lbar0 = smem_u32(&full[0]) & kPeerMask;
+      int g = 0;
+      for (int t = t_first; t < t_end; t += t_step) {
+        int64_t i0, j0;
+        tile_ij(t, i0, j0);
+        const int ya = (int)(i0 + rank * HALF), yb = (int)(j0 + rank * HALF);
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = g % STAGES;
+          mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+          const uint32_t lbar = lbar0 + s * 8;
+          tma_load_2d_pair(sAh(s), &mAh, lbar, kb * BK, ya);
+          tma_load_2d_pair(sAl(s), &mAl, lbar, kb * BK, ya);
+          tma_load_2d_pair(sBh(s), &mBh, lbar, kb * BK, yb);
+          tma_load_2d_pair(sBl(s), &mBl, lbar, kb * BK, yb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (leader): tile it into accumulator it & 1
+      constexpr uint32_t idesc = idesc_tf32(BM, BN);
+      int g = 0, it = 0;
+      for (int t = t_first; t < t_end; t += t_step, ++it) {
+        const int a = it & 1, u = it >> 1;
+        mbar_wait(&tempty[a], (u & 1) ^ 1);   // both CTAs' epilogues have drained accumulator a
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(a * BN);
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = g % STAGES;
+          mbar_wait(&full[s], (g / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t ah = smem_u32(sAh(s)), al = smem_u32(sAl(s)), bh = smem_u32(sBh(s)), bl = smem_u32(sBl(s));
+#pragma unroll
+          for (int k = 0; k < BK / t32::UMMA_K; ++k) {
+            const uint32_t o = k * t32::UMMA_K * 4;
+            umma_tf32_pair(d, umma_desc_sw64(ah + o), umma_desc_sw64(bh + o), idesc, (kb | k) != 0);
+            umma_tf32_pair(d, umma_desc_sw64(ah + o), umma_desc_sw64(bl + o), idesc, 1);
+            umma_tf32_pair(d, umma_desc_sw64(al + o), umma_desc_sw64(bh + o), idesc, 1);
+          }
+          umma_commit_pair(&empty[s]);
+        }
+        umma_commit_pair(&tfull[a]);
+      }
+    }
+  } else {
+    // ---------------- epilogue: warps 2..5 -> TMEM lanes 32*(warp%4) .. +31 = CTA rows
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const int row = q * 32 + lane;
+    const uint32_t tempty_leader = smem_u32(&tempty[0]) & kPeerMask;
+    int it = 0, nchunk = 0;
+    for (int t = t_first; t < t_end; t += t_step, ++it) {
+      const int a = it & 1, u = it >> 1;
+      int64_t i0, j0;
+      tile_ij(t, i0, j0);
+      const int64_t r0 = i0 + rank * HALF, i = r0 + row;
+      const bool bulk = vecC && !skip && (r0 + HALF <= p.M) && (j0 + BN <= p.N);
+      mbar_wait(&tfull[a], u & 1);
+      tc_fence_after();
+      const uint32_t tacc = tmem + lane_base + (uint32_t)(a * BN);
+      for (int c = 0; c < BN; c += ECOLS) {
+        if (!bulk && j0 + c >= p.N) break;
+        float v[32];
+        tmem_ld32(tacc + (uint32_t)c, v);
+        if (bulk) {
+          float* buf = stg + (nchunk & 1) * (ECOLS * HALF);
+          if (nchunk >= 2) {
+            if (warp == 2) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");   // buf's last reduce has read it
+            epi_bar_sync();
+          }
+#pragma unroll
+          for (int uu = 0; uu < 32; ++uu) {
+            const int64_t j = j0 + c + uu;
+            const bool in = p.mask == kMaskNone || (p.mask == kMaskLower ? i >= j + p.off : i <= j + p.off);
+            buf[uu * HALF + row] = in ? p.alpha * v[uu] : -0.f;
+          }
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          epi_bar_sync();
+          if (warp == 2) {
+            bulk_reduce_add_f32(p.C + r0 + (j0 + c + lane) * p.ldc, buf + lane * HALF, HALF * 4);
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          }
+          ++nchunk;
+        } else if (i < p.M && !skip) {
+          float cin[32];
+#pragma unroll
+          for (int uu = 0; uu < 32; ++uu) {
+            const int64_t j = j0 + c + uu;
+            const bool in = j < p.N && (p.mask == kMaskNone || (p.mask == kMaskLower ? i >= j + p.off : i <= j + p.off));
+            cin[uu] = (in && p.beta) ? __ldcg(p.Cin + i + j * p.ldcin) : 0.f;
+          }
+#pragma unroll
+          for (int uu = 0; uu < 32; ++uu) {
+            const int64_t j = j0 + c + uu;
+            const bool in = j < p.N && (p.mask == kMaskNone || (p.mask == kMaskLower ? i >= j + p.off : i <= j + p.off));
+            if (in) __stcg(p.C + i + j * p.ldc, fmaf(p.alpha, v[uu], cin[uu]));
+          }
+        }
+      }
+      // accumulator a is free once every epilogue warp of both CTAs has read it
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + a * 8);
+    }
+    if (warp == 2) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+  }
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
 // ------------------------------------------------------------------ split kernel
 // x -> (rna_tf32(x), rna_tf32(x - hi)), transposed from column-major (m x k, ld) to K-major
 // (row i: k contiguous values at H + i*ldk).  32 x 32 tiles through shared memory.
@@ -652,6 +853,47 @@ static cudaError_t launch_pair(const Tf32Gemm& g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+static bool persist_on() {
+  static int on = [] { const char* e = getenv("SF_TF32_PERSIST"); return e ? atoi(e) : 1; }();
+  return on != 0;
+}
+
+static cudaError_t launch_pair_persist(const Tf32Gemm& g, cudaStream_t st) {
+  using namespace t32q;
+  const int TM = (int)((g.M + BM - 1) / BM), TN = (int)((g.N + BN - 1) / BN);
+  const int ntiles = TT::count(g.mask, TM, TN, g.off);
+  if (ntiles == 0) return cudaSuccess;
+  CUtensorMap mAh, mAl, mBh, mBl;
+  cudaError_t e;
+  if ((e = make_map(&mAh, g.Ah, g.K, g.M, g.ldk_a, HALF)) != cudaSuccess) return e;
+  if ((e = make_map(&mAl, g.Al, g.K, g.M, g.ldk_a, HALF)) != cudaSuccess) return e;
+  if ((e = make_map(&mBh, g.Bh, g.K, g.N, g.ldk_b, HALF)) != cudaSuccess) return e;
+  if ((e = make_map(&mBl, g.Bl, g.K, g.N, g.ldk_b, HALF)) != cudaSuccess) return e;
+  static bool attr = false;
+  static int sms = 148;
+  if (!attr) {
+    e = cudaFuncSetAttribute(gemm_tf32x3_pair_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    attr = true;
+  }
+  Tf32Params p{g.M, g.N, g.K, g.Cin, g.ldcin, g.C, g.ldc, g.off, g.mask, g.fail, g.alpha, g.beta};
+  // bulk-reduce epilogue: in place, 16-byte aligned columns
+  const int vecC = g.beta && g.Cin == g.C && g.ldcin == g.ldc && (g.ldc % 4) == 0 && ((uintptr_t)g.C % 16) == 0;
+  static int gb_env = [] { const char* e = getenv("SF_TF32_RASTER"); return e ? atoi(e) : -1; }();
+  Raster rs;
+  const int gb = gb_env >= 0 ? gb_env : 8;
+  if (gb > 0) TT::make_raster(g.mask, TM, TN, g.off, gb, rs);
+  static int tpc = [] { const char* e = getenv("SF_TF32_TPC"); return e ? atoi(e) : 4; }();
+  const int npairs = tpc > 0 ? (ntiles + tpc - 1) / tpc : (ntiles < sms / 2 ? ntiles : sms / 2);
+  gemm_tf32x3_pair_persist_kernel<<<2 * npairs, t32::THREADS, SMEM, st>>>(mAh, mAl, mBh, mBl, p, vecC, ntiles, tpc,
+                                                                          rs);
+  count_launch();
+  return cudaGetLastError();
+}
+
 static bool pair_on() {
   static int on = [] { const char* e = getenv("SF_TF32_PAIR"); return e ? atoi(e) : 1; }();
   return on != 0;
@@ -665,7 +907,7 @@ cudaError_t gemm_tf32x3(const Tf32Gemm& g, cudaStream_t st) {
   // narrow updates (the panel recursion's corrections) take a narrower tile
   if (g.N <= 64) return launch_bn<64>(g, st);
   if (g.N <= 128) return launch_bn<128>(g, st);
-  if (pair_on()) return launch_pair(g, st);   // wide flushes: CTA pairs (cta_group::2)
+  if (pair_on()) return persist_on() ? launch_pair_persist(g, st) : launch_pair(g, st);   // wide: CTA pairs
   return launch_bn<256>(g, st);
 }
 
