@@ -853,9 +853,10 @@ static cudaError_t launch_pair(const Tf32Gemm& g, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-static bool persist_on() {
-  static int on = [] { const char* e = getenv("SF_TF32_PERSIST"); return e ? atoi(e) : 1; }();
-  return on != 0;
+// persistent pairs for flushes of at least SF_TF32_PERSIST_MIN tiles (0 = always; -1 = never)
+static bool persist_for(int ntiles) {
+  static int mn = [] { const char* e = getenv("SF_TF32_PERSIST_MIN"); return e ? atoi(e) : 0; }();
+  return mn >= 0 && ntiles >= mn;
 }
 
 static cudaError_t launch_pair_persist(const Tf32Gemm& g, cudaStream_t st) {
@@ -886,8 +887,13 @@ static cudaError_t launch_pair_persist(const Tf32Gemm& g, cudaStream_t st) {
   Raster rs;
   const int gb = gb_env >= 0 ? gb_env : 8;
   if (gb > 0) TT::make_raster(g.mask, TM, TN, g.off, gb, rs);
-  static int tpc = [] { const char* e = getenv("SF_TF32_TPC"); return e ? atoi(e) : 4; }();
-  const int npairs = tpc > 0 ? (ntiles + tpc - 1) / tpc : (ntiles < sms / 2 ? ntiles : sms / 2);
+  static int tpc = [] { const char* e = getenv("SF_TF32_TPC"); return e ? atoi(e) : 0; }();
+  // SF_TF32_RESERVE SMs are left to concurrent work (the lookahead panel) in persistent mode
+  // (measured: 16 -> cfg5 fp32 505 ms, cfg3 fp32 22.1 ms; 0 -> 505 / 23.4; 32 -> 518 / 21.6)
+  static int reserve = [] { const char* e = getenv("SF_TF32_RESERVE"); return e ? atoi(e) : 16; }();
+  int maxp = (sms - reserve) / 2;
+  if (maxp < 1) maxp = 1;
+  const int npairs = tpc > 0 ? (ntiles + tpc - 1) / tpc : (ntiles < maxp ? ntiles : maxp);
   gemm_tf32x3_pair_persist_kernel<<<2 * npairs, t32::THREADS, SMEM, st>>>(mAh, mAl, mBh, mBl, p, vecC, ntiles, tpc,
                                                                           rs);
   count_launch();
@@ -907,7 +913,10 @@ cudaError_t gemm_tf32x3(const Tf32Gemm& g, cudaStream_t st) {
   // narrow updates (the panel recursion's corrections) take a narrower tile
   if (g.N <= 64) return launch_bn<64>(g, st);
   if (g.N <= 128) return launch_bn<128>(g, st);
-  if (pair_on()) return persist_on() ? launch_pair_persist(g, st) : launch_pair(g, st);   // wide: CTA pairs
+  if (pair_on()) {   // wide flushes: CTA pairs
+    const int ntiles = t32p::TT::count(g.mask, (int)((g.M + 255) / 256), (int)((g.N + 255) / 256), g.off);
+    return persist_for(ntiles) ? launch_pair_persist(g, st) : launch_pair(g, st);
+  }
   return launch_bn<256>(g, st);
 }
 

@@ -389,7 +389,54 @@ template <> struct LL<float> {
   }
 };
 
+// Gather the Q cluster sums of columns c..w-1 (cnt = Q * wc LL words, poll until each carries
+// epoch ep) into cval[qq * w + j].  A thread's words are requested 4 at a time before any is
+// checked, so a poll pass costs one L2 round trip, not one per word (a thread owns up to
+// ceil(Q*w / 256) words).
 template <typename T>
+__device__ __forceinline__ void ll_gather(const unsigned long long* ll, int buf, int Q, int w, int c, int wc, int cnt,
+                                          unsigned ep, T* cval, int tid) {
+  constexpr int B = 4;
+  for (int base = tid; base < cnt; base += B * kMgsThreads) {
+    T v[B];
+    bool got[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int idx = base + u * kMgsThreads;
+      got[u] = idx >= cnt;
+      if (!got[u]) {
+        const int qq = idx / wc, j = c + idx % wc;
+        got[u] = LL<T>::get(ll + LL<T>::kWords * ((size_t)(buf * Q + qq) * w + j), ep, v[u]);
+      }
+    }
+    bool all = true;
+#pragma unroll
+    for (int u = 0; u < B; ++u) all = all && got[u];
+    while (!all) {
+      all = true;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        if (!got[u]) {
+          const int idx = base + u * kMgsThreads, qq = idx / wc, j = c + idx % wc;
+          got[u] = LL<T>::get(ll + LL<T>::kWords * ((size_t)(buf * Q + qq) * w + j), ep, v[u]);
+          all = all && got[u];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int idx = base + u * kMgsThreads;
+      if (idx < cnt) cval[(idx / wc) * w + c + idx % wc] = v[u];
+    }
+  }
+}
+
+// NR = the rows of its column half a thread keeps in registers (kMgsRPT: all of them); the
+// other kMgsRPT - NR live in shared memory (xs, one slot per thread: conflict-free).  With
+// NR = 32 the CTA needs ~31K registers instead of the whole register file, so flush CTAs
+// (the concurrent trailing update, 15K registers each) share the SM with the panel instead
+// of losing a third of the GPU to it for the whole panel factorization.
+template <typename T, int NR>
 __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w, int RB, const T* __restrict__ src,
                                                                 int64_t lds, T* __restrict__ dst, int64_t ldd,
                                                                 int64_t col0, const T* tolp,
@@ -405,27 +452,29 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
   const int CL = (int)cluster.num_blocks(), k = (int)cluster.block_rank();
   const int tid = threadIdx.x;
   const int G = gridDim.x, g = blockIdx.x, Q = G / CL, q = g / CL;
+  T* xs = cval + (((size_t)Q * w + 1) & ~(size_t)1);   // rows NR.. of each thread: xs[(r - NR) * kMgsThreads + tid]
   const int64_t r0 = (int64_t)g * RB;
   const int rows = (int)((r0 + RB <= n) ? RB : (n > r0 ? n - r0 : 0));
   const T tol = __ldcg(tolp);
   const int cp = tid >> 1, h = tid & 1;        // my column and half
   const int rbase = h * kMgsRPT;
   const bool mine = cp < w;
-  T x[kMgsRPT];
+  T x[NR];
+  auto X = [&](int r) -> T& { return r < NR ? x[r < NR ? r : 0] : xs[(size_t)(r - NR) * kMgsThreads + tid]; };
 #pragma unroll
   for (int r = 0; r < kMgsRPT; ++r) {
     const int rr = rbase + r;
-    x[r] = (mine && rr < rows) ? __ldcg(src + r0 + rr + (int64_t)cp * lds) : T(0);
+    X(r) = (mine && rr < rows) ? __ldcg(src + r0 + rr + (int64_t)cp * lds) : T(0);
   }
   if (cp == 0) {
 #pragma unroll
-    for (int r = 0; r < kMgsRPT; ++r) vs[h * QP + r] = x[r];
+    for (int r = 0; r < kMgsRPT; ++r) vs[h * QP + r] = X(r);
   }
   __syncthreads();
   {
     T acc = T(0);
 #pragma unroll
-    for (int r = 0; r < kMgsRPT; ++r) acc = fma(vs[h * QP + r], x[r], acc);
+    for (int r = 0; r < kMgsRPT; ++r) acc = fma(vs[h * QP + r], X(r), acc);
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
     if (mine && h == 0) mypart[0][cp] = acc;
   }
@@ -441,13 +490,7 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
       LL<T>::put(ll + LL<T>::kWords * ((size_t)(buf * Q + q) * w + j), a, ep);
     }
     const int wc = w - c, cnt = Q * wc;
-    for (int idx = tid; idx < cnt; idx += kMgsThreads) {
-      const int qq = idx / wc, j = c + idx % wc;
-      const unsigned long long* p = ll + LL<T>::kWords * ((size_t)(buf * Q + qq) * w + j);
-      T v;
-      while (!LL<T>::get(p, ep, v)) {}
-      cval[qq * w + j] = v;
-    }
+    ll_gather<T>(ll, buf, Q, w, c, wc, cnt, ep, cval, tid);
     __syncthreads();
     for (int j = c + tid; j < w; j += kMgsThreads) {
       T a = T(0);
@@ -455,20 +498,21 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
       gsum[j] = a;
     }
     __syncthreads();
-    const T nv = dsqrt(gsum[c]);
+    // 1/||v_c|| without the IEEE sqrt / division subroutines (reading P11); ||v_c|| for R3
+    const T rnv = fast_rsqrt(gsum[c]);
+    const T nv = gsum[c] * rnv;
     if (!(nv >= tol)) {
       if (g == 0 && tid == 0) record_fail(fail, col0 + c + 1);
       ok = false;
       break;
     }
-    const T rnv = T(1) / nv;
     if (cp == c) {
 #pragma unroll
-      for (int r = 0; r < kMgsRPT; ++r) { x[r] = x[r] * rnv; qs[h * QP + r] = x[r]; }
+      for (int r = 0; r < kMgsRPT; ++r) { X(r) = X(r) * rnv; qs[h * QP + r] = X(r); }
     }
     if (cp == c + 1) {
 #pragma unroll
-      for (int r = 0; r < kMgsRPT; ++r) vs[h * QP + r] = x[r];
+      for (int r = 0; r < kMgsRPT; ++r) vs[h * QP + r] = X(r);
     }
     __syncthreads();
     const bool act = mine && cp > c;
@@ -479,8 +523,9 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
 #pragma unroll
       for (int r = 0; r < kMgsRPT; ++r) {
         const T qr = qs[h * QP + r];
-        x[r] = fma(-qr, coef, x[r]);                         // v_cp -= q_c (q_c^T v_cp)
-        acc = fma(fma(-qr, cn, vs[h * QP + r]), x[r], acc);  // <v_{c+1}, v_cp> (both updated)
+        const T xr = fma(-qr, coef, X(r));                   // v_cp -= q_c (q_c^T v_cp)
+        X(r) = xr;
+        acc = fma(fma(-qr, cn, vs[h * QP + r]), xr, acc);    // <v_{c+1}, v_cp> (both updated)
       }
     }
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
@@ -491,7 +536,7 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
 #pragma unroll
   for (int r = 0; r < kMgsRPT; ++r) {
     const int rr = rbase + r;
-    if (rr < rows) dst[r0 + rr + (int64_t)cp * ldd] = x[r];
+    if (rr < rows) dst[r0 + rr + (int64_t)cp * ldd] = X(r);
   }
 }
 
@@ -551,13 +596,7 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_smem_kernel(int64_t n, 
       LL<T>::put(ll + LL<T>::kWords * ((size_t)(buf * Q + q) * w + j), a, ep);
     }
     const int wc = w - c, cnt = Q * wc;
-    for (int idx = tid; idx < cnt; idx += kMgsThreads) {
-      const int qq = idx / wc, j = c + idx % wc;
-      const unsigned long long* p = ll + LL<T>::kWords * ((size_t)(buf * Q + qq) * w + j);
-      T v;
-      while (!LL<T>::get(p, ep, v)) {}
-      cval[qq * w + j] = v;
-    }
+    ll_gather<T>(ll, buf, Q, w, c, wc, cnt, ep, cval, tid);
     __syncthreads();
     for (int j = c + tid; j < w; j += kMgsThreads) {
       T a = T(0);
@@ -565,7 +604,9 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_smem_kernel(int64_t n, 
       gsum[j] = a;
     }
     __syncthreads();
-    const T nv = dsqrt(gsum[c]);
+    // 1/||v_c|| without the IEEE sqrt / division subroutines (reading P11); ||v_c|| for R3
+    const T rnv = fast_rsqrt(gsum[c]);
+    const T nv = gsum[c] * rnv;
     if (!(nv >= tol)) {
       if (g == 0 && tid == 0) record_fail(fail, col0 + c + 1);
       ok = false;
@@ -574,7 +615,6 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_smem_kernel(int64_t n, 
     // q_c = v_c / ||v_c|| and the updated v_{c+1} as shared vectors, then a THREAD per later
     // column (no per-column warp reduction): v_cp -= q_c (q_c^T v_cp) row by row, with its
     // dot against the updated v_{c+1} formed in the same pass (the next partial Gram row)
-    const T rnv = T(1) / nv;
     const T cn = (c + 1 < w) ? gsum[c + 1] * rnv : T(0);
     for (int r = tid; r < RB; r += kMgsThreads) {
       const T qr = V[(size_t)c * RB + r] * rnv;
@@ -676,15 +716,22 @@ static bool mgs_cooperative() {
 // Grid for the LL kernels, or G = 0 when they do not apply (then the flag-exchange kernels).
 // reg: the register-resident variant (w <= 128, <= 128 rows per CTA); otherwise the
 // shared-memory one (the panel rows + exchange buffers within 220 KB per CTA).
+// register rows of the LL kernel's thread (SF_MGS_NR: 64 = all, 32 = half in shared memory)
+static int mgs_nr() {
+  static const int v = [] { const char* e = getenv("SF_MGS_NR"); return (e && atoi(e) == 64) ? 64 : 32; }();
+  return v;
+}
+
 template <typename T>
 static LLGeom ll_geom(int64_t n, int w, bool reg) {
   LLGeom r;
+  const int nr = mgs_nr();
   if (getenv("SF_MGS_NOLL") != nullptr) return r;
   if (reg && w > 128) return r;
   const int64_t G0 = (n + 2 * kMgsRPT - 1) / (2 * kMgsRPT);
   static int maxcl[2][9] = {{-1, -1, -1, -1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1, -1, -1, -1}};
   auto dyn_for = [&](int G, int CL) -> size_t {
-    if (reg) return sizeof(T) * (size_t)(G / CL) * (size_t)w;
+    if (reg) return sizeof(T) * (((size_t)(G / CL) * (size_t)w + 1) / 2 * 2 + (size_t)(kMgsRPT - nr) * kMgsThreads);
     const int RB = (int)((n + G - 1) / G);
     return sizeof(T) * ((size_t)RB * w + 3 * (size_t)w + (size_t)(G / CL) * w + 2 * (size_t)RB);
   };
@@ -702,8 +749,9 @@ static LLGeom ll_geom(int64_t n, int w, bool reg) {
       at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      const void* kf = reg ? (const void*)qr_mgs_ll_kernel<T> : (const void*)qr_mgs_ll_smem_kernel<T>;
-      if (!reg) cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      const void* kf = reg ? (nr == 64 ? (const void*)qr_mgs_ll_kernel<T, 64> : (const void*)qr_mgs_ll_kernel<T, 32>)
+                           : (const void*)qr_mgs_ll_smem_kernel<T>;
+      cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, reg ? 220 * 1024 : (int)dyn);
       int m = 0;
       if (cudaOccupancyMaxActiveClusters(&m, kf, &cfg) != cudaSuccess) { cudaGetLastError(); m = 0; }
       if (reg) mc = m;
@@ -755,7 +803,9 @@ cudaError_t qr_mgs_panel(int64_t n, int w, const T* src, int64_t lds, T* dst, in
     cfg.numAttrs = mgs_cooperative() ? 2 : 1;
     int RB = lg.RB;
     count_launch();
-    if (lreg) return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
+    if (lreg && mgs_nr() == 64)
+      return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 64>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
+    if (lreg) return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 32>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
     return cudaLaunchKernelEx(&cfg, qr_mgs_ll_smem_kernel<T>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
   }
   MgsGeom g = mgs_geom(n, w, (int)sizeof(T));
