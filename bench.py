@@ -391,7 +391,8 @@ def main():
         peak = bf16 * 1.1 / 2.25
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
-                    "kernel": "gemm_tf32x3_kernel (flush update, tcgen05.mma kind::tf32, 3xTF32: K' = 3s)",
+                    "kernel": "gemm_tf32x3_pair_persist_kernel (flush update, tcgen05.mma.cta_group::2 kind::tf32, "
+                              "3xTF32: K' = 3s)",
                     "flops_counted": "tensor flops executed = 3 x useful (hi.hi + hi.lo + lo.hi)",
                     "useful_achieved": achieved / 3.0 if achieved else None,
                     "peak_source": ("measured: MEASURED_PEAKS.json bf16_tflops_sustained x 1.1/2.25 (nominal "
@@ -400,7 +401,8 @@ def main():
         peak = peaks.get("fp64_dmma_tflops")
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": (achieved / peak) if (achieved and peak) else None, "traffic": traffic,
-                    "kernel": "gemm_f64_kernel (flush update, DMMA.8x8x4)" + (", rank 0" if ws > 1 else ""),
+                    "kernel": "gemm_f64v2_kernel (flush update, DMMA.8x8x4, 64x64 tiles, bulk-reduce epilogue)"
+                              + (", rank 0" if ws > 1 else ""),
                     "peak_source": "measured: calib/peaks_fp64_tf32.json fp64_dmma_tflops (DMMA microbenchmark, "
                                    "this pool's B200); MEASURED_PEAKS.json has no fp64 entry"}
     roofline.update({"launches_per_step": upd_n / args.steps if args.steps else None,

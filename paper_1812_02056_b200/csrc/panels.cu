@@ -26,6 +26,8 @@
 
 #include <cooperative_groups.h>
 
+#include <stdio.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -431,18 +433,17 @@ __device__ __forceinline__ void ll_gather(const unsigned long long* ll, int buf,
   }
 }
 
-// NR = the rows of its column half a thread keeps in registers (kMgsRPT: all of them); the
-// other kMgsRPT - NR live in shared memory (xs, one slot per thread: conflict-free).  With
-// NR = 32 the CTA needs ~31K registers instead of the whole register file, so flush CTAs
-// (the concurrent trailing update, 15K registers each) share the SM with the panel instead
-// of losing a third of the GPU to it for the whole panel factorization.
-template <typename T, int NR>
+// RPT = rows of its column half a thread owns (the CTA holds 2 * RPT rows), NR of them in
+// registers and RPT - NR in shared memory (xs, one slot per thread: conflict-free).
+// RPT = 128, NR = 64 halves the number of CTAs (SMs) the panel occupies at the same register
+// use per CTA, so the concurrent flush keeps more SMs (measured: DESIGN.md §5 K7).
+template <typename T, int RPT, int NR>
 __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w, int RB, const T* __restrict__ src,
                                                                 int64_t lds, T* __restrict__ dst, int64_t ldd,
                                                                 int64_t col0, const T* tolp,
                                                                 unsigned long long* ll, long long* fail) {
   if (failed(fail)) return;      // stable during the launch: every CTA of a cluster agrees
-  constexpr int QP = kMgsRPT + 2;
+  constexpr int QP = RPT + 2;
   __shared__ T qs[2 * QP], vs[2 * QP];
   __shared__ T gsum[128];
   __shared__ T mypart[2][128];
@@ -457,26 +458,28 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
   const int rows = (int)((r0 + RB <= n) ? RB : (n > r0 ? n - r0 : 0));
   const T tol = __ldcg(tolp);
   const int cp = tid >> 1, h = tid & 1;        // my column and half
-  const int rbase = h * kMgsRPT;
+  const int rbase = h * RPT;
   const bool mine = cp < w;
   T x[NR];
   auto X = [&](int r) -> T& { return r < NR ? x[r < NR ? r : 0] : xs[(size_t)(r - NR) * kMgsThreads + tid]; };
 #pragma unroll
-  for (int r = 0; r < kMgsRPT; ++r) {
+  for (int r = 0; r < RPT; ++r) {
     const int rr = rbase + r;
     X(r) = (mine && rr < rows) ? __ldcg(src + r0 + rr + (int64_t)cp * lds) : T(0);
   }
   if (cp == 0) {
 #pragma unroll
-    for (int r = 0; r < kMgsRPT; ++r) vs[h * QP + r] = X(r);
+    for (int r = 0; r < RPT; ++r) vs[h * QP + r] = X(r);
   }
   __syncthreads();
   {
-    T acc = T(0);
+    // four interleaved partial sums: the dot product's dependency chain is RPT/4 fmas deep
+    T acc[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-    for (int r = 0; r < kMgsRPT; ++r) acc = fma(vs[h * QP + r], X(r), acc);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    if (mine && h == 0) mypart[0][cp] = acc;
+    for (int r = 0; r < RPT; ++r) acc[r & 3] = fma(vs[h * QP + r], X(r), acc[r & 3]);
+    T a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    a += __shfl_xor_sync(0xffffffffu, a, 1);
+    if (mine && h == 0) mypart[0][cp] = a;
   }
 
   bool ok = true;
@@ -508,33 +511,34 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
     }
     if (cp == c) {
 #pragma unroll
-      for (int r = 0; r < kMgsRPT; ++r) { X(r) = X(r) * rnv; qs[h * QP + r] = X(r); }
+      for (int r = 0; r < RPT; ++r) { X(r) = X(r) * rnv; qs[h * QP + r] = X(r); }
     }
     if (cp == c + 1) {
 #pragma unroll
-      for (int r = 0; r < kMgsRPT; ++r) vs[h * QP + r] = X(r);
+      for (int r = 0; r < RPT; ++r) vs[h * QP + r] = X(r);
     }
     __syncthreads();
     const bool act = mine && cp > c;
-    T acc = T(0);
+    T acc[4] = {T(0), T(0), T(0), T(0)};   // interleaved partial sums (short dependency chains)
     if (act) {
       const T coef = gsum[cp] * rnv;                        // q_c^T v_cp
       const T cn = (c + 1 < w) ? gsum[c + 1] * rnv : T(0);  // q_c^T v_{c+1}
 #pragma unroll
-      for (int r = 0; r < kMgsRPT; ++r) {
+      for (int r = 0; r < RPT; ++r) {
         const T qr = qs[h * QP + r];
         const T xr = fma(-qr, coef, X(r));                   // v_cp -= q_c (q_c^T v_cp)
         X(r) = xr;
-        acc = fma(fma(-qr, cn, vs[h * QP + r]), xr, acc);    // <v_{c+1}, v_cp> (both updated)
+        acc[r & 3] = fma(fma(-qr, cn, vs[h * QP + r]), xr, acc[r & 3]);   // <v_{c+1}, v_cp>
       }
     }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    if (act && h == 0 && c + 1 < w) mypart[buf ^ 1][cp] = acc;
+    T a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    a += __shfl_xor_sync(0xffffffffu, a, 1);
+    if (act && h == 0 && c + 1 < w) mypart[buf ^ 1][cp] = a;
   }
   cluster.sync();   // no CTA leaves while a cluster peer may still read its shared memory
   if (!ok || !mine) return;
 #pragma unroll
-  for (int r = 0; r < kMgsRPT; ++r) {
+  for (int r = 0; r < RPT; ++r) {
     const int rr = rbase + r;
     if (rr < rows) dst[r0 + rr + (int64_t)cp * ldd] = X(r);
   }
@@ -716,28 +720,29 @@ static bool mgs_cooperative() {
 // Grid for the LL kernels, or G = 0 when they do not apply (then the flag-exchange kernels).
 // reg: the register-resident variant (w <= 128, <= 128 rows per CTA); otherwise the
 // shared-memory one (the panel rows + exchange buffers within 220 KB per CTA).
-// register rows of the LL kernel's thread (SF_MGS_NR: 64 = all, 32 = half in shared memory)
-static int mgs_nr() {
-  static const int v = [] { const char* e = getenv("SF_MGS_NR"); return (e && atoi(e) == 64) ? 64 : 32; }();
+// rows per thread of the LL kernel (SF_MGS_RPT: 64 = all in registers, 128 = half in shared
+// memory: twice the rows per CTA, half the CTAs)
+static int mgs_rpt() {
+  static const int v = [] { const char* e = getenv("SF_MGS_RPT"); return (e && atoi(e) == 128) ? 128 : 64; }();
   return v;
 }
 
 template <typename T>
 static LLGeom ll_geom(int64_t n, int w, bool reg) {
   LLGeom r;
-  const int nr = mgs_nr();
+  const int rpt = reg ? mgs_rpt() : kMgsRPT;
   if (getenv("SF_MGS_NOLL") != nullptr) return r;
   if (reg && w > 128) return r;
-  const int64_t G0 = (n + 2 * kMgsRPT - 1) / (2 * kMgsRPT);
+  const int64_t G0 = (n + 2 * rpt - 1) / (2 * rpt);
   static int maxcl[2][9] = {{-1, -1, -1, -1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1, -1, -1, -1}};
   auto dyn_for = [&](int G, int CL) -> size_t {
-    if (reg) return sizeof(T) * (((size_t)(G / CL) * (size_t)w + 1) / 2 * 2 + (size_t)(kMgsRPT - nr) * kMgsThreads);
+    if (reg) return sizeof(T) * (((size_t)(G / CL) * (size_t)w + 1) / 2 * 2 + (size_t)(rpt - 64) * kMgsThreads);
     const int RB = (int)((n + G - 1) / G);
     return sizeof(T) * ((size_t)RB * w + 3 * (size_t)w + (size_t)(G / CL) * w + 2 * (size_t)RB);
   };
   auto fits = [&](int CL, int G) -> bool {
     const size_t dyn = dyn_for(G, CL);
-    if (dyn > 220 * 1024) return false;
+    if (dyn > (reg ? 200 : 220) * 1024) return false;
     int& mc = maxcl[reg ? 0 : 1][CL];
     if (mc < 0 || !reg) {   // the shared-memory variant's occupancy depends on its size
       cudaLaunchConfig_t cfg = {};
@@ -749,11 +754,16 @@ static LLGeom ll_geom(int64_t n, int w, bool reg) {
       at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      const void* kf = reg ? (nr == 64 ? (const void*)qr_mgs_ll_kernel<T, 64> : (const void*)qr_mgs_ll_kernel<T, 32>)
+      const void* kf = reg ? (rpt == 64 ? (const void*)qr_mgs_ll_kernel<T, 64, 64> : (const void*)qr_mgs_ll_kernel<T, 128, 64>)
                            : (const void*)qr_mgs_ll_smem_kernel<T>;
-      cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, reg ? 220 * 1024 : (int)dyn);
+      // (the register variant's dynamic size varies a little with G: allow up to 200 KB)
+      cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, reg ? 200 * 1024 : (int)dyn);
       int m = 0;
-      if (cudaOccupancyMaxActiveClusters(&m, kf, &cfg) != cudaSuccess) { cudaGetLastError(); m = 0; }
+      cudaError_t oe = cudaOccupancyMaxActiveClusters(&m, kf, &cfg);
+      if (getenv("SF_MGS_DEBUG"))
+        fprintf(stderr, "mgs geom: reg %d rpt %d CL %d G %d dyn %zu -> max clusters %d (%s)\n", (int)reg, rpt, CL, G,
+                dyn, m, cudaGetErrorString(oe));
+      if (oe != cudaSuccess) { cudaGetLastError(); m = 0; }
       if (reg) mc = m;
       else return G / CL <= m;
     }
@@ -771,7 +781,7 @@ static LLGeom ll_geom(int64_t n, int w, bool reg) {
   if (G == 0) return r;
   r.G = G; r.CL = CL;
   r.RB = (int)((n + G - 1) / G);
-  if (r.RB > (reg ? 2 * kMgsRPT : 32 * kMgsRJ)) return LLGeom{};
+  if (r.RB > (reg ? 2 * rpt : 32 * kMgsRJ)) return LLGeom{};
   r.dyn = dyn_for(G, CL);
   return r;
 }
@@ -803,9 +813,10 @@ cudaError_t qr_mgs_panel(int64_t n, int w, const T* src, int64_t lds, T* dst, in
     cfg.numAttrs = mgs_cooperative() ? 2 : 1;
     int RB = lg.RB;
     count_launch();
-    if (lreg && mgs_nr() == 64)
-      return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 64>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
-    if (lreg) return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 32>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
+    if (lreg && mgs_rpt() == 64)
+      return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 64, 64>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
+    if (lreg)
+      return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 128, 64>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
     return cudaLaunchKernelEx(&cfg, qr_mgs_ll_smem_kernel<T>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
   }
   MgsGeom g = mgs_geom(n, w, (int)sizeof(T));
