@@ -51,8 +51,13 @@ def build(force=False, verbose=False):
         return LIB
     os.makedirs(os.path.join(PKG, "build"), exist_ok=True)
 
+    newest_header = max(os.path.getmtime(h) for h in headers())
+
     def compile_one(src):
         obj = os.path.join(PKG, "build", os.path.basename(src) + ".o")
+        # incremental: an object newer than its source and every header is reused
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), newest_header):
+            return src, obj, subprocess.CompletedProcess([], 0, "", "")
         cmd = [NVCC, *ARCH, *[f for f in FLAGS if f != "-shared"], "-c",
                "-I", os.path.join(ROOT, "include"), "-I", NCCL_INC, "-o", obj, src]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -193,6 +193,107 @@ static int64_t lu_la_min_m() {
   return v;
 }
 
+// Two-deep lookahead for LU (SF_LU_LA2; default on for fp64: cfg2 6.21 -> 5.57 ms, bench).  The flush of panel p is split three ways:
+//   F1(p): the L-shaped region panel p+1 reads (its columns, rows >= c; its U rows, columns
+//          right of it) — on the panel stream, right before panel p+1;
+//   F2(p): the L-shaped region of panel p+2 — first on the main stream, so F1(p+1) (same
+//          region, next contribution) can start as soon as it and panel p+1 are done;
+//   F3(p): the rest, rows and columns >= the start of panel p+3 — main stream, overlapping
+//          the panel chain.
+// The critical chain is panel(p) -> F1(p) -> panel(p+1) -> ...; it no longer waits behind the
+// bulk of the previous flush as in the one-deep scheme (where part 1 of flush p+1 queued
+// behind all of part 2 of flush p).  Every element still receives the flushes p = 0, 1, ...
+// in order, each from one tile with the same K order: the result is bitwise the same.
+// fp32 keeps the one-deep scheme: its small L-shaped products each pay a 3xTF32 operand
+// split and a workspace allocation on the critical path (cfg2 fp32: 9.48 vs 6.39 ms).
+template <typename T>
+static bool lu_la2_on() {
+  static const int on = [] {
+    const char* e = getenv("SF_LU_LA2");
+    return e ? atoi(e) : (std::is_same<T, double>::value ? 1 : 0);
+  }();
+  return on != 0;
+}
+
+template <typename T>
+static int lu_run_la2(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int64_t ldd, int64_t* d_info,
+                      cudaStream_t st, PanelHook* hook, long long* fail, T* tol) {
+  Side* sd = nullptr;
+  SF_CUDA(side_stream(sd));
+  cudaStream_t ps = sd->st;
+  SF_CUDA(fork_join(*sd, st, ps));
+  {
+    ProfScope pr(1, 0.0, ps);
+    const int64_t w0 = S.w(0);
+    SF_CUDA(lu_panel_rec<T>(n, w0, n - w0, A, lda, LU, ldd, 0, tol, fail, ps));
+    if (hook) SF_CUDA(hook->done(0, w0, ps));
+  }
+  cudaEvent_t ev_pan = sd->event();
+  SF_CUDA(cudaEventRecord(ev_pan, ps));
+  cudaEvent_t ev_f2 = nullptr;   // F2(p-1) done (main stream)
+  for (int64_t p = 0; p + 1 < S.P(); ++p) {
+    const int64_t z = S.z(p), w = S.w(p), c = z + w;
+    const int64_t w2 = S.w(p + 1), c2 = c + w2;
+    const int64_t w3 = (p + 2 < S.P()) ? S.w(p + 2) : 0, c3 = c2 + w3;
+    const T* src = (z == 0) ? A : LU;
+    const int64_t lds = (z == 0) ? lda : ldd;
+    const T* RL = LU + c + z * ldd;   // R_L = L[c:n, z:c)
+    const T* RU = LU + z + c * ldd;   // R_U = U[z:c, c:n)
+    // the L-shaped region of the panel [a, a + wl): its columns (rows >= a) and its U rows
+    // (columns >= a + wl), as ONE grouped launch (fp64) — flush p restricted to it
+    auto lshape = [&](int64_t a, int64_t wl, cudaStream_t s) -> int {
+      if (wl <= 0) return SF_OK;
+      const int64_t ma = n - a;
+      ProfScope pf(0, 2.0 * w * ((double)ma * wl + (double)wl * (ma - wl)), s);
+      const T* ra = RL + (a - c);
+      if constexpr (std::is_same<T, double>::value) {
+        GemmGroup g[2] = {};
+        int ng = 0;
+        g[ng].M = ma; g[ng].N = wl; g[ng].A = ra; g[ng].B = RU + (a - c) * ldd;
+        g[ng].Cin = src + a + a * lds; g[ng].C = LU + a + a * ldd; ++ng;
+        if (ma > wl) {
+          g[ng].M = wl; g[ng].N = ma - wl; g[ng].A = ra; g[ng].B = RU + (a + wl - c) * ldd;
+          g[ng].Cin = src + a + (a + wl) * lds; g[ng].C = LU + a + (a + wl) * ldd; ++ng;
+        }
+        GemmF64 p64{0, 0, w, nullptr, ldd, nullptr, ldd, nullptr, lds, nullptr, ldd, -1.0, 1, 1, nullptr, fail};
+        SF_CUDA(gemm_f64_grouped(p64, g, ng, 0, 1, kMaskNone, s));
+      } else {
+        SF_CUDA(gemm_sub<T>(ma, wl, w, ra, ldd, 0, RU + (a - c) * ldd, ldd, 1, src + a + a * lds, lds,
+                            LU + a + a * ldd, ldd, kMaskNone, fail, s));
+        if (ma > wl)
+          SF_CUDA(gemm_sub<T>(wl, ma - wl, w, ra, ldd, 0, RU + (a + wl - c) * ldd, ldd, 1, src + a + (a + wl) * lds,
+                              lds, LU + a + (a + wl) * ldd, ldd, kMaskNone, fail, s));
+      }
+      return SF_OK;
+    };
+    // panel stream: F1(p) (after F2(p-1) wrote the same region), then panel p+1
+    if (ev_f2) SF_CUDA(cudaStreamWaitEvent(ps, ev_f2, 0));
+    if (int rc = lshape(c, w2, ps)) return rc;
+    {
+      ProfScope pr(1, 0.0, ps);
+      SF_CUDA(lu_panel_rec<T>(n - c, w2, n - c2, LU + c + c * ldd, ldd, LU + c + c * ldd, ldd, c, tol, fail, ps));
+      if (hook) SF_CUDA(hook->done(c, w2, ps));
+    }
+    // main stream: F2(p), F3(p) once panel p is final
+    SF_CUDA(cudaStreamWaitEvent(st, ev_pan, 0));
+    ev_pan = sd->event();
+    SF_CUDA(cudaEventRecord(ev_pan, ps));   // panel p+1 final (read by F2/F3(p+1))
+    if (int rc = lshape(c2, w3, st)) return rc;
+    ev_f2 = sd->event();
+    SF_CUDA(cudaEventRecord(ev_f2, st));
+    if (c3 < n) {
+      const int64_t m3 = n - c3;
+      const double fl = 2.0 * w * (double)m3 * (double)m3;
+      ProfScope pf(0, fl, st);
+      SF_CUDA(flush_general<T>(m3, m3, w, RL + (c3 - c), ldd, 0, RU + (c3 - c) * ldd, ldd, 1, src + c3 + c3 * lds, lds,
+                               LU + c3 + c3 * ldd, ldd, fail, st));
+    }
+  }
+  SF_CUDA(fork_join(*sd, ps, st));
+  SF_CUDA(finish_info(fail, d_info, st));
+  return SF_OK;
+}
+
 template <typename T>
 static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int64_t ldd, int64_t* d_info,
                   cudaStream_t st, PanelHook* hook = nullptr) {
@@ -206,6 +307,7 @@ static int lu_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* LU, int
   Side* sd = nullptr;
   const bool la = lookahead_on() && S.P() > 1;
   if (la) { SF_CUDA(side_stream(sd)); ws.join(sd->st); }
+  if (la && lu_la2_on<T>()) return lu_run_la2<T>(n, S, A, lda, LU, ldd, d_info, st, hook, fail, tol);
   {
     ProfScope ps(1, 0.0, st);
     const int64_t w0 = S.w(0);

@@ -726,6 +726,17 @@ static int mgs_rpt() {
   static const int v = [] { const char* e = getenv("SF_MGS_RPT"); return (e && atoi(e) == 128) ? 128 : 64; }();
   return v;
 }
+// rows of the 64 a thread owns that stay in registers (SF_MGS_NR: 64, or 32 = half in shared
+// memory: ~half the registers per CTA, so two flush CTAs share the panel CTA's SM)
+static int mgs_nr() {
+  static const int v = [] { const char* e = getenv("SF_MGS_NR"); return (e && atoi(e) == 32) ? 32 : 64; }();
+  return v;
+}
+template <typename T>
+static const void* mgs_ll_reg_fn() {
+  if (mgs_rpt() == 128) return (const void*)qr_mgs_ll_kernel<T, 128, 64>;
+  return mgs_nr() == 32 ? (const void*)qr_mgs_ll_kernel<T, 64, 32> : (const void*)qr_mgs_ll_kernel<T, 64, 64>;
+}
 
 template <typename T>
 static LLGeom ll_geom(int64_t n, int w, bool reg) {
@@ -736,7 +747,7 @@ static LLGeom ll_geom(int64_t n, int w, bool reg) {
   const int64_t G0 = (n + 2 * rpt - 1) / (2 * rpt);
   static int maxcl[2][9] = {{-1, -1, -1, -1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1, -1, -1, -1}};
   auto dyn_for = [&](int G, int CL) -> size_t {
-    if (reg) return sizeof(T) * (((size_t)(G / CL) * (size_t)w + 1) / 2 * 2 + (size_t)(rpt - 64) * kMgsThreads);
+    if (reg) return sizeof(T) * (((size_t)(G / CL) * (size_t)w + 1) / 2 * 2 + (size_t)(rpt - (rpt == 64 ? mgs_nr() : 64)) * kMgsThreads);
     const int RB = (int)((n + G - 1) / G);
     return sizeof(T) * ((size_t)RB * w + 3 * (size_t)w + (size_t)(G / CL) * w + 2 * (size_t)RB);
   };
@@ -754,8 +765,7 @@ static LLGeom ll_geom(int64_t n, int w, bool reg) {
       at[0].val.clusterDim.x = CL; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      const void* kf = reg ? (rpt == 64 ? (const void*)qr_mgs_ll_kernel<T, 64, 64> : (const void*)qr_mgs_ll_kernel<T, 128, 64>)
-                           : (const void*)qr_mgs_ll_smem_kernel<T>;
+      const void* kf = reg ? mgs_ll_reg_fn<T>() : (const void*)qr_mgs_ll_smem_kernel<T>;
       // (the register variant's dynamic size varies a little with G: allow up to 200 KB)
       cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, reg ? 200 * 1024 : (int)dyn);
       int m = 0;
@@ -813,6 +823,8 @@ cudaError_t qr_mgs_panel(int64_t n, int w, const T* src, int64_t lds, T* dst, in
     cfg.numAttrs = mgs_cooperative() ? 2 : 1;
     int RB = lg.RB;
     count_launch();
+    if (lreg && mgs_rpt() == 64 && mgs_nr() == 32)
+      return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 64, 32>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
     if (lreg && mgs_rpt() == 64)
       return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 64, 64>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
     if (lreg)

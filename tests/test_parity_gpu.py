@@ -666,3 +666,41 @@ def test_qr_host_overlapped_copies(n, s):
     Qg, Rg, ig = run_qr(A, s)
     assert info == ig == 0
     assert np.array_equal(hQ, Qg) and np.array_equal(hR, Rg)
+
+
+_LA_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1812_02056_b200 as sf, synth
+n, s, dt = int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+A = synth.gen_numpy("diag_dominant", n, seed=7)
+dA = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+if dt == "f32":
+    dA = dA.float()
+out = torch.empty_like(dA)
+info = torch.zeros(1, dtype=torch.int64, device="cuda")
+for _ in range(3):     # eager, graph capture, graph replay: all three must agree
+    out.zero_()
+    sf.lu_colmajor(n, s, dA, n, out, n, info, dtype=sf.SF_F32 if dt == "f32" else sf.SF_F64)
+    torch.cuda.synchronize()
+    np.save(sys.argv[5] + f"_{_}.npy", out.cpu().numpy())
+assert int(info.item()) == 0
+"""
+
+
+@pytest.mark.parametrize("n,s,dt", [(4096, 64, "f64"), (1000, 96, "f64"), (2048, 64, "f32")])
+def test_lu_two_deep_lookahead_bitwise(tmp_path, n, s, dt):
+    """SF_LU_LA2 (default): the flush of panel p split into the next panel's L shape, the one
+    after it, and the rest, on two streams — every element receives the same flushes in the
+    same order from the same tile kernels, so the factor is BITWISE the one-deep scheme's
+    (SF_LU_LA2=0) and the same on eager, captured and replayed calls."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for la2 in ("1", "0"):
+        env = dict(os.environ, SF_LU_LA2=la2)
+        base = str(tmp_path / f"la{la2}")
+        subprocess.run([sys.executable, "-c", _LA_CHILD, root, str(n), str(s), dt, base], env=env, check=True)
+        outs[la2] = [np.load(base + f"_{i}.npy") for i in range(3)]
+    for i in range(3):
+        assert np.array_equal(outs["1"][i], outs["0"][0]), i
