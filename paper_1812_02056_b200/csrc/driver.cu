@@ -65,6 +65,18 @@ static int chol_run(int64_t n, const Sched& S, const T* A, int64_t lda, T* L, in
   SF_CUDA(ws.init(4096, st));
   long long* fail = ws.take<long long>(2);   // [0] first failed column, [1] leaf counter
   SF_CUDA(init_fail(fail, st));
+  if constexpr (std::is_same<T, double>::value) {
+    // small n: the whole schedule in one thread-block cluster, shared-memory resident (small.cu)
+    if (S.fixed() && chol_small_applies(n, S.fixed(), 8)) {
+      {
+        ProfScope ps(1, 0.0, st);
+        SF_CUDA(chol_small(n, S.fixed(), A, lda, L, ldl, fail, st));
+      }
+      if (hook) SF_CUDA(hook->done(0, n, st));
+      SF_CUDA(finish_info(fail, d_info, st));
+      return SF_OK;
+    }
+  }
   Side* sd = nullptr;
   const bool la = lookahead_on() && S.P() > 1;
   if (la) { SF_CUDA(side_stream(sd)); ws.join(sd->st); }

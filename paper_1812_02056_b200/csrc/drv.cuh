@@ -180,6 +180,12 @@ struct Sched {
   int64_t P() const { return (int64_t)start.size() - 1; }
   int64_t z(int64_t p) const { return start[p]; }
   int64_t w(int64_t p) const { return start[p + 1] - start[p]; }
+  // the step if every panel but the last has the same width (and the last is not wider), else 0
+  int64_t fixed() const {
+    const int64_t s = w(0);
+    for (int64_t p = 0; p + 1 < P(); ++p) if (w(p) != s) return 0;
+    return w(P() - 1) <= s ? s : 0;
+  }
   int64_t maxw() const {
     int64_t m = 1;
     for (int64_t p = 0; p < P(); ++p) m = w(p) > m ? w(p) : m;

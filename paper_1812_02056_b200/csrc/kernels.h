@@ -100,6 +100,11 @@ void mgs_order_after(cudaStream_t st);
 template <typename T>
 cudaError_t lu_panel64(int64_t m, int64_t ncr, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
                        const T* tol, long long* fail, cudaStream_t st);
+// Whole Cholesky of a small matrix (n <= 256, s | 32) in one thread-block cluster, the
+// matrix resident in shared memory (small.cu).
+bool chol_small_applies(int64_t n, int64_t s, int elt);
+cudaError_t chol_small(int64_t n, int64_t s, const double* A, int64_t lda, double* L, int64_t ldl, long long* fail,
+                       cudaStream_t st);
 template <typename T>
 cudaError_t chol_panel64(int64_t m, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
                          long long* fail, cudaStream_t st);

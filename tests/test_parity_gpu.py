@@ -704,3 +704,23 @@ def test_lu_two_deep_lookahead_bitwise(tmp_path, n, s, dt):
         outs[la2] = [np.load(base + f"_{i}.npy") for i in range(3)]
     for i in range(3):
         assert np.array_equal(outs["1"][i], outs["0"][0]), i
+
+
+@pytest.mark.parametrize("n,s", [(256, 1), (256, 4), (256, 16), (256, 32), (200, 8), (64, 2)])
+def test_chol_small_cluster_planted_and_failure(n, s):
+    """n <= 256, s | 32: the whole schedule runs in ONE thread-block cluster from shared
+    memory (small.cu).  Planted integer factors come out exactly; an interior failed pivot
+    stops every CTA with the oracle's info (R3); random SPD input meets the R2 bar."""
+    Lx = synth.planted_chol(n, seed=n + s)
+    Lg, info = run_chol(Lx @ Lx.T, s)
+    assert info == 0 and np.array_equal(np.tril(Lg), Lx)
+    B = synth.gen_numpy("paper_spd", n, seed=s)
+    bad = (3 * n) // 4
+    B[bad, bad] = -5.0
+    io = oracle.chol(B, s)[1]
+    assert io == bad + 1 and run_chol(B, s)[1] == io
+    A = synth.gen_numpy("spd_shift", n, seed=s)
+    Lo, _ = oracle.chol(A, s)
+    for inplace in (True, False):
+        Lg, ig = run_chol(A, s, inplace)
+        assert ig == 0 and synth.r2_error(np.tril(Lg), Lo) <= TOL64
