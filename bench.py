@@ -184,6 +184,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--dist", action="store_true", help="use the distributed (block-cyclic) driver even at N=1")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--push", action="store_true",
+                    help="multi-GPU panel transport: device-initiated push (f3, sf_comm_set_push) instead of ncclBroadcast")
     ap.add_argument("--loopback", type=int, default=0,
                     help="test mode: run the distributed driver with G ranks emulated on this one GPU")
     ap.add_argument("--strassen", type=int, default=0, metavar="MIN_DIM",
@@ -299,6 +301,8 @@ def main():
         if ws > 1:
             dist.broadcast_object_list(uid, src=0)
         comm = sf.Comm.nccl(ws, rank, uid[0])
+    if comm is not None and args.push:
+        comm.set_push(True)
     my_ranks = comm.local_ranks if comm is not None else [rank]
 
     # ---- inputs (synthetic, seeded, same recipe on every rank; A stays pristine: out of place)
@@ -415,6 +419,8 @@ def main():
                      "panel_us_per_column": pan_ms / args.steps * 1e3 / n})
     # ---- per rank (N > 1): where each rank's step went, so the scaling curve explains itself
     bc_ms, bc_n, bc_bytes = prof.get("bcast", (0.0, 0, 0.0))
+    if use_dist:   # rank 0's panel exchange (broadcast, or the device wait of the push transport)
+        roofline["bcast_ms_per_step"] = bc_ms / args.steps
     if ws > 1:
         mine = torch.tensor([ms, upd_ms, pan_ms, bc_ms, bc_bytes], dtype=torch.float64, device="cuda")
         allr = [torch.zeros_like(mine) for _ in range(ws)]
@@ -499,10 +505,12 @@ def main():
                          f"{flops / (fl / dt) / 3600:.2f} h"}
 
     if rank == 0:
-        par = f"block-cyclic s-column panels over {ws} GPU(s), NCCL panel broadcast" if use_dist else "single GPU"
+        xport = ("device-initiated panel push (f3: symmetric-window stores + device flags)" if args.push
+                 else "NCCL panel broadcast")
+        par = f"block-cyclic s-column panels over {ws} GPU(s), {xport}" if use_dist else "single GPU"
         if args.loopback:
             par = (f"LOOPBACK TEST MODE: {G} ranks of the block-cyclic schedule emulated on 1 GPU "
-                   "(device-copy broadcast; not a scaling measurement)")
+                   f"({'device-initiated push' if args.push else 'device-copy broadcast'}; not a scaling measurement)")
         line = {"metric": "factorization GFLOP/s (classical count) and % of FP64 tensor peak",
                 "value": value, "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "strong",

@@ -179,6 +179,18 @@ int sf_comm_init(sf_comm_t* comm, int nranks, int rank, const uint8_t id[128]); 
 int sf_comm_init_loopback(sf_comm_t* comm, int nranks);
 int sf_comm_destroy(sf_comm_t comm);
 int sf_comm_size(sf_comm_t comm);
+/* Panel transport.  on = 0 (default): the owner packs each factored panel
+ * and it travels by ncclBroadcast (loopback: a device copy) on a communication stream.
+ * on = 1: device-initiated push — ONE kernel on the owner's panel stream reads the factored
+ * panel and stores it packed into every rank's receive buffer (NCCL: through the peers'
+ * load/store pointers into a symmetric window, ncclMemAlloc + ncclCommWindowRegister,
+ * allocated collectively at the first dist call that needs it and freed by
+ * sf_comm_destroy), then raises each rank's ready flag (release); receivers wait on their
+ * flag on the device before the flush and signal every rank when done with the buffer.
+ * Cholesky and LU (QR keeps the broadcast of whole Q panels).  Same bytes, same results
+ * (bitwise).  Every rank must set the same mode.  SF_EINVAL for a NULL comm, on not in
+ * {0, 1}, or more than 16 ranks; NCCL window failures surface as SF_ENCCL at the dist call. */
+int sf_comm_set_push(sf_comm_t comm, int on);
 /* Payload bytes of every panel message this communicator has broadcast so far (cumulative):
  * panel p of a Cholesky / LU run sends rows [p*s, n) of its w columns, packed ((n - p*s) * w
  * elements; the last panel, never flushed, is not sent); QR sends whole Q panels (n * w).

@@ -82,6 +82,7 @@ def lib():
         "sf_comm_destroy": [p],
         "sf_comm_size": [p],
         "sf_comm_local_ranks": [p],
+        "sf_comm_set_push": [p, i32],
     }
     for name, args in dist_sig.items():
         f = getattr(L, name)
@@ -118,7 +119,7 @@ EXPORTS = ("chol_factor", "lu_factor", "qr_factor", "chol_factor_host", "lu_fact
            "sf_profile_collect", "sf_get_unique_id", "sf_comm_init", "sf_comm_init_loopback", "sf_comm_destroy",
            "sf_comm_size", "sf_comm_local_ranks", "sf_local_cols", "chol_factor_dist", "lu_factor_dist",
            "qr_factor_dist", "chol_factor_steps", "lu_factor_steps", "qr_factor_steps", "chol_solve", "lu_solve",
-           "qr_solve", "sf_set_strassen", "sf_schedule", "sf_comm_bcast_bytes")
+           "qr_solve", "sf_set_strassen", "sf_schedule", "sf_comm_bcast_bytes", "sf_comm_set_push")
 
 
 def _check(rc):
@@ -397,6 +398,10 @@ class Comm:
         h = ctypes.c_void_p()
         _check(lib().sf_comm_init_loopback(ctypes.byref(h), nranks))
         return cls(h, nranks, list(range(nranks)))
+
+    def set_push(self, on=True):
+        """Panel transport: device-initiated push (f3) instead of the broadcast (stepfact.h)."""
+        _check(lib().sf_comm_set_push(self.handle, 1 if on else 0))
 
     def bcast_bytes(self):
         """Payload bytes of the panel messages this communicator has broadcast so far."""

@@ -28,6 +28,7 @@
 // rank with its own buffers and streams, the broadcast a device copy), which is how the
 // multi-rank path is parity-tested on a single B200.
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include <cstring>
 #include <map>
@@ -42,6 +43,15 @@ struct sf_comm_ {
   int device = 0;
   ncclComm_t nccl = nullptr;
   int64_t bcast_bytes = 0;   // payload of every panel message sent so far (sf_comm_bcast_bytes)
+  // f3 (sf_comm_set_push): device-initiated panel push instead of ncclBroadcast.  NCCL: the
+  // receive buffers and flags live in a symmetric window (ncclMemAlloc +
+  // ncclCommWindowRegister), peers addressed by their load/store (LSA) pointers.
+  int push = 0;
+  uint64_t calls = 0;        // dist calls so far: the high half of the push flag tags
+  void* win_base = nullptr;
+  size_t win_bytes = 0;
+  ncclWindow_t win = nullptr;
+  std::vector<char*> peer_base;   // every rank's window base, as addressable from this GPU
   bool loopback() const { return nccl == nullptr; }
   int nlocal() const { return loopback() ? nranks : 1; }
   int local_rank(int i) const { return loopback() ? i : rank; }
@@ -228,6 +238,102 @@ static int exchange(sf_comm_t comm, std::vector<Rank<T>>& rk, int64_t p, int own
   return SF_OK;
 }
 
+// ------------------------------------------------------------------ f3: device-initiated push
+// SURVEY.md §8 f3.  Instead of pack (device copy) + ncclBroadcast on a third stream, the
+// owner of panel q runs ONE kernel right after the panel's last kernel on its panel stream:
+// it reads the factored panel (rows [qs, n) of its w columns, strided, from its own storage)
+// and stores it packed into EVERY rank's receive buffer for slot q & 1 — through the peers'
+// load/store-accessible window pointers (NVLink / NVSwitch) for an NCCL communicator, plain
+// device pointers for loopback — then the last CTA, after a system-scope fence, raises each
+// rank's `ready[slot]` flag (release) to the panel's tag.  A receiver's main stream runs a
+// one-thread wait (acquire) before its flush of panel p, and after that flush writes its
+// `consumed` tag into every rank's flags; the owner of panel q waits until all ranks consumed
+// panel q-2 (same slot) before pushing.  No host, NCCL call or stream event on the data path;
+// same bytes as the packed broadcast, same operands for the flush (results bitwise equal).
+constexpr int kMaxPushRanks = 16;
+struct PushFlags {
+  unsigned long long ready[2];                 // tag of the panel in slot 0 / 1
+  unsigned long long consumed[kMaxPushRanks];  // tag of the last panel rank r finished flushing
+  unsigned long long counter;                  // CTA arrivals of the running push kernel
+  unsigned long long pad[13];
+};
+struct PushTargets {
+  void* dst[kMaxPushRanks];
+  unsigned long long* flag[kMaxPushRanks];
+  int G;
+};
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// packed element (i, k) of the panel (i < m rows from its first row, k < w) -> dst[i + k*m]
+template <typename T>
+__global__ void __launch_bounds__(256) push_panel_kernel(const T* __restrict__ src, int64_t ld, int64_t m, int w,
+                                                         PushTargets tg, unsigned long long tag,
+                                                         unsigned long long* counter) {
+  const int64_t total = m * (int64_t)w;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % m, k = t / m;
+    const T v = __ldcg(src + i + k * ld);
+    for (int r = 0; r < tg.G; ++r) __stcg(static_cast<T*>(tg.dst[r]) + t, v);
+  }
+  __threadfence_system();   // this CTA's stores are performed for every observer
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long old = atomicAdd(counter, 1ull);
+    if (old == gridDim.x - 1) {   // the last CTA: all CTAs' stores are fenced
+      *counter = 0;
+      __threadfence_system();
+      for (int r = 0; r < tg.G; ++r) st_release_sys(tg.flag[r], tag);
+    }
+  }
+}
+// one thread per flag: spin (acquire) until every flag reaches the tag
+__global__ void wait_flags_kernel(PushTargets tg, unsigned long long tag) {
+  if ((int)threadIdx.x < tg.G)
+    while (ld_acquire_sys(tg.flag[threadIdx.x]) < tag) __nanosleep(100);
+}
+__global__ void signal_flags_kernel(PushTargets tg, unsigned long long tag) {
+  if ((int)threadIdx.x < tg.G) st_release_sys(tg.flag[threadIdx.x], tag);
+}
+__global__ void lsa_pointers_kernel(ncclWindow_t w, int G, char** out) {
+  if ((int)threadIdx.x < G) out[threadIdx.x] = (char*)ncclGetPeerPointer(w, 0, (int)threadIdx.x);
+}
+
+// The symmetric window of an NCCL communicator, per rank: [PushFlags (4 KB) | slot 0 | slot 1]
+// — the flags at a fixed offset, so their tags carry over between calls of any size.
+// Collective (every rank calls the dist entry point with the same sizes).
+constexpr size_t kFlagBytes = 4096;
+static_assert(sizeof(PushFlags) <= kFlagBytes, "flag block");
+static int ensure_window(sf_comm_t comm, size_t buf_bytes) {
+  const size_t need = kFlagBytes + 2 * buf_bytes;
+  if (comm->win && comm->win_bytes >= need) return SF_OK;
+  if (comm->win) {
+    SF_CUDA(cudaDeviceSynchronize());
+    SF_NCCL(ncclCommWindowDeregister(comm->nccl, comm->win));
+    SF_NCCL(ncclMemFree(comm->win_base));
+    comm->win = nullptr; comm->win_base = nullptr; comm->win_bytes = 0;
+  }
+  const size_t bytes = (need + (size_t(1) << 21) - 1) & ~((size_t(1) << 21) - 1);
+  SF_NCCL(ncclMemAlloc(&comm->win_base, bytes));
+  SF_CUDA(cudaMemset(comm->win_base, 0, bytes));
+  SF_NCCL(ncclCommWindowRegister(comm->nccl, comm->win_base, bytes, &comm->win, NCCL_WIN_COLL_SYMMETRIC));
+  comm->win_bytes = bytes;
+  char** d = nullptr;
+  SF_CUDA(cudaMalloc(&d, sizeof(char*) * comm->nranks));
+  lsa_pointers_kernel<<<1, 32>>>(comm->win, comm->nranks, d);
+  comm->peer_base.assign(comm->nranks, nullptr);
+  cudaError_t e = cudaMemcpy(comm->peer_base.data(), d, sizeof(char*) * comm->nranks, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  SF_CUDA(e);
+  return SF_OK;
+}
+
 // info: all-reduce(min) of the first failed column over ranks, then per-rank d_info
 template <typename T>
 static int finish_dist(sf_comm_t comm, std::vector<Rank<T>>& rk, cudaStream_t caller) {
@@ -388,6 +494,108 @@ struct Span {
   }
 };
 
+// Panel exchange of the Span-packed drivers (Cholesky, LU): the broadcast (pack + NCCL /
+// loopback copy) or the push (f3).  send() after the owner factored panel q (panel stream),
+// recv(p) before the flushes of panel p (leaves recv[p] recorded where the flush waits),
+// consumed() after a rank's flush of panel p (main stream).
+template <typename T>
+struct PanelXfer {
+  sf_comm_t comm;
+  std::vector<Rank<T>>& rk;
+  const Span<T>& sp;
+  bool push = false;
+  unsigned long long call = 0;
+  std::vector<T*> gbuf[2];               // every rank's receive buffer per slot (device addresses)
+  std::vector<PushFlags*> gflags;        // every rank's flags
+  std::vector<PushFlags*> lflags;        // the local ranks' own flags
+
+  PanelXfer(sf_comm_t c, std::vector<Rank<T>>& r, const Span<T>& s) : comm(c), rk(r), sp(s) {}
+  unsigned long long tag(int64_t p) const { return (call << 32) | (unsigned long long)(p + 1); }
+
+  int setup(size_t buf_elems, cudaStream_t caller) {
+    push = comm->push != 0;
+    call = ++comm->calls;
+    if (!push) return SF_OK;
+    const int G = comm->nranks;
+    if (G > kMaxPushRanks) return fail_with(SF_EINVAL, "push transport supports at most %d ranks", kMaxPushRanks);
+    gbuf[0].assign(G, nullptr); gbuf[1].assign(G, nullptr); gflags.assign(G, nullptr);
+    if (comm->loopback()) {
+      for (auto& x : rk) {
+        PushFlags* f = x.ws.template take<PushFlags>(1);
+        SF_CUDA(cudaMemsetAsync(f, 0, sizeof(PushFlags), caller));
+        gbuf[0][x.r] = x.buf[0]; gbuf[1][x.r] = x.buf[1]; gflags[x.r] = f;
+        lflags.push_back(f);
+      }
+    } else {
+      const size_t bb = (buf_elems * sizeof(T) + 255) & ~(size_t)255;
+      if (int rc = ensure_window(comm, bb)) return rc;
+      Rank<T>& me = rk[0];
+      me.buf[0] = (T*)((char*)comm->win_base + kFlagBytes);
+      me.buf[1] = (T*)((char*)comm->win_base + kFlagBytes + bb);
+      for (int r = 0; r < G; ++r) {
+        gflags[r] = (PushFlags*)comm->peer_base[r];
+        gbuf[0][r] = (T*)(comm->peer_base[r] + kFlagBytes);
+        gbuf[1][r] = (T*)(comm->peer_base[r] + kFlagBytes + bb);
+      }
+      lflags.push_back((PushFlags*)comm->win_base);   // tags grow across calls: no reset
+    }
+    cudaEvent_t e = pool_event();   // the rank streams see the zeroed flags
+    SF_CUDA(cudaEventRecord(e, caller));
+    for (auto& x : rk) { SF_CUDA(wait_on(x.st.mn, e)); SF_CUDA(wait_on(x.st.pan, e)); }
+    return SF_OK;
+  }
+  PushFlags* own(const Rank<T>& x) const { return comm->loopback() ? lflags[x.r] : lflags[0]; }
+
+  int send(Rank<T>& x, int64_t q, cudaEvent_t prev, cudaStream_t st) {
+    if (!push) return sp.pack(x, q, prev, st);
+    const int G = comm->nranks;
+    if (q >= 2) {   // every rank finished flushing panel q-2 out of this slot
+      PushTargets w{};
+      w.G = G;
+      for (int r = 0; r < G; ++r) w.flag[r] = &own(x)->consumed[r];
+      wait_flags_kernel<<<1, 32, 0, st>>>(w, tag(q - 2));
+      count_launch();
+    }
+    const int slot = (int)(q & 1);
+    PushTargets tg{};
+    tg.G = G;
+    for (int r = 0; r < G; ++r) { tg.dst[r] = gbuf[slot][r]; tg.flag[r] = &gflags[r]->ready[slot]; }
+    const int64_t m = sp.ldp(q);
+    const T* src = x.X + q * sp.cy.s + sp.cy.slot(q) * sp.cy.s * sp.ld;
+    const int64_t total = m * sp.cy.width(q);
+    int grid = (int)((total + 255) / 256);
+    if (grid > 4 * 148) grid = 4 * 148;
+    push_panel_kernel<T><<<grid, 256, 0, st>>>(src, sp.ld, m, (int)sp.cy.width(q), tg, tag(q), &own(x)->counter);
+    count_launch();
+    return cudaGetLastError() == cudaSuccess ? SF_OK : fail_with(SF_ECUDA, "push_panel_kernel launch");
+  }
+  template <typename FreeF>
+  int recv(int64_t p, int owner, FreeF free_ev) {
+    if (!push)
+      return exchange<T>(comm, rk, p, owner, sp.count(p), [&](Rank<T>& x) { return sp.at(x, p); }, free_ev);
+    comm->bcast_bytes += (int64_t)(sp.count(p) * sizeof(T));
+    for (auto& x : rk) {
+      PushTargets w{};
+      w.G = 1;
+      w.flag[0] = &own(x)->ready[p & 1];
+      ProfScope pb(3, (double)(sp.count(p) * sizeof(T)), x.st.mn);
+      wait_flags_kernel<<<1, 32, 0, x.st.mn>>>(w, tag(p));
+      count_launch();
+      SF_CUDA(cudaEventRecord(x.recv[p], x.st.mn));
+    }
+    return SF_OK;
+  }
+  int consumed(Rank<T>& x, int64_t p, cudaStream_t st) {
+    if (!push) return SF_OK;
+    PushTargets w{};
+    w.G = comm->nranks;
+    for (int r = 0; r < w.G; ++r) w.flag[r] = &gflags[r]->consumed[x.r];
+    signal_flags_kernel<<<1, 32, 0, st>>>(w, tag(p));
+    count_launch();
+    return SF_OK;
+  }
+};
+
 template <typename T>
 static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, void* const* dL, int64_t ld,
                          int64_t* const* d_info, cudaStream_t caller) {
@@ -406,6 +614,9 @@ static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, 
     }
   }
   const Span<T> sp{cy, ld};
+  PanelXfer<T> xf(comm, rk, sp);
+  rc = xf.setup((size_t)s * ld, caller);
+  if (rc) return rc;
   // prologue: panel 0 on its owner, out of place from A
   for (auto& o : rk) {
     if (o.r != 0) continue;
@@ -413,12 +624,11 @@ static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, 
       ProfScope ps(1, 0.0, o.st.pan);
       SF_CUDA(chol_panel_any(o, n, cy.width(0), o.A, ld, o.X, ld, 0, o.st.pan));
     }
-    if (cy.P > 1) { rc = sp.pack(o, 0, nullptr, o.st.pan); if (rc) return rc; }
+    if (cy.P > 1) { rc = xf.send(o, 0, nullptr, o.st.pan); if (rc) return rc; }
     SF_CUDA(cudaEventRecord(o.ready[0], o.st.pan));
   }
   for (int64_t p = 0; p + 1 < cy.P; ++p) {   // the last panel is never flushed: not sent
-    rc = exchange<T>(comm, rk, p, cy.owner(p), sp.count(p), [&](Rank<T>& x) { return sp.at(x, p); },
-                     [&](Rank<T>& x) -> cudaEvent_t { return p >= 2 ? x.done[p - 2] : nullptr; });
+    rc = xf.recv(p, cy.owner(p), [&](Rank<T>& x) -> cudaEvent_t { return p >= 2 ? x.done[p - 2] : nullptr; });
     if (rc) return rc;
     for (auto& x : rk) {
       SF_CUDA(wait_on(x.st.mn, x.recv[p]));
@@ -444,7 +654,7 @@ static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, 
           T* P0 = x.X + qs + j * s * ld;
           SF_CUDA(chol_panel_any(x, n - qs, wq, P0, ld, P0, ld, qs, x.st.pan));
         }
-        if (q + 1 < cy.P) { rc = sp.pack(x, q, q >= 2 ? x.done[q - 2] : nullptr, x.st.pan); if (rc) return rc; }
+        if (q + 1 < cy.P) { rc = xf.send(x, q, q >= 2 ? x.done[q - 2] : nullptr, x.st.pan); if (rc) return rc; }
         SF_CUDA(cudaEventRecord(x.ready[q], x.st.pan));
       }
       {
@@ -454,6 +664,8 @@ static int chol_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, 
         pf.r.flops = fl;
       }
       SF_CUDA(cudaEventRecord(x.done[p], x.st.mn));
+      rc = xf.consumed(x, p, x.st.mn);
+      if (rc) return rc;
     }
   }
   for (auto& x : rk) { rc = join_rank<T>(x); if (rc) return rc; }
@@ -494,18 +706,20 @@ static int lu_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, vo
     SF_CUDA(wait_on(x.st.mn, e)); SF_CUDA(wait_on(x.st.pan, e)); SF_CUDA(wait_on(x.st.com, e));
   }
   const Span<T> sp{cy, ld};   // the L panel incl. U11 in its diagonal block
+  PanelXfer<T> xf(comm, rk, sp);
+  rc = xf.setup((size_t)s * ld, caller);
+  if (rc) return rc;
   for (auto& o : rk) {
     if (o.r != 0) continue;
     {
       ProfScope ps(1, 0.0, o.st.pan);
       SF_CUDA(lu_panel_rec<T>(n, cy.width(0), 0, o.X, ld, o.X, ld, 0, o.tol, o.fail, o.st.pan));
     }
-    if (cy.P > 1) { rc = sp.pack(o, 0, nullptr, o.st.pan); if (rc) return rc; }
+    if (cy.P > 1) { rc = xf.send(o, 0, nullptr, o.st.pan); if (rc) return rc; }
     SF_CUDA(cudaEventRecord(o.ready[0], o.st.pan));
   }
   for (int64_t p = 0; p + 1 < cy.P; ++p) {   // the last panel is never flushed: not sent
-    rc = exchange<T>(comm, rk, p, cy.owner(p), sp.count(p), [&](Rank<T>& x) { return sp.at(x, p); },
-                     [&](Rank<T>& x) -> cudaEvent_t { return p >= 2 ? x.done[p - 2] : nullptr; });
+    rc = xf.recv(p, cy.owner(p), [&](Rank<T>& x) -> cudaEvent_t { return p >= 2 ? x.done[p - 2] : nullptr; });
     if (rc) return rc;
     for (auto& x : rk) {
       SF_CUDA(wait_on(x.st.mn, x.recv[p]));
@@ -529,7 +743,7 @@ static int lu_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, vo
           T* P0 = x.X + qs + j * s * ld;
           SF_CUDA(lu_panel_rec<T>(n - qs, wq, 0, P0, ld, P0, ld, qs, x.tol, x.fail, x.st.pan));
         }
-        if (q + 1 < cy.P) { rc = sp.pack(x, q, q >= 2 ? x.done[q - 2] : nullptr, x.st.pan); if (rc) return rc; }
+        if (q + 1 < cy.P) { rc = xf.send(x, q, q >= 2 ? x.done[q - 2] : nullptr, x.st.pan); if (rc) return rc; }
         SF_CUDA(cudaEventRecord(x.ready[q], x.st.pan));
       }
       {
@@ -539,6 +753,8 @@ static int lu_dist_run(sf_comm_t comm, int64_t n, int64_t s, void* const* dA, vo
         pf.r.flops = fl;
       }
       SF_CUDA(cudaEventRecord(x.done[p], x.st.mn));
+      rc = xf.consumed(x, p, x.st.mn);
+      if (rc) return rc;
     }
   }
   for (auto& x : rk) { rc = join_rank<T>(x); if (rc) return rc; }
@@ -716,6 +932,11 @@ int sf_comm_destroy(sf_comm_t comm) {
   SF_API_LOCK;
   if (!comm) return SF_OK;
   int rc = SF_OK;
+  if (comm->win) {
+    cudaDeviceSynchronize();
+    ncclCommWindowDeregister(comm->nccl, comm->win);
+    ncclMemFree(comm->win_base);
+  }
   if (comm->nccl) {
     ncclResult_t r = ncclCommDestroy(comm->nccl);
     if (r != ncclSuccess) rc = fail_with(SF_ENCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
@@ -724,6 +945,13 @@ int sf_comm_destroy(sf_comm_t comm) {
   return rc;
 }
 
+int sf_comm_set_push(sf_comm_t comm, int on) {
+  SF_API_LOCK;
+  if (!comm || (on != 0 && on != 1)) return fail_with(SF_EINVAL, "sf_comm_set_push: bad arguments");
+  if (on && comm->nranks > sf::kMaxPushRanks) return fail_with(SF_EINVAL, "push transport: at most %d ranks", sf::kMaxPushRanks);
+  comm->push = on;
+  return SF_OK;
+}
 int sf_comm_size(sf_comm_t comm) { return comm ? comm->nranks : 0; }
 int64_t sf_comm_bcast_bytes(sf_comm_t comm) { return comm ? comm->bcast_bytes : -1; }
 int sf_comm_local_ranks(sf_comm_t comm) { return comm ? comm->nlocal() : 0; }

@@ -276,3 +276,92 @@ def test_dist_bcast_bytes_packed(kind, n, s, G):
         Lo, Uo, _ = oracle.lu(A, s)
         F = outs[0]
         assert synth.r2_error(np.tril(F), Lo) <= TOL64 and synth.r2_error(np.triu(F, 1) + np.eye(n), Uo) <= TOL64
+
+
+# ---------------------------------------------------------------- f3: device-initiated push
+
+PUSH_CASES = [(1, 1, 1), (64, 16, 2), (300, 64, 4), (300, 100, 8), (520, 128, 3), (1000, 168, 4), (2048, 512, 5)]
+
+
+@pytest.mark.parametrize("n,s,G", PUSH_CASES)
+def test_chol_dist_push_bitwise(n, s, G):
+    """sf_comm_set_push: the owner's ONE push kernel stores the packed
+    panel into every rank's buffer and raises their ready flags; receivers wait on the
+    device, signal `consumed` after the flush.  Same bytes on the wire (counted), same
+    operands: the factor is bitwise the broadcast's and the single GPU's (fp64 and fp32)."""
+    A = synth.gen_numpy("paper_spd", n, seed=n + G)
+    L1, _ = run_chol(A, s, inplace=False)
+    for dtype in (sf.SF_F64, sf.SF_F32):
+        outs = {}
+        for push in (False, True):
+            comm = sf.Comm.loopback(G)
+            try:
+                comm.set_push(push)
+                b0 = comm.bcast_bytes()
+                (Lg,), info = run_dist("chol", A, s, G, comm=comm, dtype=dtype)
+                assert info == 0
+                outs[push] = (Lg, comm.bcast_bytes() - b0)
+            finally:
+                comm.destroy()
+        assert np.array_equal(outs[True][0], outs[False][0]) and outs[True][1] == outs[False][1]
+        if dtype == sf.SF_F64:
+            assert np.array_equal(np.tril(outs[True][0]), np.tril(L1))
+
+
+@pytest.mark.parametrize("n,s,G", PUSH_CASES)
+def test_lu_dist_push_bitwise(n, s, G):
+    A = synth.gen_numpy("diag_dominant", n, seed=n + G)
+    outs = {}
+    for push in (False, True):
+        comm = sf.Comm.loopback(G)
+        try:
+            comm.set_push(push)
+            (F,), info = run_dist("lu", A, s, G, comm=comm)
+            assert info == 0
+            outs[push] = F
+        finally:
+            comm.destroy()
+    assert np.array_equal(outs[True], outs[False])
+    Lo, Uo, _ = oracle.lu(A, s)
+    assert synth.r2_error(np.tril(outs[True]), Lo) <= TOL64
+
+
+def test_push_failure_and_repeated_calls():
+    """A failed pivot under the push transport: every rank reports the oracle's column and no
+    rank waits forever on a flag; the same communicator then serves further calls (the flag
+    tags grow per call, so stale flags never release a wait)."""
+    comm = sf.Comm.loopback(3)
+    try:
+        comm.set_push(True)
+        B = synth.gen_numpy("paper_spd", 300, seed=3)
+        B[200, 200] = -5.0
+        io = oracle.chol(B, 64)[1]
+        assert run_dist("chol", B, 64, 3, comm=comm)[1] == io == 201
+        A = synth.gen_numpy("paper_spd", 300, seed=4)
+        L1, _ = run_chol(A, 64, inplace=False)
+        for _ in range(3):
+            (Lg,), info = run_dist("chol", A, 64, 3, comm=comm)
+            assert info == 0 and np.array_equal(np.tril(Lg), np.tril(L1))
+    finally:
+        comm.destroy()
+
+
+def test_nccl_push_single_rank():
+    """The push transport on a real NCCL communicator (one rank): the receive buffers and
+    flags live in a symmetric window (ncclMemAlloc + ncclCommWindowRegister), the push kernel
+    addresses them through the window's load/store pointer; repeated calls reuse it."""
+    uid = sf.unique_id()
+    comm = sf.Comm.nccl(1, 0, uid)
+    try:
+        comm.set_push(True)
+        A = synth.gen_numpy("spd_scaled", 600, seed=1)
+        L1, _ = run_chol(A, 128, inplace=False)
+        for _ in range(2):
+            (Lg,), info = run_dist("chol", A, 128, 1, comm=comm)
+            assert info == 0 and np.array_equal(np.tril(Lg), np.tril(L1))
+        B = synth.gen_numpy("diag_dominant", 500, seed=2)
+        (F,), info = run_dist("lu", B, 96, 1, comm=comm)
+        Lo, Uo, _ = oracle.lu(B, 96)
+        assert info == 0 and synth.r2_error(np.tril(F), Lo) <= TOL64
+    finally:
+        comm.destroy()
