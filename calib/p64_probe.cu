@@ -29,12 +29,16 @@ int main() {
     lu_panel64<double>(m, m - w, (int)w, d, m, d, m, 0, tol, fail, 0);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
-    unsigned long long t[16];
+    unsigned long long t[16], tc[16];
     cudaMemcpyFromSymbol(t, p64_times, sizeof(t));
+    cudaMemcpyFromSymbol(tc, p64_times_col, sizeof(tc));
     printf("rep %d: %.1f us total;", rep, ms * 1000);
     for (int k = 1; k < 10; ++k) printf(" %s %.2f", names[k], (t[k] - t[k - 1]) / 1000.0);
     printf(" | CTA0 start->T0 %.2f, grid span %.2f, rows done %.2f (us) err=%s\n", (t[0] - t[10]) / 1000.0,
            (t[11] - t[10]) / 1000.0, (t[12] - t[10]) / 1000.0, cudaGetErrorString(cudaGetLastError()));
+    printf("   column CTA:");
+    for (int k = 1; k < 10; ++k) printf(" %s %.2f", names[k], (tc[k] - tc[k - 1]) / 1000.0);
+    printf(" | start->T0 %.2f, done at %.2f (us)\n", (tc[0] - t[10]) / 1000.0, (tc[9] - t[10]) / 1000.0);
   }
   return 0;
 }

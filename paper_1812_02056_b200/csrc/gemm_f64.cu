@@ -106,8 +106,19 @@ __host__ __device__ __forceinline__ int masked_tiles(int mask, int TM, int TN, i
   return T64::count(mask, TM, TN, off);
 }
 
+// bulk-async reduction of a shared-memory column segment into global memory (in-place epilogues)
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_reduce_add_f64(double* gdst, const double* ssrc, int bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n" ::"l"(gdst), "r"(s),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+
 template <bool AK, bool BKC, bool V16, int MASK, int NT = g64::THREADS>
-__device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vecC) {
+__device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vecC, int bulk = 0) {
   using namespace g64;
   // NT = 128: 4 warps as 2 (i) x 2 (j), warp tile 64 x 32; NT = 256 (short K): 8 warps as
   // 4 x 2, warp tile 32 x 32 — twice the issuing warps per SM sub-partition
@@ -194,14 +205,37 @@ __device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vec
 
   // ---- epilogue, step 1: park the accumulator tile in shared memory, Cs[j*CPAD + i]
   double* Cs = smem;
+  const int64_t rows = (p.M - i0 < BM) ? p.M - i0 : BM;
+  // in place (Cin == C): add alpha*acc to C in L2 by one bulk reduction per column (as the
+  // v2 tile), -0.0 where the mask excludes an entry (x + -0.0 == x: bit-identical)
+  const bool use_bulk = bulk && p.splits == 1 && (rows & 1) == 0;
 #pragma unroll
   for (int a = 0; a < ATM; ++a) {
     const int il = wm * WTM + a * 8 + 2 * (lane & 3);
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int jl = wn * 32 + b * 8 + (lane >> 2);
-      *reinterpret_cast<double2*>(Cs + jl * CPAD + il) = make_double2(acc[a][b][0], acc[a][b][1]);
+      double v0 = acc[a][b][0], v1 = acc[a][b][1];
+      if (use_bulk) {
+        const int64_t i = i0 + il, jd = j0 + jl + p.off;
+        const bool in0 = MASK == kMaskNone || (MASK == kMaskLower ? i >= jd : i <= jd);
+        const bool in1 = MASK == kMaskNone || (MASK == kMaskLower ? i + 1 >= jd : i + 1 <= jd);
+        v0 = in0 ? p.alpha * v0 : -0.0;
+        v1 = in1 ? p.alpha * v1 : -0.0;
+      }
+      *reinterpret_cast<double2*>(Cs + jl * CPAD + il) = make_double2(v0, v1);
     }
+  }
+  if (use_bulk) {
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid < BN) {
+      const int64_t j = j0 + tid;
+      if (j < p.N) bulk_reduce_add_f64(p.C + i0 + j * p.ldc, Cs + tid * CPAD, (int)(rows * 8));
+      bulk_commit();
+      bulk_wait_read0();
+    }
+    return;
   }
   __syncthreads();
 
@@ -293,15 +327,6 @@ template <int BM, bool AK, bool BKC> constexpr size_t smem_bytes() {
 }
 }  // namespace g64v2
 
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-__device__ __forceinline__ void bulk_reduce_add_f64(double* gdst, const double* ssrc, int bytes) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
-  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;\n" ::"l"(gdst), "r"(s),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 
 template <int BM, bool PAIR, bool AK, bool BKC, bool V16, int MASK>
 __device__ __forceinline__ void gemm_f64_body2(const GemmF64& p, int bid, int vecC, int bulk) {
@@ -522,9 +547,9 @@ __global__ void __launch_bounds__(128, MINB) gemm_f64v2_kernel(GemmF64 p, int ve
 }
 
 template <bool AK, bool BKC, bool V16, int MASK, int NT = g64::THREADS>
-__global__ void __launch_bounds__(NT, 2) gemm_f64_kernel(GemmF64 p, int vecC) {
+__global__ void __launch_bounds__(NT, 2) gemm_f64_kernel(GemmF64 p, int vecC, int bulk) {
   if (p.fail && failed(p.fail)) return;
-  gemm_f64_body<AK, BKC, V16, MASK, NT>(p, blockIdx.x, vecC);
+  gemm_f64_body<AK, BKC, V16, MASK, NT>(p, blockIdx.x, vecC, bulk);
 }
 
 // Bounded grid (max_ctas > 0): each CTA loops over tiles, leaving SMs to a concurrent stream.
@@ -540,14 +565,14 @@ __global__ void __launch_bounds__(g64::THREADS, 2) gemm_f64_loop_kernel(GemmF64 
 
 // Grouped launch: several independent C blocks sharing K, the operand leading dimensions
 // and the mask, one CTA grid (the block-cyclic distributed updates).
-template <bool AK, bool BKC, bool V16, int MASK>
-__global__ void __launch_bounds__(g64::THREADS, 2) gemm_f64_grouped_kernel(GemmF64 p, GemmGroups gs, int vecC) {
+template <bool AK, bool BKC, bool V16, int MASK, int NT = g64::THREADS>
+__global__ void __launch_bounds__(NT, 2) gemm_f64_grouped_kernel(GemmF64 p, GemmGroups gs, int vecC, int bulk) {
   if (p.fail && failed(p.fail)) return;
   int g = 0;
   while (g + 1 < gs.count && (int)blockIdx.x >= gs.g[g + 1].tile0) ++g;
   p.M = gs.g[g].M; p.N = gs.g[g].N; p.off = gs.g[g].off; p.rs.ngroups = 0;
   p.A = gs.g[g].A; p.B = gs.g[g].B; p.Cin = gs.g[g].Cin; p.C = gs.g[g].C;
-  gemm_f64_body<AK, BKC, V16, MASK>(p, (int)blockIdx.x - gs.g[g].tile0, vecC);
+  gemm_f64_body<AK, BKC, V16, MASK, NT>(p, (int)blockIdx.x - gs.g[g].tile0, vecC, bulk);
 }
 
 // Fixed-order split-K reduction: C = (beta ? Cin : 0) + alpha * sum_sp work[sp].
@@ -582,8 +607,14 @@ static int64_t short_k_max() {
   return k;
 }
 
+static bool grouped_short_k8() {
+  // measured neutral at cfg2 (5.19 vs 5.14 ms without): off by default
+  static const int on = [] { const char* e = getenv("SF_GROUPED_SHORTK8"); return e ? atoi(e) : 0; }();
+  return on != 0;
+}
+
 template <bool AK, bool BKC, bool V16, int MASK>
-static cudaError_t launch_t(const GemmF64& p, const GemmGroups* gs, int ntiles, int vecC, cudaStream_t st) {
+static cudaError_t launch_t(const GemmF64& p, const GemmGroups* gs, int ntiles, int vecC, int bulk, cudaStream_t st) {
   static bool attr_set = false;  // per template instance
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemm_f64_kernel<AK, BKC, V16, MASK>,
@@ -597,29 +628,38 @@ static cudaError_t launch_t(const GemmF64& p, const GemmGroups* gs, int ntiles, 
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(gemm_f64_kernel<AK, BKC, V16, MASK, 256>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g64::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(gemm_f64_grouped_kernel<AK, BKC, V16, MASK, 256>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g64::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   dim3 grid(ntiles, p.splits);
-  if (gs) gemm_f64_grouped_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, *gs, vecC);
+  if (gs && p.K <= short_k_max() && short_k_wide() && grouped_short_k8())
+    // the short-K grouped launches (LU's L-shaped lookahead flush part, K = s = 64) sit on the
+    // panel chain: 8 warps per CTA keep two issuing warps per SM sub-partition on an SM of
+    // its own (one 4-warp CTA issues DMMA at about half rate)
+    gemm_f64_grouped_kernel<AK, BKC, V16, MASK, 256><<<grid, 256, g64::SMEM, st>>>(p, *gs, vecC, bulk);
+  else if (gs) gemm_f64_grouped_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, *gs, vecC, bulk);
   else if (p.max_ctas > 0 && p.max_ctas < ntiles) {
     grid.x = p.max_ctas;
     gemm_f64_loop_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, vecC);
   } else if (p.K <= short_k_max() && short_k_wide()) {
     // short K: the per-tile prologue/epilogue is a large share of each tile; 8-warp CTAs keep
     // two issuing warps per SM sub-partition through the co-resident CTA's epilogue
-    gemm_f64_kernel<AK, BKC, V16, MASK, 256><<<grid, 256, g64::SMEM, st>>>(p, vecC);
-  } else gemm_f64_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, vecC);
+    gemm_f64_kernel<AK, BKC, V16, MASK, 256><<<grid, 256, g64::SMEM, st>>>(p, vecC, bulk);
+  } else gemm_f64_kernel<AK, BKC, V16, MASK><<<grid, g64::THREADS, g64::SMEM, st>>>(p, vecC, bulk);
   count_launch();
   return cudaGetLastError();
 }
 
 template <bool AK, bool BKC, bool V16>
-static cudaError_t launch_mask(const GemmF64& p, const GemmGroups* gs, int mask, int ntiles, int vecC, cudaStream_t st) {
+static cudaError_t launch_mask(const GemmF64& p, const GemmGroups* gs, int mask, int ntiles, int vecC, int bulk,
+                               cudaStream_t st) {
   switch (mask) {
-    case kMaskLower: return launch_t<AK, BKC, V16, kMaskLower>(p, gs, ntiles, vecC, st);
-    case kMaskUpper: return launch_t<AK, BKC, V16, kMaskUpper>(p, gs, ntiles, vecC, st);
-    default: return launch_t<AK, BKC, V16, kMaskNone>(p, gs, ntiles, vecC, st);
+    case kMaskLower: return launch_t<AK, BKC, V16, kMaskLower>(p, gs, ntiles, vecC, bulk, st);
+    case kMaskUpper: return launch_t<AK, BKC, V16, kMaskUpper>(p, gs, ntiles, vecC, bulk, st);
+    default: return launch_t<AK, BKC, V16, kMaskNone>(p, gs, ntiles, vecC, bulk, st);
   }
 }
 
@@ -628,17 +668,17 @@ static bool aligned16(const void* ptr, int64_t ld) {
 }
 
 static cudaError_t launch_key(const GemmF64& p, const GemmGroups* gs, int a_kcontig, int b_kcontig, bool v16, int mask,
-                              int ntiles, int vecC, cudaStream_t st) {
+                              int ntiles, int vecC, cudaStream_t st, int bulk = 0) {
   const int key = (a_kcontig ? 1 : 0) | (b_kcontig ? 2 : 0) | (v16 ? 4 : 0);
   switch (key) {
-    case 0: return launch_mask<false, false, false>(p, gs, mask, ntiles, vecC, st);
-    case 1: return launch_mask<true, false, false>(p, gs, mask, ntiles, vecC, st);
-    case 2: return launch_mask<false, true, false>(p, gs, mask, ntiles, vecC, st);
-    case 3: return launch_mask<true, true, false>(p, gs, mask, ntiles, vecC, st);
-    case 4: return launch_mask<false, false, true>(p, gs, mask, ntiles, vecC, st);
-    case 5: return launch_mask<true, false, true>(p, gs, mask, ntiles, vecC, st);
-    case 6: return launch_mask<false, true, true>(p, gs, mask, ntiles, vecC, st);
-    default: return launch_mask<true, true, true>(p, gs, mask, ntiles, vecC, st);
+    case 0: return launch_mask<false, false, false>(p, gs, mask, ntiles, vecC, bulk, st);
+    case 1: return launch_mask<true, false, false>(p, gs, mask, ntiles, vecC, bulk, st);
+    case 2: return launch_mask<false, true, false>(p, gs, mask, ntiles, vecC, bulk, st);
+    case 3: return launch_mask<true, true, false>(p, gs, mask, ntiles, vecC, bulk, st);
+    case 4: return launch_mask<false, false, true>(p, gs, mask, ntiles, vecC, bulk, st);
+    case 5: return launch_mask<true, false, true>(p, gs, mask, ntiles, vecC, bulk, st);
+    case 6: return launch_mask<false, true, true>(p, gs, mask, ntiles, vecC, bulk, st);
+    default: return launch_mask<true, true, true>(p, gs, mask, ntiles, vecC, bulk, st);
   }
 }
 
@@ -744,7 +784,8 @@ cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStre
   p.ntiles = ntiles;
   const bool v16 = aligned16(p.A, p.lda) && aligned16(p.B, p.ldb);
   const int vecC = aligned16(p.C, p.ldc) && (!p.beta || aligned16(p.Cin, p.ldcin));
-  cudaError_t e = launch_key(p, nullptr, a_kcontig, b_kcontig, v16, mask, ntiles, vecC, st);
+  const int bulk = dmma_bulk() && p.splits == 1 && p.beta && vecC && p.Cin == p.C && p.ldcin == p.ldc;
+  cudaError_t e = launch_key(p, nullptr, a_kcontig, b_kcontig, v16, mask, ntiles, vecC, st, bulk);
   if (e != cudaSuccess || p.splits == 1) return e;
   return splitk_reduce(p, st);
 }
@@ -759,12 +800,15 @@ cudaError_t gemm_f64_grouped(GemmF64 p, const GemmGroup* groups, int count, int 
   p.splits = 1;
   GemmGroups gs{};
   int ntiles = 0;
+  bool inplace = p.beta && p.ldcin == p.ldc;
   for (int i = 0; i < count; ++i) {
     const GemmGroup& g = groups[i];
     if (g.M <= 0 || g.N <= 0) continue;
     v16 = v16 && aligned16(g.A, p.lda) && aligned16(g.B, p.ldb);
     vecC = vecC && aligned16(g.C, p.ldc) && (!p.beta || aligned16(g.Cin, p.ldcin));
+    inplace = inplace && g.Cin == g.C;
   }
+  const int bulk = dmma_bulk() && inplace && vecC;
   for (int i = 0; i < count; ++i) {
     GemmGroup g = groups[i];
     if (g.M <= 0 || g.N <= 0) continue;
@@ -772,7 +816,7 @@ cudaError_t gemm_f64_grouped(GemmF64 p, const GemmGroup* groups, int count, int 
     const int nt = masked_tiles(mask, TM, TN, g.off);
     if (nt == 0) continue;
     if (gs.count == kMaxGroups) {
-      cudaError_t e = launch_key(p, &gs, a_kcontig, b_kcontig, v16, mask, ntiles, vecC, st);
+      cudaError_t e = launch_key(p, &gs, a_kcontig, b_kcontig, v16, mask, ntiles, vecC, st, bulk);
       if (e != cudaSuccess) return e;
       gs.count = 0; ntiles = 0;
     }
@@ -781,7 +825,7 @@ cudaError_t gemm_f64_grouped(GemmF64 p, const GemmGroup* groups, int count, int 
     ntiles += nt;
   }
   if (gs.count == 0) return cudaSuccess;
-  return launch_key(p, &gs, a_kcontig, b_kcontig, v16, mask, ntiles, vecC, st);
+  return launch_key(p, &gs, a_kcontig, b_kcontig, v16, mask, ntiles, vecC, st, bulk);
 }
 
 }  // namespace sf

@@ -42,8 +42,9 @@ namespace sf {
 // SF_P64_TIMING (calib/p64_probe.cu only): CTA 0 thread 0 records %globaltimer at phase ends
 #ifdef SF_P64_TIMING
 __device__ unsigned long long p64_times[16];
-#define P64_T(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) { unsigned long long t; \
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); p64_times[k] = t; } } while (0)
+__device__ unsigned long long p64_times_col[16];   // the first column-block CTA (blockIdx.x == nrb)
+#define P64_T(k) do { if ((blockIdx.x == 0 || (int)blockIdx.x == nrb) && threadIdx.x == 0) { unsigned long long t; \
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); (blockIdx.x == 0 ? p64_times : p64_times_col)[k] = t; } } while (0)
 // [10] earliest CTA start, [11] latest thread end, [12] latest row-block end
 #define P64_EDGE(k, op) do { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); \
   op(&p64_times[k], t); } while (0)
