@@ -437,6 +437,21 @@ __device__ __forceinline__ void ll_gather(const unsigned long long* ll, int buf,
 // registers and RPT - NR in shared memory (xs, one slot per thread: conflict-free).
 // RPT = 128, NR = 64 halves the number of CTAs (SMs) the panel occupies at the same register
 // use per CTA, so the concurrent flush keeps more SMs (measured: DESIGN.md §5 K7).
+// SF_MGS_TIMING (calib/mgs_ll_probe.cu only): thread 0 of every CTA accumulates clock64
+// cycles per phase of the column step: [0] cluster barrier, [1] DSMEM sum + LL put,
+// [2] LL gather, [3] Gram row sum (2 CTA barriers), [4] scale q_c / publish (1 barrier),
+// [5] projections + partial Gram row of c+1
+#ifdef SF_MGS_TIMING
+__device__ unsigned long long mgs_times[256][8];
+#define MG_T0() long long mg_t = clock64(); long long mg_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}
+#define MG_T(ph) do { long long t_ = clock64(); mg_acc[ph] += t_ - mg_t; mg_t = t_; } while (0)
+#define MG_TEND() do { if (threadIdx.x == 0) for (int q_ = 0; q_ < 8; ++q_) mgs_times[blockIdx.x & 255][q_] = mg_acc[q_]; } while (0)
+#else
+#define MG_T0() do {} while (0)
+#define MG_T(ph) do {} while (0)
+#define MG_TEND() do {} while (0)
+#endif
+
 template <typename T, int RPT, int NR>
 __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w, int RB, const T* __restrict__ src,
                                                                 int64_t lds, T* __restrict__ dst, int64_t ldd,
@@ -483,17 +498,21 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
   }
 
   bool ok = true;
+  MG_T0();
   for (int c = 0; c < w; ++c) {
     const int buf = c & 1;
     const unsigned ep = (unsigned)(col0 + c + 1);
     cluster.sync();   // every CTA of the cluster wrote its partial row of column c
+    MG_T(0);
     for (int j = c + k + CL * tid; j < w; j += CL * kMgsThreads) {
       T a = T(0);
       for (int rr = 0; rr < CL; ++rr) a += cluster.map_shared_rank(&mypart[buf][0], rr)[j];
       LL<T>::put(ll + LL<T>::kWords * ((size_t)(buf * Q + q) * w + j), a, ep);
     }
     const int wc = w - c, cnt = Q * wc;
+    MG_T(1);
     ll_gather<T>(ll, buf, Q, w, c, wc, cnt, ep, cval, tid);
+    MG_T(2);
     __syncthreads();
     for (int j = c + tid; j < w; j += kMgsThreads) {
       T a = T(0);
@@ -501,6 +520,7 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
       gsum[j] = a;
     }
     __syncthreads();
+    MG_T(3);
     // 1/||v_c|| without the IEEE sqrt / division subroutines (reading P11); ||v_c|| for R3
     const T rnv = fast_rsqrt(gsum[c]);
     const T nv = gsum[c] * rnv;
@@ -518,6 +538,7 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
       for (int r = 0; r < RPT; ++r) vs[h * QP + r] = X(r);
     }
     __syncthreads();
+    MG_T(4);
     const bool act = mine && cp > c;
     T acc[4] = {T(0), T(0), T(0), T(0)};   // interleaved partial sums (short dependency chains)
     if (act) {
@@ -534,7 +555,9 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
     T a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     a += __shfl_xor_sync(0xffffffffu, a, 1);
     if (act && h == 0 && c + 1 < w) mypart[buf ^ 1][cp] = a;
+    MG_T(5);
   }
+  MG_TEND();
   cluster.sync();   // no CTA leaves while a cluster peer may still read its shared memory
   if (!ok || !mine) return;
 #pragma unroll
