@@ -768,7 +768,8 @@ static LLGeom ll_geom(int64_t n, int w, bool reg) {
   if (getenv("SF_MGS_NOLL") != nullptr) return r;
   if (reg && w > 128) return r;
   const int64_t G0 = (n + 2 * rpt - 1) / (2 * rpt);
-  static int maxcl[2][9] = {{-1, -1, -1, -1, -1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1, -1, -1, -1, -1}};
+  static int maxcl[2][17] = {{-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1},
+                             {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1}};
   auto dyn_for = [&](int G, int CL) -> size_t {
     if (reg) return sizeof(T) * (((size_t)(G / CL) * (size_t)w + 1) / 2 * 2 + (size_t)(rpt - (rpt == 64 ? mgs_nr() : 64)) * kMgsThreads);
     const int RB = (int)((n + G - 1) / G);
@@ -791,6 +792,7 @@ static LLGeom ll_geom(int64_t n, int w, bool reg) {
       const void* kf = reg ? mgs_ll_reg_fn<T>() : (const void*)qr_mgs_ll_smem_kernel<T>;
       // (the register variant's dynamic size varies a little with G: allow up to 200 KB)
       cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, reg ? 200 * 1024 : (int)dyn);
+      if (CL > 8) cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       int m = 0;
       cudaError_t oe = cudaOccupancyMaxActiveClusters(&m, kf, &cfg);
       if (getenv("SF_MGS_DEBUG"))
@@ -806,7 +808,11 @@ static LLGeom ll_geom(int64_t n, int w, bool reg) {
   if (G0 <= 8) {
     if (fits((int)G0, (int)G0)) { G = (int)G0; CL = (int)G0; }
   } else {
-    for (int cl : {8, 4}) {
+    // SF_MGS_CL16: try non-portable 16-CTA clusters first (half as many clusters to exchange
+    // through global memory, twice the partial rows summed in distributed shared memory)
+    static const bool cl16 = getenv("SF_MGS_CL16") && atoi(getenv("SF_MGS_CL16"));
+    for (int cl : {16, 8, 4}) {
+      if (cl == 16 && !cl16) continue;
       const int g = (int)((G0 + cl - 1) / cl * cl);
       if (fits(cl, g)) { G = g; CL = cl; break; }
     }

@@ -34,6 +34,7 @@ python tools/prof_fact.py chol 256 16 > /dev/null 2>&1 && \
 for r in lu_flush lu_f1 lu_panel64 qr_flush qr_mgs syrk_cfg5 syrk_cfg3 tf32_cfg5 chol_small; do
   echo "== $r"; python tools/ncu_summary.py rep $O/$r.ncu-rep 2>&1
 done > $O/ncu_summary.txt
+rm -f $O/*.ncu-rep   # gpurun copies back <= 64 MiB: keep the summaries, not the reports
 python tools/ncu_summary.py launches $O/launches_cfg5.csv > $O/launches_cfg5_summary.txt 2>&1
 tail -2 $O/pytest_gpu.log; cat $O/smoke.log | tail -1
 for f in $O/bench_*.json; do echo "== $f"; cut -c1-200 $f; done
