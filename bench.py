@@ -389,6 +389,8 @@ def main():
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):
         traffic = json.load(open(tr_path)).get(args.workload)
+    if dtype == "f32" and kind != "chol" and achieved:
+        achieved *= 3.0   # LU / QR fp32 drivers count useful flops; 3xTF32 executes three products
     if dtype == "f32":
         # TF32 dense peak = measured bf16 (sustained: the kernel runs inside a long step) x
         # the nominal tf32/bf16 ratio 1.1/2.25 (B200_PROFILING.md)
