@@ -190,6 +190,7 @@ def parse():
                     help="multi-GPU panel transport: device-initiated push (f3, sf_comm_set_push) instead of ncclBroadcast")
     ap.add_argument("--loopback", type=int, default=0,
                     help="test mode: run the distributed driver with G ranks emulated on this one GPU")
+    ap.add_argument("--strassen-levels", type=int, default=1, help="Strassen recursion depth with --strassen (1-3)")
     ap.add_argument("--strassen", type=int, default=0, metavar="MIN_DIM",
                     help="f1: one Strassen-Winograd level in fp64 flushes with sides >= MIN_DIM (0 = off)")
     return ap.parse_args()
@@ -339,7 +340,7 @@ def main():
             sf.qr_colmajor(n, s, A, n, out1, n, out2, n, info, stream=stream)
 
     if args.strassen:
-        sf.set_strassen(1, args.strassen)
+        sf.set_strassen(args.strassen_levels, args.strassen)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -540,7 +541,7 @@ def main():
                 "vs_baseline": None, "dtype": dtype, "data": "synthetic",
                 "config": {"workload": args.workload, "kind": kind, "n": n, "s": s, "baseline_config": cfgname,
                            "generator": gen, "seed": args.seed, "parallelism": par,
-                           **({"strassen": {"levels": 1, "min_dim": args.strassen,
+                           **({"strassen": {"levels": args.strassen_levels, "min_dim": args.strassen,
                                             "note": "roofline.achieved counts classical-equivalent flops"}}
                               if args.strassen else {}),
                            "l2": f"inputs larger than L2 ({A.numel() * A.element_size() / 1e9:.2f} GB per rank "

@@ -212,14 +212,15 @@ int qr_factor_dist(sf_comm_t comm, int64_t n, int64_t s, int dtype, void* const*
                    void* const* dR_local, int64_t ld_local, int64_t* const* d_info, void* stream);
 
 /* Fast multiplication in the flush ("using a fast
- * rectangular matrix multiplication algorithm", 186-188).  levels = 1: fp64 flushes whose
- * two output sides are >= min_dim use ONE Strassen-Winograd level (7 half-size DMMA
- * products, operand/output block sums elementwise; uneven halves zero-padded) — LU's
- * A -= R_L R_U, QR's M -= B_Q C, and the off-diagonal half of Cholesky's A -= R R^T.
- * levels = 0 (default): classical products only.  Process-wide, single-GPU drivers, fp64;
- * clears the library's captured CUDA graphs.  Rounding differs from the classical product
- * (normwise error bound, not componentwise).  Errors: SF_EINVAL if levels not in {0, 1} or
- * min_dim < 64. */
+ * rectangular matrix multiplication algorithm", 186-190: the paper used 2-3 recursions).
+ * levels = L in 1..3: fp64 flushes whose two output sides are >= min_dim use Strassen-
+ * Winograd (7 half-size products, operand/output block sums elementwise; uneven halves
+ * zero-padded), the half-size products recursing while they still meet min_dim, at most L
+ * levels deep — LU's A -= R_L R_U, QR's M -= B_Q C, and the off-diagonal half of Cholesky's
+ * A -= R R^T.  levels = 0 (default): classical products only.  Process-wide, single-GPU
+ * drivers, fp64; clears the library's captured CUDA graphs.  Rounding differs from the
+ * classical product (normwise error bound, not componentwise).  Errors: SF_EINVAL if levels
+ * not in 0..3 or min_dim < 64. */
 int sf_set_strassen(int levels, int64_t min_dim);
 
 /* Number of flushes the c = z+s schedule performs: floor((n-1)/s). */

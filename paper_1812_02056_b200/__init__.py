@@ -170,7 +170,7 @@ def launch_counter():
 
 
 def set_strassen(levels, min_dim=4096):
-    """sf_set_strassen: one Strassen-Winograd level in fp64 flushes with sides >= min_dim (f1)."""
+    """sf_set_strassen: Strassen-Winograd (levels 1-3, 0 = off) in fp64 flushes with sides >= min_dim (f1)."""
     _check(lib().sf_set_strassen(int(levels), int(min_dim)))
 
 

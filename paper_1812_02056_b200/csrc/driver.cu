@@ -1062,7 +1062,7 @@ int64_t sf_launch_counter(void) { return g_launches.load(); }
 
 int sf_set_strassen(int levels, int64_t min_dim) {
   SF_API_LOCK;
-  if (levels < 0 || levels > 1 || min_dim < 64) return fail_with(SF_EINVAL, "strassen: levels must be 0 or 1, min_dim >= 64");
+  if (levels < 0 || levels > 3 || min_dim < 64) return fail_with(SF_EINVAL, "strassen: levels must be 0..3, min_dim >= 64");
   strassen_cfg().levels = levels;
   strassen_cfg().min_dim = min_dim;
   for (auto& g : g_graphs)   // captured factorizations embed the old choice

@@ -339,11 +339,15 @@ inline const T* opblk(const T* X, int64_t ld, int kc, int64_t r0, int64_t c0) {
   return X + (kc ? c0 + r0 * ld : r0 + c0 * ld);
 }
 
-// C = Cin - op(A) op(B), one Strassen-Winograd level (fp64).  C may equal Cin (in place).
+inline bool strassen_applies(int64_t M, int64_t N, int64_t K);
+
+// C = beta*Cin + alpha*op(A) op(B) (alpha = +-1, beta in {0, 1}) by Strassen-Winograd, `depth`
+// levels deep (PAPER.md:186-190 used 2-3 recursions): the 7 half-size products recurse while
+// they still meet the size threshold.  fp64.  C may equal Cin (in place); beta = 0 never reads Cin.
 template <typename T>
-inline cudaError_t strassen_sub(int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, int ak, const T* B,
-                                int64_t ldb, int bk, const T* Cin, int64_t ldcin, T* C, int64_t ldc,
-                                const long long* fail, cudaStream_t st) {
+inline cudaError_t strassen_gen(int64_t M, int64_t N, int64_t K, T alpha, const T* A, int64_t lda, int ak, const T* B,
+                                int64_t ldb, int bk, int beta, const T* Cin, int64_t ldcin, T* C, int64_t ldc,
+                                const long long* fail, cudaStream_t st, int depth) {
   const int64_t m1 = (M + 1) / 2, m2 = M - m1, k1 = (K + 1) / 2, k2 = K - k1, n1 = (N + 1) / 2, n2 = N - n1;
   // op(B)(k, j): bk ? B[k + j*ldb] : B[j + k*ldb]  ->  as an "op(X)(row k, col j)" with kc = !bk
   const int bkc = bk ? 0 : 1;
@@ -358,6 +362,7 @@ inline cudaError_t strassen_sub(int64_t M, int64_t N, int64_t K, const T* A, int
   T *T1 = ws.take<T>(k1 * n1), *T2 = ws.take<T>(k1 * n1), *T3 = ws.take<T>(k1 * n1), *T4 = ws.take<T>(k1 * n1);
   T *W = ws.take<T>(m1 * n1), *V = ws.take<T>(m1 * n1), *X = ws.take<T>(m1 * n1);
   const T one = T(1), mone = T(-1);
+  const T* cin = beta ? Cin : nullptr;   // beta = 0: the block sums read zeros, not Cin
 #define SF_TRY(x) do { e = (x); if (e != cudaSuccess) return e; } while (0)
   // operand block sums (zero padded to m1 x k1 / k1 x n1)
   SF_TRY(comb<T>(m1, k1, one, A21, lda, ak, m2, k1, one, A22, lda, ak, m2, k2, S1, m1, st));   // S1 = A21 + A22
@@ -368,30 +373,44 @@ inline cudaError_t strassen_sub(int64_t M, int64_t N, int64_t K, const T* A, int
   SF_TRY(comb<T>(k1, n1, one, B22, ldb, bkc, k2, n2, mone, T1, k1, 0, k1, n1, T2, k1, st));     // T2 = B22 - T1
   SF_TRY(comb<T>(k1, n1, one, B22, ldb, bkc, k2, n2, mone, B12, ldb, bkc, k1, n2, T3, k1, st)); // T3 = B22 - B12
   SF_TRY(comb<T>(k1, n1, one, T2, k1, 0, k1, n1, mone, B21, ldb, bkc, k2, n1, T4, k1, st));     // T4 = T2 - B21
+  // c = beta_p*cin + alpha_p*op(a) op(b): one more Strassen level while the product is large
   auto prod = [&](int64_t mm, int64_t nn, int64_t kk, const T* a, int64_t la, int aak, const T* b, int64_t lb, int bbk,
-                  double alpha, int beta, const T* cin, int64_t lci, T* c, int64_t lc) -> cudaError_t {
+                  double alpha_p, int beta_p, const T* ci, int64_t lci, T* c, int64_t lc) -> cudaError_t {
     if (mm <= 0 || nn <= 0) return cudaSuccess;
-    Gemm<T> g{mm, nn, kk, a, la, aak, b, lb, bbk, cin, lci, c, lc, alpha, beta, kMaskNone, 1, nullptr, fail};
+    if (depth > 1 && strassen_applies(mm, nn, kk))
+      return strassen_gen<T>(mm, nn, kk, (T)alpha_p, a, la, aak, b, lb, bbk, beta_p, ci, lci, c, lc, fail, st, depth - 1);
+    Gemm<T> g{mm, nn, kk, a, la, aak, b, lb, bbk, ci, lci, c, lc, alpha_p, beta_p, kMaskNone, 1, nullptr, fail};
     return run_gemm(g, st);
   };
+  const double al = (double)alpha;
   // products (gemm operands: plain temps are idx-contiguous: ak = 0; as B: bk = 1 means B[k + j*ld])
   SF_TRY(prod(m1, n1, k1, A11, lda, ak, B11, ldb, bk, 1.0, 0, nullptr, 0, W, m1));  // W = P1
-  SF_TRY(comb<T>(m1, n1, one, Cin, ldcin, 0, m1, n1, mone, W, m1, 0, m1, n1, C, ldc, st));            // C11 = Cin11 - P1
-  SF_TRY(prod(m1, n1, k2, A12, lda, ak, B21, ldb, bk, -1.0, 1, C, ldc, C, ldc));   // C11 -= P2
+  SF_TRY(comb<T>(m1, n1, one, cin, ldcin, 0, m1, n1, alpha, W, m1, 0, m1, n1, C, ldc, st));           // C11 = b Cin11 + a P1
+  SF_TRY(prod(m1, n1, k2, A12, lda, ak, B21, ldb, bk, al, 1, C, ldc, C, ldc));      // C11 += a P2
   SF_TRY(prod(m1, n1, k1, S2, m1, 0, T2, k1, 1, 1.0, 1, W, m1, W, m1));             // W = U2
   SF_TRY(prod(m1, n1, k1, S3, m1, 0, T3, k1, 1, 1.0, 1, W, m1, V, m1));             // V = U3
   SF_TRY(prod(m1, n1, k1, S1, m1, 0, T1, k1, 1, 1.0, 0, nullptr, 0, X, m1));        // X = P5
   T* C21 = C + m1;
-  const T* Cin21 = Cin + m1;
-  SF_TRY(comb<T>(m2, n1, one, Cin21, ldcin, 0, m2, n1, mone, V, m1, 0, m1, n1, C21, ldc, st));         // C21 = Cin21 - U3
-  SF_TRY(prod(m2, n1, k2, A22, lda, ak, T4, k1, 1, 1.0, 1, C21, ldc, C21, ldc)); // C21 += P4
+  const T* Cin21 = cin ? cin + m1 : nullptr;
+  SF_TRY(comb<T>(m2, n1, one, Cin21, ldcin, 0, m2, n1, alpha, V, m1, 0, m1, n1, C21, ldc, st));        // C21 = b Cin21 + a U3
+  SF_TRY(prod(m2, n1, k2, A22, lda, ak, T4, k1, 1, -al, 1, C21, ldc, C21, ldc));   // C21 -= a P4
   SF_TRY(comb<T>(m1, n1, one, V, m1, 0, m1, n1, one, X, m1, 0, m1, n1, V, m1, st));                    // V = U7
-  SF_TRY(comb<T>(m2, n2, one, Cin21 + n1 * ldcin, ldcin, 0, m2, n2, mone, V, m1, 0, m1, n1, C21 + n1 * ldc, ldc, st));
+  SF_TRY(comb<T>(m2, n2, one, cin ? Cin21 + n1 * ldcin : nullptr, ldcin, 0, m2, n2, alpha, V, m1, 0, m1, n1,
+                 C21 + n1 * ldc, ldc, st));                                                            // C22
   SF_TRY(comb<T>(m1, n1, one, W, m1, 0, m1, n1, one, X, m1, 0, m1, n1, W, m1, st));                    // W = U4
-  SF_TRY(comb<T>(m1, n2, one, Cin + n1 * ldcin, ldcin, 0, m1, n2, mone, W, m1, 0, m1, n1, C + n1 * ldc, ldc, st));
-  SF_TRY(prod(m1, n2, k2, S4, m1, 0, B22, ldb, bk, -1.0, 1, C + n1 * ldc, ldc, C + n1 * ldc, ldc));                                                                       // C12 -= P3
+  SF_TRY(comb<T>(m1, n2, one, cin ? cin + n1 * ldcin : nullptr, ldcin, 0, m1, n2, alpha, W, m1, 0, m1, n1,
+                 C + n1 * ldc, ldc, st));                                                              // C12 = b Cin12 + a U4
+  SF_TRY(prod(m1, n2, k2, S4, m1, 0, B22, ldb, bk, al, 1, C + n1 * ldc, ldc, C + n1 * ldc, ldc));      // C12 += a P3
 #undef SF_TRY
   return cudaSuccess;
+}
+
+// C = Cin - op(A) op(B) by Strassen-Winograd (the flush; strassen_cfg().levels levels).
+template <typename T>
+inline cudaError_t strassen_sub(int64_t M, int64_t N, int64_t K, const T* A, int64_t lda, int ak, const T* B,
+                                int64_t ldb, int bk, const T* Cin, int64_t ldcin, T* C, int64_t ldc,
+                                const long long* fail, cudaStream_t st) {
+  return strassen_gen<T>(M, N, K, T(-1), A, lda, ak, B, ldb, bk, 1, Cin, ldcin, C, ldc, fail, st, strassen_cfg().levels);
 }
 
 inline bool strassen_applies(int64_t M, int64_t N, int64_t K) {

@@ -151,7 +151,8 @@ def test_new_entry_points_reject_bad_arguments(L):
 def test_set_strassen_arguments(L):
     """sf_set_strassen validates synchronously (no GPU needed) and 0 restores the default."""
     SF_EINVAL = 1
-    assert L.sf_set_strassen(2, 4096) == SF_EINVAL
+    assert L.sf_set_strassen(4, 4096) == SF_EINVAL
+    assert L.sf_set_strassen(2, 4096) == 0 and L.sf_set_strassen(3, 4096) == 0   # PAPER.md:186-190: 2-3 levels
     assert L.sf_set_strassen(1, 10) == SF_EINVAL
     assert L.sf_set_strassen(-1, 4096) == SF_EINVAL
     assert L.sf_set_strassen(0, 4096) == 0
