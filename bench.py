@@ -367,6 +367,7 @@ def main():
         dist.barrier()
     l1 = sf.launch_counter()
     prof = sf.profile_collect()
+    prof_union = sf.profile_union()
     sf.profile_enable(False)
     ck = clocks.stop()
     ms = e0.elapsed_time(e1)
@@ -414,6 +415,13 @@ def main():
                               + (", rank 0" if ws > 1 else ""),
                     "peak_source": "measured: calib/peaks_fp64_tf32.json fp64_dmma_tflops (DMMA microbenchmark, "
                                    "this pool's B200); MEASURED_PEAKS.json has no fp64 entry"}
+    # wall-clock view: the flush flops over the union of the flush regions (LU's lookahead runs
+    # flush parts on two streams at once, which the per-launch average above counts twice)
+    upd_wall = prof_union.get("update", 0.0)
+    if upd_wall > 0 and achieved:
+        roofline["achieved_wall"] = achieved * upd_ms / upd_wall
+        roofline["frac_wall"] = roofline["achieved_wall"] / peak if peak else None
+        roofline["update_wall_ms_per_step"] = upd_wall / args.steps
     roofline.update({"launches_per_step": upd_n / args.steps if args.steps else None,
                      "avg_launch_ms": upd_ms / upd_n if upd_n else None,
                      "flops_per_launch": upd_fl / upd_n if upd_n else None,

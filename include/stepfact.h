@@ -247,6 +247,11 @@ int64_t sf_launch_counter(void);
  * bytes); arrays of length 4; then it clears the record.  Not for use during graph capture. */
 void sf_profile_enable(int on);
 int sf_profile_collect(double* ms, int64_t* count, double* flops);
+/* Per kind, the wall-clock milliseconds covered by the union of the regions the last
+ * sf_profile_collect summed (regions on different streams may overlap: LU's lookahead flush
+ * part on the panel stream beside the rest of the flush).  ms_union: 4 doubles.  SF_EINVAL
+ * for NULL. */
+int sf_profile_union(double* ms_union);
 
 const char* sf_strerror(int status);
 const char* sf_last_error(void);

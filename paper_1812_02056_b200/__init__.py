@@ -109,6 +109,8 @@ def lib():
     L.sf_profile_enable.restype = None
     L.sf_profile_collect.argtypes = [p, p, p]
     L.sf_profile_collect.restype = i32
+    L.sf_profile_union.argtypes = [p]
+    L.sf_profile_union.restype = i32
     _lib = L
     return L
 
@@ -119,7 +121,8 @@ EXPORTS = ("chol_factor", "lu_factor", "qr_factor", "chol_factor_host", "lu_fact
            "sf_profile_collect", "sf_get_unique_id", "sf_comm_init", "sf_comm_init_loopback", "sf_comm_destroy",
            "sf_comm_size", "sf_comm_local_ranks", "sf_local_cols", "chol_factor_dist", "lu_factor_dist",
            "qr_factor_dist", "chol_factor_steps", "lu_factor_steps", "qr_factor_steps", "chol_solve", "lu_solve",
-           "qr_solve", "sf_set_strassen", "sf_schedule", "sf_comm_bcast_bytes", "sf_comm_set_push")
+           "qr_solve", "sf_set_strassen", "sf_schedule", "sf_comm_bcast_bytes", "sf_comm_set_push",
+           "sf_profile_union")
 
 
 def _check(rc):
@@ -184,6 +187,13 @@ def profile_collect():
     ms = (ctypes.c_double * 4)(); cnt = (ctypes.c_int64 * 4)(); fl = (ctypes.c_double * 4)()
     _check(lib().sf_profile_collect(ctypes.addressof(ms), ctypes.addressof(cnt), ctypes.addressof(fl)))
     return {k: (ms[i], cnt[i], fl[i]) for i, k in enumerate(("update", "panel", "qr_r", "bcast"))}
+
+
+def profile_union():
+    """{kind: wall-clock ms of the union of that kind's regions} from the last profile_collect."""
+    ms = (ctypes.c_double * 4)()
+    _check(lib().sf_profile_union(ctypes.addressof(ms)))
+    return {k: ms[i] for i, k in enumerate(("update", "panel", "qr_r", "bcast"))}
 
 
 # ----------------------------------------------------------------------- raw column-major API

@@ -13,6 +13,7 @@
 // Panels wider than the leaf width are factored recursively: factor the left half,
 // subtract its contribution from the right half with one GEMM (the same terms the paper's
 // k-loops subtract, grouped), factor the right half.  DESIGN.md §5 discusses why.
+#include <algorithm>
 #include <type_traits>
 #include <atomic>
 #include <cstdarg>
@@ -1076,21 +1077,46 @@ void sf_profile_enable(int on) {
   g_prof = on != 0;
 }
 
+static double g_prof_union[4] = {0.0, 0.0, 0.0, 0.0};
+
 int sf_profile_collect(double* ms, int64_t* count, double* flops) {
   SF_API_LOCK;
-  for (int k = 0; k < 4; ++k) { ms[k] = 0.0; count[k] = 0; flops[k] = 0.0; }
+  for (int k = 0; k < 4; ++k) { ms[k] = 0.0; count[k] = 0; flops[k] = 0.0; g_prof_union[k] = 0.0; }
   int rc = SF_OK;
+  // per kind: the intervals on a common time axis (relative to the first recorded event), so
+  // that regions running concurrently on two streams (LU's two-deep lookahead: F1 on the
+  // panel stream beside F2/F3) are also reported as their wall-clock union
+  std::vector<std::pair<double, double>> iv[4];
+  const cudaEvent_t ref = g_prof_recs.empty() ? nullptr : g_prof_recs.front().a;
   for (auto& r : g_prof_recs) {
     if (r.kind < 0 || r.kind > 3) continue;
-    float t = 0.f;
+    float t = 0.f, t0 = 0.f;
     cudaError_t e = cudaEventSynchronize(r.b);
     if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t0, ref, r.a);
     if (e != cudaSuccess) rc = fail_with(SF_ECUDA, "profile events: %s", cudaGetErrorString(e));
     ms[r.kind] += t; count[r.kind] += 1; flops[r.kind] += r.flops;
-    g_event_pool.push_back(r.a); g_event_pool.push_back(r.b);
+    iv[r.kind].push_back({(double)t0, (double)t0 + t});
   }
+  for (int k = 0; k < 4; ++k) {
+    std::sort(iv[k].begin(), iv[k].end());
+    double cur_a = 0.0, cur_b = -1.0;
+    for (auto& x : iv[k]) {
+      if (x.first > cur_b) { if (cur_b > cur_a) g_prof_union[k] += cur_b - cur_a; cur_a = x.first; cur_b = x.second; }
+      else if (x.second > cur_b) cur_b = x.second;
+    }
+    if (cur_b > cur_a) g_prof_union[k] += cur_b - cur_a;
+  }
+  for (auto& r : g_prof_recs) { g_event_pool.push_back(r.a); g_event_pool.push_back(r.b); }
   g_prof_recs.clear();
   return rc;
+}
+
+int sf_profile_union(double* ms_union) {
+  SF_API_LOCK;
+  if (!ms_union) return fail_with(SF_EINVAL, "sf_profile_union: null output");
+  for (int k = 0; k < 4; ++k) ms_union[k] = g_prof_union[k];
+  return SF_OK;
 }
 
 const char* sf_strerror(int status) {
