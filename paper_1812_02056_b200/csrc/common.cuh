@@ -82,6 +82,13 @@ __device__ __forceinline__ float fast_rsqrt(float d) {
   return y * fmaf(-h * y, y, 1.5f);
 }
 
+// round to TF32, nearest with ties away (the 3xTF32 split: hi = tf32_rna(x), lo = tf32_rna(x - hi))
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -152,7 +152,8 @@ static int chol_run_f32(int64_t n, const Sched& S, const float* A, int64_t lda, 
     const int64_t w0 = S.w(0);
     SF_CUDA(chol_panel_rec_f32(n, w0, A, lda, L, ldl, 0, sb[0], fail, st));
     if (hook) SF_CUDA(hook->done(0, w0, st));
-    if (w0 < n) SF_CUDA(split_tf32(n - w0, w0, L + w0, ldl, sb[0].at(w0, 0).h, sb[0].at(w0, 0).l, ldk, st));
+    if (w0 < n && !chol32_fused_split(n))
+      SF_CUDA(split_tf32(n - w0, w0, L + w0, ldl, sb[0].at(w0, 0).h, sb[0].at(w0, 0).l, ldk, st));
   }
   for (int64_t p = 0; p + 1 < S.P(); ++p) {
     const int64_t z = S.z(p), w = S.w(p), c = z + w;
@@ -174,7 +175,8 @@ static int chol_run_f32(int64_t n, const Sched& S, const float* A, int64_t lda, 
       ProfScope ps(1, 0.0, pst);
       SF_CUDA(chol_panel_rec_f32(m, w2, L + c + c * ldl, ldl, L + c + c * ldl, ldl, c, nxt, fail, pst));
       if (hook) SF_CUDA(hook->done(c, w2, pst));
-      if (w2 < m) SF_CUDA(split_tf32(m - w2, w2, L + c + w2 + c * ldl, ldl, nxt.at(w2, 0).h, nxt.at(w2, 0).l, ldk, pst));
+      if (w2 < m && !chol32_fused_split(m))
+        SF_CUDA(split_tf32(m - w2, w2, L + c + w2 + c * ldl, ldl, nxt.at(w2, 0).h, nxt.at(w2, 0).l, ldk, pst));
     }
     if (la) {
       if (m > w2) {

@@ -504,17 +504,28 @@ inline cudaError_t syrk_tf32(int64_t M, int64_t N, int64_t K, const SplitBuf& a,
 // `sb` before the 3xTF32 correction of the right half.  On return the panel's columns are
 // split for rows [w, m) only up to the last left half: the caller splits the whole panel
 // for the flush.
+// fp32 panels whose leaves are one-launch panels (panel64) write the split of every row below
+// their diagonal blocks themselves (the substitution's final registers), so neither the
+// recursion nor the caller needs a separate split pass over those rows.
+inline bool chol32_fused_split(int64_t m) {
+  // measured slower (cfg3 fp32 23.2 vs 22.3 ms, cfg5 fp32 ~499 vs ~494 ms): each thread stores
+  // its own row's split (one sector per lane) where split_tf32 transposes through shared memory
+  static const int on = [] { const char* e = getenv("SF_CHOL32_FUSED_SPLIT"); return e ? atoi(e) : 0; }();
+  return on && m <= chol32_p64_maxm();
+}
+
 inline cudaError_t chol_panel_rec_f32(int64_t m, int64_t w, const float* src, int64_t lds, float* dst, int64_t ldd,
                                       int64_t col0, SplitBuf sb, long long* fail, cudaStream_t st) {
   const bool p64 = m <= chol32_p64_maxm();
   const int leaf = p64 ? 64 : chol_leaf_width();
   if (w <= leaf)
-    return p64 ? chol_panel64<float>(m, (int)w, src, lds, dst, ldd, col0, fail, st)
+    return p64 ? chol_panel64<float>(m, (int)w, src, lds, dst, ldd, col0, fail, st,
+                                     chol32_fused_split(m) ? sb.h : nullptr, sb.l, sb.ldk)
                : chol_leaf<float>(m, (int)w, src, lds, dst, ldd, col0, fail, st);
   const int64_t h = half_of(w, leaf);
   cudaError_t e = chol_panel_rec_f32(m, h, src, lds, dst, ldd, col0, sb, fail, st);
   if (e != cudaSuccess) return e;
-  e = split_tf32(m - h, h, dst + h, ldd, sb.at(h, 0).h, sb.at(h, 0).l, sb.ldk, st);
+  if (!chol32_fused_split(m)) e = split_tf32(m - h, h, dst + h, ldd, sb.at(h, 0).h, sb.at(h, 0).l, sb.ldk, st);
   if (e != cudaSuccess) return e;
   const SplitBuf lh = sb.at(h, 0);
   e = syrk_tf32(m - h, w - h, h, lh, lh, src + h + h * lds, lds, dst + h + h * ldd, ldd, fail, st);

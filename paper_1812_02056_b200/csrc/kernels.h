@@ -105,9 +105,12 @@ cudaError_t lu_panel64(int64_t m, int64_t ncr, int w, const T* src, int64_t lds,
 bool chol_small_applies(int64_t n, int64_t s, int elt);
 cudaError_t chol_small(int64_t n, int64_t s, const double* A, int64_t lda, double* L, int64_t ldl, long long* fail,
                        cudaStream_t st);
+// sph / spl (fp32 only, may be NULL): also write the 3xTF32 split (hi / lo) of the rows below
+// the diagonal block, K-major with row stride spld, row r of the panel at sph + r*spld.
 template <typename T>
 cudaError_t chol_panel64(int64_t m, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
-                         long long* fail, cudaStream_t st);
+                         long long* fail, cudaStream_t st, float* sph = nullptr, float* spl = nullptr,
+                         int64_t spld = 0);
 
 // LU U rows only, against an already factored diagonal block L11 (ldl): the U part of
 // lu_leaf for ncols columns (block-cyclic distributed LU).

@@ -181,7 +181,7 @@ __device__ __forceinline__ bool p64_factor_quarter(T* D, T* inv, int o, int wq, 
 // register window for columns c0..c0+JN-1; on return it has moved on by 8 columns.
 template <typename T, int JN>
 __device__ __forceinline__ void p64_subst_block(T (&x)[p64::W], const T* Op, const T* inv, bool use_u, int c0, int w,
-                                                T* out, int64_t ostride) {
+                                                T* out, int64_t ostride, float* sh = nullptr, float* sl = nullptr) {
   using namespace p64;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
@@ -198,6 +198,19 @@ __device__ __forceinline__ void p64_subst_block(T (&x)[p64::W], const T* Op, con
 #pragma unroll
   for (int c = 0; c < 8; ++c)
     if (c0 + c < w) out[(int64_t)(c0 + c) * ostride] = x[c];
+  if constexpr (std::is_same<T, float>::value) {
+    // fp32 Cholesky rows: the 3xTF32 split of the final values, K-major (what split_tf32
+    // would produce from `out` afterwards, computed from the same registers)
+    if (sh) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c0 + c < w) {
+          const float hi = tf32_rna(x[c]);
+          sh[c0 + c] = hi;
+          sl[c0 + c] = tf32_rna(x[c] - hi);
+        }
+    }
+  }
 #pragma unroll
   for (int j = 0; j < JN - 8; ++j) x[j] = x[j + 8];
 #pragma unroll
@@ -210,7 +223,8 @@ __device__ __forceinline__ void p64_subst_block(T (&x)[p64::W], const T* Op, con
 template <typename T, bool LU>
 __global__ void __launch_bounds__(p64::NT) panel64_kernel(int64_t m, int64_t ncr, int w, const T* __restrict__ src,
                                                           int64_t lds, T* __restrict__ dst, int64_t ldd, int64_t col0,
-                                                          const T* tolp, long long* fail, int nrb) {
+                                                          const T* tolp, long long* fail, int nrb, float* sph,
+                                                          float* spl, int64_t spld) {
   using namespace p64;
   if (threadIdx.x == 0) P64_EDGE(10, atomicMin);
   if (failed(fail)) return;
@@ -369,10 +383,13 @@ __global__ void __launch_bounds__(p64::NT) panel64_kernel(int64_t m, int64_t ncr
   const int64_t ostride = rowblock ? ldd : 1;
   const int nb = (w + 7) / 8;
   const int nb1 = nb < 4 ? nb : 4;
+  // fp32 Cholesky: this row's split (hi / lo, K-major, row r of the panel below the block)
+  float* sh = (!LU && rowblock && sph) ? sph + r * spld : nullptr;
+  float* sl = sh ? spl + r * spld : nullptr;
 #pragma unroll 1
-  for (int b = 0; b < nb1; ++b) p64_subst_block<T, 64>(x, Op, inv, use_u, 8 * b, w, out, ostride);
+  for (int b = 0; b < nb1; ++b) p64_subst_block<T, 64>(x, Op, inv, use_u, 8 * b, w, out, ostride, sh, sl);
 #pragma unroll 1
-  for (int b = 4; b < nb; ++b) p64_subst_block<T, 32>(x, Op, inv, use_u, 8 * b, w, out, ostride);
+  for (int b = 4; b < nb; ++b) p64_subst_block<T, 32>(x, Op, inv, use_u, 8 * b, w, out, ostride, sh, sl);
   P64_T(9);
   P64_EDGE(11, atomicMax);
   if (rowblock) P64_EDGE(12, atomicMax);
@@ -380,7 +397,8 @@ __global__ void __launch_bounds__(p64::NT) panel64_kernel(int64_t m, int64_t ncr
 
 template <typename T, bool LU>
 static cudaError_t launch_panel64(int64_t m, int64_t ncr, int w, const T* src, int64_t lds, T* dst, int64_t ldd,
-                                  int64_t col0, const T* tol, long long* fail, cudaStream_t st) {
+                                  int64_t col0, const T* tol, long long* fail, cudaStream_t st, float* sph = nullptr,
+                                  float* spl = nullptr, int64_t spld = 0) {
   if (w <= 0 || m <= 0) return cudaSuccess;
   if (w > p64::W) return cudaErrorInvalidValue;
   const int64_t below = m - w;
@@ -395,7 +413,8 @@ static cudaError_t launch_panel64(int64_t m, int64_t ncr, int w, const T* src, i
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  panel64_kernel<T, LU><<<grid, p64::NT, dyn, st>>>(m, LU ? ncr : 0, w, src, lds, dst, ldd, col0, tol, fail, nrb);
+  panel64_kernel<T, LU><<<grid, p64::NT, dyn, st>>>(m, LU ? ncr : 0, w, src, lds, dst, ldd, col0, tol, fail, nrb, sph,
+                                                     spl, spld);
   count_launch();
   return cudaGetLastError();
 }
@@ -407,8 +426,8 @@ cudaError_t lu_panel64(int64_t m, int64_t ncr, int w, const T* src, int64_t lds,
 }
 template <typename T>
 cudaError_t chol_panel64(int64_t m, int w, const T* src, int64_t lds, T* dst, int64_t ldd, int64_t col0,
-                         long long* fail, cudaStream_t st) {
-  return launch_panel64<T, false>(m, 0, w, src, lds, dst, ldd, col0, nullptr, fail, st);
+                         long long* fail, cudaStream_t st, float* sph, float* spl, int64_t spld) {
+  return launch_panel64<T, false>(m, 0, w, src, lds, dst, ldd, col0, nullptr, fail, st, sph, spl, spld);
 }
 
 template cudaError_t lu_panel64<double>(int64_t, int64_t, int, const double*, int64_t, double*, int64_t, int64_t,
@@ -416,8 +435,8 @@ template cudaError_t lu_panel64<double>(int64_t, int64_t, int, const double*, in
 template cudaError_t lu_panel64<float>(int64_t, int64_t, int, const float*, int64_t, float*, int64_t, int64_t,
                                        const float*, long long*, cudaStream_t);
 template cudaError_t chol_panel64<double>(int64_t, int, const double*, int64_t, double*, int64_t, int64_t, long long*,
-                                          cudaStream_t);
+                                          cudaStream_t, float*, float*, int64_t);
 template cudaError_t chol_panel64<float>(int64_t, int, const float*, int64_t, float*, int64_t, int64_t, long long*,
-                                         cudaStream_t);
+                                         cudaStream_t, float*, float*, int64_t);
 
 }  // namespace sf
