@@ -433,6 +433,38 @@ __device__ __forceinline__ void ll_gather(const unsigned long long* ll, int buf,
   }
 }
 
+// Gather + sum in one pass: thread t polls the Q cluster sums of column j = c + t (all its
+// words requested before any is checked, one L2 round trip per poll pass) and adds them in
+// cluster order q = 0, 1, ... (the order of the two-pass gather + sum: the same bits), so the
+// Gram row needs no staging buffer and one CTA barrier instead of two.
+template <typename T>
+__device__ __forceinline__ void ll_gather_sum(const unsigned long long* ll, int buf, int Q, int w, int c, unsigned ep,
+                                              T* gsum, int tid) {
+  for (int j = c + tid; j < w; j += kMgsThreads) {
+    T a = T(0);
+    for (int q0 = 0; q0 < Q; q0 += 8) {   // 8 words in flight (registers, static indices)
+      T v[8];
+      unsigned pending = 0;                // bit u: word q0 + u not yet valid
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        v[u] = T(0);
+        if (q0 + u < Q && !LL<T>::get(ll + LL<T>::kWords * ((size_t)(buf * Q + q0 + u) * w + j), ep, v[u]))
+          pending |= 1u << u;
+      }
+      while (pending) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if ((pending >> u) & 1u)
+            if (LL<T>::get(ll + LL<T>::kWords * ((size_t)(buf * Q + q0 + u) * w + j), ep, v[u])) pending &= ~(1u << u);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q0 + u < Q) a += v[u];
+    }
+    gsum[j] = a;
+  }
+}
+
 // RPT = rows of its column half a thread owns (the CTA holds 2 * RPT rows), NR of them in
 // registers and RPT - NR in shared memory (xs, one slot per thread: conflict-free).
 // RPT = 128, NR = 64 halves the number of CTAs (SMs) the panel occupies at the same register
@@ -456,7 +488,8 @@ template <typename T, int RPT, int NR>
 __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w, int RB, const T* __restrict__ src,
                                                                 int64_t lds, T* __restrict__ dst, int64_t ldd,
                                                                 int64_t col0, const T* tolp,
-                                                                unsigned long long* ll, long long* fail) {
+                                                                unsigned long long* ll, long long* fail,
+                                                                int mgs_two_pass) {
   if (failed(fail)) return;      // stable during the launch: every CTA of a cluster agrees
   constexpr int QP = RPT + 2;
   __shared__ T qs[2 * QP], vs[2 * QP];
@@ -509,15 +542,20 @@ __global__ void __launch_bounds__(kMgsThreads) qr_mgs_ll_kernel(int64_t n, int w
       for (int rr = 0; rr < CL; ++rr) a += cluster.map_shared_rank(&mypart[buf][0], rr)[j];
       LL<T>::put(ll + LL<T>::kWords * ((size_t)(buf * Q + q) * w + j), a, ep);
     }
-    const int wc = w - c, cnt = Q * wc;
     MG_T(1);
-    ll_gather<T>(ll, buf, Q, w, c, wc, cnt, ep, cval, tid);
-    MG_T(2);
-    __syncthreads();
-    for (int j = c + tid; j < w; j += kMgsThreads) {
-      T a = T(0);
-      for (int qq = 0; qq < Q; ++qq) a += cval[qq * w + j];
-      gsum[j] = a;
+    if (Q <= 32 && !mgs_two_pass) {
+      ll_gather_sum<T>(ll, buf, Q, w, c, ep, gsum, tid);
+      MG_T(2);
+    } else {
+      const int wc = w - c, cnt = Q * wc;
+      ll_gather<T>(ll, buf, Q, w, c, wc, cnt, ep, cval, tid);
+      MG_T(2);
+      __syncthreads();
+      for (int j = c + tid; j < w; j += kMgsThreads) {
+        T a = T(0);
+        for (int qq = 0; qq < Q; ++qq) a += cval[qq * w + j];
+        gsum[j] = a;
+      }
     }
     __syncthreads();
     MG_T(3);
@@ -745,6 +783,14 @@ static bool mgs_cooperative() {
 // shared-memory one (the panel rows + exchange buffers within 220 KB per CTA).
 // rows per thread of the LL kernel (SF_MGS_RPT: 64 = all in registers, 128 = half in shared
 // memory: twice the rows per CTA, half the CTAs)
+// SF_MGS_TWO_PASS (default 1): the gather spreads the Q x (w - c) words over all threads,
+// stages them, then sums per column.  0: one pass, thread t polls and sums column c + t
+// (measured slower: 3.0 vs 1.4 us per column in the gather — half the threads idle, twice the
+// words per poller; cfg4 80.8 vs 76.4 ms).
+static int mgs_two_pass() {
+  static const int v = [] { const char* e = getenv("SF_MGS_TWO_PASS"); return e ? atoi(e) : 1; }();
+  return v;
+}
 static int mgs_rpt() {
   static const int v = [] { const char* e = getenv("SF_MGS_RPT"); return (e && atoi(e) == 128) ? 128 : 64; }();
   return v;
@@ -853,11 +899,14 @@ cudaError_t qr_mgs_panel(int64_t n, int w, const T* src, int64_t lds, T* dst, in
     int RB = lg.RB;
     count_launch();
     if (lreg && mgs_rpt() == 64 && mgs_nr() == 32)
-      return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 64, 32>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
+      return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 64, 32>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail,
+                                mgs_two_pass());
     if (lreg && mgs_rpt() == 64)
-      return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 64, 64>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
+      return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 64, 64>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail,
+                                mgs_two_pass());
     if (lreg)
-      return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 128, 64>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
+      return cudaLaunchKernelEx(&cfg, qr_mgs_ll_kernel<T, 128, 64>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail,
+                                mgs_two_pass());
     return cudaLaunchKernelEx(&cfg, qr_mgs_ll_smem_kernel<T>, n, w, RB, src, lds, dst, ldd, col0, tol, ll, fail);
   }
   MgsGeom g = mgs_geom(n, w, (int)sizeof(T));
