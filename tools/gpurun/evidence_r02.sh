@@ -3,6 +3,7 @@
 # oracle baseline; the reference arm), the launch list of the default step, ncu --set full of
 # the flush kernels of every config (their DRAM traffic feeds profiles/traffic.json).
 mkdir -p gpurun_out/ev
+rm -f gpurun_out/ev/*
 O=gpurun_out/ev
 timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1
