@@ -598,6 +598,226 @@ static cudaError_t splitk_reduce(const GemmF64& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------
+// K1s — chunked short-K flush (K <= 64, in place, no mask; DESIGN.md §5 K1s).  The LU flush
+// at s = 64 (A[c:n,c:n] -= R_L R_U with K = s) is 1 MFLOP per 128x64 tile:
+// with one tile per CTA the operand fill and the epilogue are as long as the 2048 DMMAs.
+// Here a CTA owns a CHUNK of consecutive tiles of one row block: the 128 x K block of R_L is
+// loaded ONCE (bulk copies, mbarrier-tracked), the K x 64 blocks of R_U stream through a
+// double buffer, and the result of tile t is added to C in L2 by bulk reductions issued by a
+// producer warp while the 8 consumer warps already run the DMMAs of tile t+1.  No CTA-wide
+// barrier in the main loop: consumers and producer meet only on mbarriers.
+//   warps 0-7 : consumers, 4 (i) x 2 (j), warp tile 32 x 32 (4 x 4 DMMA atoms)
+//   warp 8    : producer (operand bulk copies, C bulk reductions)
+// Every element gets the same DMMA chain as gemm_f64_kernel (k in ascending groups of 4,
+// accumulator from 0, then C + (-acc) by the bulk reduction): bitwise the same result.
+namespace g64s {
+constexpr int BM = 128, BN = 64, KMAX = 64, NCW = 8, NT = (NCW + 1) * 32;
+constexpr int PA = BM + 4;     // As[k*PA + i]   (idx-contiguous rows, == 4 mod 16 doubles)
+constexpr int PB = KMAX + 4;   // Bs[j*PB + k]   (k-contiguous rows)
+constexpr int CP = BM + 2;     // Cs[j*CP + i]   (staging for the column bulk reductions)
+constexpr size_t A_BYTES = sizeof(double) * KMAX * PA;
+constexpr size_t B_BYTES = sizeof(double) * BN * PB;
+constexpr size_t C_BYTES = sizeof(double) * BN * CP;
+constexpr size_t SMEM = A_BYTES + 2 * B_BYTES + C_BYTES + 64;
+static_assert(SMEM <= 227 * 1024, "one CTA per SM");
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+}  // namespace g64s
+
+// C[i0:i0+rows, j] += alpha * sum_k A[i, k] B[k, j]   (A idx-contiguous, B k-contiguous)
+__global__ void __launch_bounds__(g64s::NT, 1) gemm_f64_chunk_kernel(GemmF64 p, int TN, int chunk, int cpr) {
+  using namespace g64s;
+  extern __shared__ __align__(128) unsigned char g64s_raw[];
+  double* As = reinterpret_cast<double*>(g64s_raw);
+  double* Bs = reinterpret_cast<double*>(g64s_raw + A_BYTES);   // [2][BN * PB]
+  double* Cs = reinterpret_cast<double*>(g64s_raw + A_BYTES + 2 * B_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(g64s_raw + A_BYTES + 2 * B_BYTES + C_BYTES);
+  uint64_t* full = bars;        // [2] operands of the tile in B buffer b have landed
+  uint64_t* empty = bars + 2;   // [2] the consumers are done reading B buffer b
+  uint64_t* parked = bars + 4;  // the tile's result is in Cs
+  uint64_t* stgfree = bars + 5; // the bulk reductions have read Cs
+  __shared__ int skip;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    skip = (p.fail && failed(p.fail)) ? 1 : 0;   // one CTA-uniform decision
+    mb_init(&full[0], 1); mb_init(&full[1], 1);
+    mb_init(&empty[0], NCW); mb_init(&empty[1], NCW);
+    mb_init(parked, NCW); mb_init(stgfree, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (skip) return;
+  const int ti = (int)blockIdx.x / cpr, tj0 = ((int)blockIdx.x % cpr) * chunk;
+  const int T = (TN - tj0 < chunk) ? TN - tj0 : chunk;
+  const int64_t i0 = (int64_t)ti * BM;
+  const int rows = (p.M - i0 < BM) ? (int)(p.M - i0) : BM;   // even (launcher: M even)
+  const int K = (int)p.K;                                       // multiple of 4, <= KMAX
+  auto cols_of = [&](int t) {
+    const int64_t j0 = (int64_t)(tj0 + t) * BN;
+    return (p.N - j0 < BN) ? (int)(p.N - j0) : BN;
+  };
+
+  if (warp == NCW) {   // ---------------- producer
+    // tile t's R_U block into B buffer t & 1 (tile 0: together with the R_L block)
+    auto load = [&](int t) {
+      const int b = t & 1, cols = cols_of(t);
+      const int64_t j0 = (int64_t)(tj0 + t) * BN;
+      const uint32_t abytes = t == 0 ? (uint32_t)(K * rows * 8) : 0u;
+      if (lane == 0) mb_expect_tx(&full[b], abytes + (uint32_t)(cols * K * 8));
+      __syncwarp();
+      if (t == 0)
+        for (int k = lane; k < K; k += 32) bulk_g2s(As + k * PA, p.A + i0 + (int64_t)k * p.lda, rows * 8, &full[0]);
+      for (int j = lane; j < cols; j += 32) bulk_g2s(Bs + b * (BN * PB) + j * PB, p.B + (j0 + j) * p.ldb, K * 8, &full[b]);
+    };
+    load(0);
+    if (T > 1) load(1);
+    for (int t = 0; t < T; ++t) {
+      if (t + 2 < T) {
+        mb_wait(&empty[t & 1], (t >> 1) & 1);
+        load(t + 2);
+      }
+      mb_wait(parked, t & 1);
+      const int cols = cols_of(t);
+      const int64_t j0 = (int64_t)(tj0 + t) * BN;
+      for (int j = lane; j < cols; j += 32) bulk_reduce_add_f64(p.C + i0 + (j0 + j) * p.ldc, Cs + j * CP, rows * 8);
+      bulk_commit();
+      bulk_wait_read0();
+      __syncwarp();
+      if (lane == 0) mb_arrive(stgfree);
+    }
+    bulk_wait_all();
+    return;
+  }
+  // ---------------- consumers
+  const int wm = warp & 3, wn = warp >> 2, q = lane & 3, r = lane >> 2;
+  const int nk = K / 4;
+  const double alpha = p.alpha;
+  const bool neg = alpha == -1.0;
+  for (int t = 0; t < T; ++t) {
+    const int b = t & 1;
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+    mb_wait(&full[b], (t >> 1) & 1);
+    const double* bs = Bs + b * (BN * PB) + (wn * 32 + r) * PB + q;
+    const double* as = As + q * PA + wm * 32 + 2 * r;
+#pragma unroll
+    for (int kk = 0; kk < KMAX / 4; ++kk) {
+      if (kk >= nk) break;
+      double fa[4], fb[4];
+#pragma unroll
+      for (int b2 = 0; b2 < 2; ++b2) {
+        // paired atoms: atom 2b2 row r = logical row 16 b2 + 2r, atom 2b2+1 = 16 b2 + 2r + 1
+        const double2 v = *reinterpret_cast<const double2*>(as + kk * 4 * PA + 16 * b2);
+        fa[2 * b2] = v.x; fa[2 * b2 + 1] = v.y;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) fb[c] = bs[c * 8 * PB + kk * 4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dmma_8x8x4(acc[a][c][0], acc[a][c][1], fb[c], fa[a]);
+    }
+    __syncwarp();
+    if (lane == 0) mb_arrive(&empty[b]);
+    if (t > 0) mb_wait(stgfree, (t - 1) & 1);
+    // park alpha * acc (D = C^T: MMA row = j, MMA column = i); alpha = -1 is a sign flip
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int jl = wn * 32 + 8 * c + r;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int il = wm * 32 + 16 * (a >> 1) + 2 * (2 * q + e) + (a & 1);
+          const double v = acc[a][c][e];
+          Cs[jl * CP + il] =
+              neg ? __longlong_as_double(__double_as_longlong(v) ^ (long long)0x8000000000000000ULL) : alpha * v;
+        }
+      }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mb_arrive(parked);
+  }
+}
+
+// SF_DMMA_CHUNK=0 disables K1s; SF_DMMA_CHUNK_MIN = fewest tiles for which it is used;
+// SF_DMMA_CHUNK_T = fixed chunk length (tiles per CTA)
+static bool chunk_on() {
+  static const int on = [] { const char* e = getenv("SF_DMMA_CHUNK"); return e ? atoi(e) : 0; }();
+  return on != 0;
+}
+static int chunk_min_tiles() {
+  static const int v = [] { const char* e = getenv("SF_DMMA_CHUNK_MIN"); return e ? atoi(e) : 444; }();
+  return v;
+}
+static int chunk_fixed() {
+  static const int v = [] { const char* e = getenv("SF_DMMA_CHUNK_T"); return e ? atoi(e) : 0; }();
+  return v;
+}
+
+// true if gemm_f64_chunk_kernel serves this product
+static bool chunk_eligible(const GemmF64& p, int a_kcontig, int b_kcontig, int mask) {
+  if (!chunk_on() || mask != kMaskNone || p.splits != 1 || p.max_ctas > 0 || a_kcontig || !b_kcontig) return false;
+  if (p.K <= 0 || p.K > g64s::KMAX || (p.K & 3) || (p.M & 1) || !p.beta || p.Cin != p.C || p.ldcin != p.ldc)
+    return false;
+  auto al = [](const void* q, int64_t ld) { return (((uintptr_t)q) & 15) == 0 && (ld % 2) == 0; };
+  if (!al(p.A, p.lda) || !al(p.B, p.ldb) || !al(p.C, p.ldc)) return false;
+  const int64_t tiles = ((p.M + g64s::BM - 1) / g64s::BM) * ((p.N + g64s::BN - 1) / g64s::BN);
+  return tiles >= chunk_min_tiles();
+}
+
+static cudaError_t launch_chunk(const GemmF64& p, cudaStream_t st) {
+  const int TM = (int)((p.M + g64s::BM - 1) / g64s::BM), TN = (int)((p.N + g64s::BN - 1) / g64s::BN);
+  // about two waves of one-CTA-per-SM chunks; chunks of a row balanced to equal length
+  int chunk = chunk_fixed();
+  if (chunk <= 0) chunk = (int)(((int64_t)TM * TN + 2 * 148 - 1) / (2 * 148));
+  if (chunk < 1) chunk = 1;
+  if (chunk > TN) chunk = TN;
+  const int cpr = (TN + chunk - 1) / chunk;
+  chunk = (TN + cpr - 1) / cpr;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_f64_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)g64s::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  gemm_f64_chunk_kernel<<<TM * cpr, g64s::NT, g64s::SMEM, st>>>(p, TN, chunk, cpr);
+  count_launch();
+  return cudaGetLastError();
+}
+
 static bool short_k_wide() {
   static const int on = [] { const char* e = getenv("SF_GEMM_SHORTK8"); return e ? atoi(e) : 1; }();
   return on != 0;
@@ -758,6 +978,7 @@ cudaError_t gemm_f64(GemmF64 p, int a_kcontig, int b_kcontig, int mask, cudaStre
     p.K = 0;
   }
   if (p.splits < 1) p.splits = 1;
+  if (chunk_eligible(p, a_kcontig, b_kcontig, mask)) return launch_chunk(p, st);
   {
     const int var = dmma_variant_for(p.K);
     if (var > 0 && p.max_ctas == 0 && p.K > 0) {
