@@ -91,6 +91,40 @@ __device__ __forceinline__ void load_slice(double* Xs, const double* __restrict_
   }
 }
 
+// The same slice for a tile that lies wholly inside the operand and the K range (no zero
+// fill): `g` is this thread's first 16-byte chunk in global memory, `xs` its place in the
+// slot; the thread's other chunks sit at compile-time row steps from both.  A handful of
+// integer instructions per stage instead of the generic path's per-chunk index / bound /
+// address arithmetic, which each warp otherwise executes between its DMMA groups.
+template <int NIDX, bool KC, int NT>
+constexpr bool slice_full_ok() { return KC ? NT % (g64::BK / 2) == 0 : NT % (NIDX / 2) == 0; }
+template <int NIDX, bool KC, int NT>
+__device__ __forceinline__ void load_slice_full(double* xs, const double* __restrict__ g, int64_t ld) {
+  using namespace g64;
+  using S = Slice<NIDX>;
+  constexpr int RS = KC ? NT / (BK / 2) : NT / (NIDX / 2);   // rows (idx | k) between a thread's chunks
+  static_assert(slice_full_ok<NIDX, KC, NT>(), "chunk rows");
+  const unsigned sb = (unsigned)__cvta_generic_to_shared(xs);
+#pragma unroll
+  for (int r = 0; r < S::template chunks<NT>(); ++r) {
+    const unsigned d = sb + (unsigned)(r * RS * (KC ? PAD_KI : S::PAD_IK) * sizeof(double));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(g + (int64_t)(r * RS) * ld));
+  }
+}
+// this thread's first chunk of the slice at (idx0, k0): offset in the operand / in the slot
+template <int NIDX, bool KC, int NT>
+__device__ __forceinline__ int64_t slice_goff(int64_t ld, int64_t idx0, int64_t k0, int tid) {
+  using namespace g64;
+  if (!KC) return idx0 + 2 * (tid % (NIDX / 2)) + (k0 + tid / (NIDX / 2)) * ld;
+  return k0 + 2 * (tid % (BK / 2)) + (idx0 + tid / (BK / 2)) * ld;
+}
+template <int NIDX, bool KC, int NT>
+__device__ __forceinline__ int slice_soff(int tid) {
+  using namespace g64;
+  if (!KC) return (tid / (NIDX / 2)) * Slice<NIDX>::PAD_IK + 2 * (tid % (NIDX / 2));
+  return (tid / (BK / 2)) * PAD_KI + 2 * (tid % (BK / 2));
+}
+
 template <int NIDX, bool KC>
 __device__ __forceinline__ double frag(const double* Xs, int base, int kk, int lane) {
   using namespace g64;
@@ -372,12 +406,28 @@ __device__ __forceinline__ void gemm_f64_body2(const GemmF64& p, int bid, int ve
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
+  // interior tiles (all of the big flushes but their last tile row / column): running
+  // per-thread source pointers, see load_slice_full
+  constexpr bool FULL_OK = slice_full_ok<BM, AK, NT>() && slice_full_ok<64, BKC, NT>();
+  const bool full = FULL_OK && V16 && i0 + BM <= p.M && j0 + 64 <= p.N;
+  const double* ga = p.A + slice_goff<BM, AK, NT>(p.lda, i0, kbeg, tid);
+  const double* gb = p.B + slice_goff<64, BKC, NT>(p.ldb, j0, kbeg, tid);
+  const int soa = slice_soff<BM, AK, NT>(tid), sob = slice_soff<64, BKC, NT>(tid);
   auto issue = [&](int kb) {
     if (kb < nk) {
       const int slot = kb % STAGES;
       const int64_t k0 = kbeg + (int64_t)kb * BK;
-      load_slice<BM, AK, V16, NT>(As + slot * SA, p.A, p.lda, i0, p.M, k0, kend, tid);
-      load_slice<64, BKC, V16, NT>(Bs + slot * SB, p.B, p.ldb, j0, p.N, k0, kend, tid);
+      if (full && k0 + BK <= kend) {
+        if constexpr (FULL_OK) {
+          load_slice_full<BM, AK, NT>(As + slot * SA + soa, ga, p.lda);
+          load_slice_full<64, BKC, NT>(Bs + slot * SB + sob, gb, p.ldb);
+        }
+      } else {
+        load_slice<BM, AK, V16, NT>(As + slot * SA, p.A, p.lda, i0, p.M, k0, kend, tid);
+        load_slice<64, BKC, V16, NT>(Bs + slot * SB, p.B, p.ldb, j0, p.N, k0, kend, tid);
+      }
+      ga += AK ? (int64_t)BK : (int64_t)BK * p.lda;    // issue() runs for kb = 0, 1, 2, ... in order
+      gb += BKC ? (int64_t)BK : (int64_t)BK * p.ldb;
     }
     cp_async_commit();
   };
