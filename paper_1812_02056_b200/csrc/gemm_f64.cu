@@ -193,12 +193,29 @@ __device__ __forceinline__ void gemm_f64_body(const GemmF64& p, int bid, int vec
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
+  // interior tiles: running per-thread source pointers (load_slice_full)
+  // (not for the lower-masked instantiation: it only serves SYRK flushes with K <= 64, where
+  // the pointer set-up cost more than it saved: m = 16384, K = 64 0.783 -> 0.842 ms)
+  constexpr bool FULL_OK = slice_full_ok<BM, AK, NT>() && slice_full_ok<BN, BKC, NT>() && MASK != kMaskLower;
+  const bool full = FULL_OK && V16 && i0 + BM <= p.M && j0 + BN <= p.N;
+  const double* ga = p.A + slice_goff<BM, AK, NT>(p.lda, i0, kbeg, tid);
+  const double* gb = p.B + slice_goff<BN, BKC, NT>(p.ldb, j0, kbeg, tid);
+  const int soa = slice_soff<BM, AK, NT>(tid), sob = slice_soff<BN, BKC, NT>(tid);
   auto issue = [&](int kb) {
     if (kb < nk) {
       const int slot = kb % STAGES;
       const int64_t k0 = kbeg + (int64_t)kb * BK;
-      load_slice<BM, AK, V16, NT>(As + slot * OPER_A, p.A, p.lda, i0, p.M, k0, kend, tid);
-      load_slice<BN, BKC, V16, NT>(Bs + slot * OPER_B, p.B, p.ldb, j0, p.N, k0, kend, tid);
+      if (full && k0 + BK <= kend) {
+        if constexpr (FULL_OK) {
+          load_slice_full<BM, AK, NT>(As + slot * OPER_A + soa, ga, p.lda);
+          load_slice_full<BN, BKC, NT>(Bs + slot * OPER_B + sob, gb, p.ldb);
+        }
+      } else {
+        load_slice<BM, AK, V16, NT>(As + slot * OPER_A, p.A, p.lda, i0, p.M, k0, kend, tid);
+        load_slice<BN, BKC, V16, NT>(Bs + slot * OPER_B, p.B, p.ldb, j0, p.N, k0, kend, tid);
+      }
+      ga += AK ? (int64_t)BK : (int64_t)BK * p.lda;    // issue() runs for kb = 0, 1, 2, ... in order
+      gb += BKC ? (int64_t)BK : (int64_t)BK * p.ldb;
     }
     cp_async_commit();
   };
